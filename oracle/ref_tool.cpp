@@ -1,0 +1,193 @@
+// ref_tool.cpp -- TEST INFRASTRUCTURE ONLY.
+//
+// Thin driver around the UNMODIFIED reference headers
+// (/root/reference/proj/include/prag/annindex.hpp, perfmodel.hpp), compiled by
+// oracle/Makefile with the reference's own CMake Release flags into
+// oracle/_ref/ref_tool. It is used (a) to generate the golden fixtures in
+// tests/golden/ with the reference's own train_index/store_index/search, and
+// (b) as the CPU baseline / `bench.py --impl reference` arm, timing
+// prag::search on indexes loaded with prag::load_index (as every reference
+// tool does: perfmodel_main.cpp:49). No reference source is copied here.
+//
+// Commands:
+//   train   <vectors.f32> <n> <d> <nlist> <nsq> <seed> <out.pragix>
+//   search  <index> <queries.f32> <nq> <nprobe> <k> <out.bin>
+//   bench   <index> <queries.f32> <nq> <nprobe> <k> <threads> <reps> <warmups> [max_seconds]
+//   calibrate <index> <queries.f32> <nq> <k> <grid_csv> <repeats>
+//   brute   <vectors.f32> <n> <d> <queries.f32> <nq> <k> <out.bin>
+#include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <fstream>
+#include <iostream>
+#include <sstream>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "prag/annindex.hpp"
+#include "prag/perfmodel.hpp"
+
+namespace {
+
+std::vector<float> read_f32(const std::string& path, std::size_t count) {
+    std::vector<float> v(count);
+    std::ifstream is(path, std::ios::binary);
+    if (!is) throw std::runtime_error("cannot open " + path);
+    is.read(reinterpret_cast<char*>(v.data()), count * sizeof(float));
+    if (!is) throw std::runtime_error("short read " + path);
+    return v;
+}
+
+std::vector<std::vector<float>> rows(const std::vector<float>& flat, std::size_t n, std::size_t d) {
+    std::vector<std::vector<float>> out(n, std::vector<float>(d));
+    for (std::size_t i = 0; i < n; ++i)
+        for (std::size_t j = 0; j < d; ++j) out[i][j] = flat[i * d + j];
+    return out;
+}
+
+// Result file: per query u32 count, u32 scanned_lists, u64 scanned_vectors,
+// then k x (u64 id, f32 dist), unused slots zero.
+void write_results(const std::string& path, const std::vector<prag::SearchResult>& res, std::uint32_t k) {
+    std::ofstream os(path, std::ios::binary);
+    for (const auto& r : res) {
+        std::uint32_t count = static_cast<std::uint32_t>(r.neighbors.size());
+        os.write(reinterpret_cast<const char*>(&count), 4);
+        os.write(reinterpret_cast<const char*>(&r.scanned_lists), 4);
+        os.write(reinterpret_cast<const char*>(&r.scanned_vectors), 8);
+        for (std::uint32_t i = 0; i < k; ++i) {
+            std::uint64_t id = i < count ? r.neighbors[i].chunk_id : 0;
+            float dist = i < count ? r.neighbors[i].distance : 0.0f;
+            os.write(reinterpret_cast<const char*>(&id), 8);
+            os.write(reinterpret_cast<const char*>(&dist), 4);
+        }
+    }
+}
+
+double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+    if (argc < 2) {
+        std::cerr << "usage: ref_tool train|search|bench|calibrate|brute ...\n";
+        return 2;
+    }
+    std::string cmd = argv[1];
+    try {
+        if (cmd == "train" && argc == 9) {
+            std::size_t n = std::stoull(argv[3]);
+            std::uint32_t d = std::stoul(argv[4]);
+            prag::TrainParams params;
+            params.nlist = std::stoul(argv[5]);
+            params.n_subquantizers = std::stoul(argv[6]);
+            params.seed = std::stoull(argv[7]);
+            auto vecs = rows(read_f32(argv[2], n * d), n, d);
+            auto [index, codebook] = prag::train_index(vecs, params);
+            prag::store_index(index, codebook, argv[8]);
+            return 0;
+        }
+        if (cmd == "search" && argc == 8) {
+            auto [index, codebook] = prag::load_index(argv[2]);
+            std::size_t nq = std::stoull(argv[4]);
+            std::uint32_t nprobe = std::stoul(argv[5]), k = std::stoul(argv[6]);
+            auto qs = rows(read_f32(argv[3], nq * index.d), nq, index.d);
+            std::vector<prag::SearchResult> res;
+            for (const auto& q : qs) res.push_back(prag::search(index, codebook, q, {nprobe, k, false}));
+            write_results(argv[7], res, k);
+            return 0;
+        }
+        if (cmd == "brute" && argc == 9) {
+            std::size_t n = std::stoull(argv[3]);
+            std::uint32_t d = std::stoul(argv[4]);
+            std::size_t nq = std::stoull(argv[6]);
+            std::uint32_t k = std::stoul(argv[7]);
+            auto vecs = rows(read_f32(argv[2], n * d), n, d);
+            auto qs = rows(read_f32(argv[5], nq * d), nq, d);
+            std::vector<prag::SearchResult> res;
+            for (const auto& q : qs) res.push_back(prag::brute_force_search(vecs, q, k));
+            write_results(argv[8], res, k);
+            return 0;
+        }
+        if (cmd == "bench" && (argc == 10 || argc == 11)) {
+            double t_load0 = now_s();
+            auto [index, codebook] = prag::load_index(argv[2]);
+            double t_load = now_s() - t_load0;
+            std::size_t nq = std::stoull(argv[4]);
+            std::uint32_t nprobe = std::stoul(argv[5]), k = std::stoul(argv[6]);
+            int threads = std::stoi(argv[7]), reps = std::stoi(argv[8]), warm = std::stoi(argv[9]);
+            double max_s = argc == 11 ? std::stod(argv[10]) : 1e30;
+            if (threads <= 0) threads = static_cast<int>(std::thread::hardware_concurrency());
+            auto qs = rows(read_f32(argv[3], nq * index.d), nq, index.d);
+            std::vector<double> times;
+            std::uint64_t scanned = 0;
+            double t_begin = now_s();
+            for (int r = 0; r < warm + reps; ++r) {
+                std::atomic<std::size_t> next{0};
+                std::atomic<std::uint64_t> sc{0};
+                double t0 = now_s();
+                std::vector<std::thread> pool;
+                for (int t = 0; t < threads; ++t) {
+                    pool.emplace_back([&] {
+                        for (;;) {
+                            std::size_t q = next.fetch_add(1);
+                            if (q >= nq) break;
+                            auto res = prag::search(index, codebook, qs[q], {nprobe, k, false});
+                            sc += res.scanned_vectors;
+                        }
+                    });
+                }
+                for (auto& th : pool) th.join();
+                double dt = now_s() - t0;
+                if (r >= warm) times.push_back(dt);
+                scanned = sc.load();
+                if (r >= warm && now_s() - t_begin > max_s) break;
+            }
+            std::vector<double> sorted = times;
+            std::sort(sorted.begin(), sorted.end());
+            double p50 = sorted[sorted.size() / 2];
+            std::printf("{\"nq\": %zu, \"nprobe\": %u, \"k\": %u, \"threads\": %d, \"reps\": %zu, "
+                        "\"p50_s\": %.9g, \"best_s\": %.9g, \"qps\": %.6g, \"scanned_vectors\": %llu, "
+                        "\"load_s\": %.4g}\n",
+                        nq, nprobe, k, threads, times.size(), p50, sorted.front(), nq / p50,
+                        static_cast<unsigned long long>(scanned), t_load);
+            return 0;
+        }
+        if (cmd == "calibrate" && argc == 8) {
+            // perfmodel_main.cpp:57-70 protocol: per-query seconds, sequential.
+            auto [index, codebook] = prag::load_index(argv[2]);
+            std::size_t nq = std::stoull(argv[4]);
+            std::uint32_t k = std::stoul(argv[5]);
+            int repeats = std::stoi(argv[7]);
+            auto qs = rows(read_f32(argv[3], nq * index.d), nq, index.d);
+            std::vector<std::uint32_t> grid;
+            std::stringstream ss(argv[6]);
+            std::string item;
+            while (std::getline(ss, item, ',')) grid.push_back(std::stoul(item));
+            auto measure = [&](std::uint32_t nprobe) {
+                prag::Stopwatch clock;
+                for (const auto& q : qs) prag::search(index, codebook, q, {nprobe, k, false});
+                return clock.elapsed_s() / qs.size();
+            };
+            auto model = prag::calibrate_retrieval(measure, grid, repeats);
+            std::printf("{\"slope_s\": %.9g, \"intercept_s\": %.9g, \"fit_residual_s\": %.9g, \"clamped\": %s}\n",
+                        model.slope_s, model.intercept_s, model.fit_residual_s,
+                        model.clamped ? "true" : "false");
+            return 0;
+        }
+    } catch (const prag::ConfigError& e) {
+        std::cerr << "ConfigError: " << e.what() << "\n";
+        return 3;
+    } catch (const prag::FormatError& e) {
+        std::cerr << "FormatError: " << e.what() << "\n";
+        return 4;
+    } catch (const std::exception& e) {
+        std::cerr << "error: " << e.what() << "\n";
+        return 1;
+    }
+    std::cerr << "bad arguments\n";
+    return 2;
+}
