@@ -1,0 +1,185 @@
+/*
+ * prag_gpu.h -- C ABI of the B200-native IVF-PQ retrieval hot path.
+ *
+ * Drop-in boundary for PipeRAG's retriever path. The reference has no FFI:
+ * its extension point is the abstract C++ class prag::Retriever
+ * (/root/reference/proj/include/prag/pipeline.hpp:200-208) wrapping the free
+ * function prag::search (annindex.hpp:262-315) and the performance model
+ * (perfmodel.hpp:92-157). Each entry point below names the reference
+ * interface it replaces; include/prag_gpu.hpp wraps them back into the
+ * reference's C++ shapes (SearchResult, Retriever) and INTEGRATION.md shows
+ * the binding a maintainer adds.
+ *
+ * Conventions
+ *  - Every function returns int status: 0 OK, 1 CONFIG (reference ConfigError),
+ *    2 FORMAT (reference FormatError), 3 CUDA, 4 NCCL, 5 OOM, 6 NO_DEVICE.
+ *    prag_gpu_last_error() returns the thread-local message of the last
+ *    failure, worded like the reference's exception text.
+ *  - Plain pointers and sizes only. Query/result pointers may be host or
+ *    device memory (detected per pointer). With any host output the call
+ *    returns only after results are in host memory; with all-device outputs
+ *    the call is asynchronous on `stream` (a cudaStream_t, NULL = legacy).
+ *  - The index is immutable after load; concurrent prag_gpu_search calls on
+ *    different streams are safe (per-call workspaces from a pool).
+ *  - There is no CPU fallback: without a CUDA device every compute entry
+ *    point fails with status 6.
+ */
+#ifndef PRAG_GPU_H
+#define PRAG_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    PRAG_GPU_OK = 0,
+    PRAG_GPU_CONFIG = 1,
+    PRAG_GPU_FORMAT = 2,
+    PRAG_GPU_CUDA = 3,
+    PRAG_GPU_NCCL = 4,
+    PRAG_GPU_OOM = 5,
+    PRAG_GPU_NO_DEVICE = 6
+};
+
+typedef struct prag_gpu_index prag_gpu_index;
+
+/* Shape and placement of a loaded index (or one shard of it). */
+typedef struct prag_gpu_index_desc {
+    uint32_t nlist;           /* IvfIndex::nlist (annindex.hpp:22)                 */
+    uint32_t d;               /* IvfIndex::d                                       */
+    uint32_t nsq;             /* PqCodebook::n_subquantizers (m, bytes per code)    */
+    uint32_t sub_dim;         /* PqCodebook::sub_dim                               */
+    uint64_t ntotal;          /* entries resident on this device                   */
+    uint64_t ntotal_global;   /* entries in the whole index file                   */
+    uint32_t max_list_len;    /* longest resident list                             */
+    int32_t device;           /* CUDA ordinal                                      */
+    int32_t shard_rank;       /* 0 when unsharded                                  */
+    int32_t shard_world;      /* 1 when unsharded                                  */
+    uint64_t device_bytes;    /* HBM held by the index                             */
+    uint32_t code_layout;     /* 0 = plain [entry][m]; 1 = lane-skewed tiles (m=32,64) */
+    uint32_t reserved;
+} prag_gpu_index_desc;
+
+/* Fitted retrieval-latency line; same fields and meaning as
+ * prag::RetrievalPerfModel (perfmodel.hpp:19-26). */
+typedef struct prag_gpu_perf_model {
+    double slope_s;
+    double intercept_s;
+    double fit_residual_s;
+    int32_t clamped;
+    int32_t reserved;
+} prag_gpu_perf_model;
+
+/* Per-phase device time of the most recent search on an index with
+ * profiling enabled (CUDA events on the search stream), milliseconds. */
+typedef struct prag_gpu_timings {
+    float coarse_ms;   /* K1: queries x centroids exact distances          */
+    float select_ms;   /* K1b: per-query top-nprobe                         */
+    float plan_ms;     /* work-item plan (list sizes, prefix sums)          */
+    float scan_ms;     /* K2+K3+K4: fused LUT build + list scan + top-k      */
+    float final_ms;    /* per-query merge of partial top-k                  */
+    float total_ms;    /* first event to last event                         */
+    uint64_t scanned_bytes; /* algorithmic code bytes: sum scanned_vectors * m */
+    uint64_t work_items;
+} prag_gpu_timings;
+
+/* ---------------------------------------------------------------- errors */
+const char* prag_gpu_last_error(void);
+int prag_gpu_version(void);
+/* Number of visible CUDA devices (0 on a host without a GPU; never fails). */
+int prag_gpu_device_count(void);
+
+/* ---------------------------------------------------------------- index */
+/* Replaces prag::load_index (annindex.hpp:361-411): reads a PRAGIX01 file
+ * and builds the HBM-resident list-major layout on `device`. Errors carry the
+ * reference's FormatError wording and byte offsets. */
+int prag_gpu_index_load(const char* pragix01_path, int device, prag_gpu_index** out);
+
+/* Sharded load: keeps only the inverted lists that prag_gpu_plan_shards
+ * assigns to `rank` of `world`; centroids and codebook are replicated so
+ * every shard computes the identical probe set. */
+int prag_gpu_index_load_shard(const char* pragix01_path, int device, int rank, int world,
+                              prag_gpu_index** out);
+
+/* Builds an index from host arrays in the reference's logical layout:
+ * centroids[nlist][d], codewords[nsq][256][d/nsq], list_off[nlist+1] (entry
+ * offsets into ids/codes), ids[ntotal], codes[ntotal][nsq]
+ * (IvfIndex/PqCodebook, annindex.hpp:16-33, flattened). */
+int prag_gpu_index_from_host(uint32_t nlist, uint32_t d, uint32_t nsq, const float* centroids,
+                             const float* codewords, const uint64_t* list_off, const uint64_t* ids,
+                             const uint8_t* codes, int device, prag_gpu_index** out);
+
+void prag_gpu_index_free(prag_gpu_index* index);
+int prag_gpu_index_describe(const prag_gpu_index* index, prag_gpu_index_desc* out);
+/* IvfIndex::nlist, as prag::Retriever::nlist() (pipeline.hpp:207). */
+uint32_t prag_gpu_index_nlist(const prag_gpu_index* index);
+/* Resident list lengths (host array of nlist). */
+int prag_gpu_index_list_sizes(const prag_gpu_index* index, uint64_t* out_sizes);
+
+/* ---------------------------------------------------------------- search */
+/* Replaces prag::search(index, codebook, query, {nprobe, k, false})
+ * (annindex.hpp:262-315) for a batch of nq queries (row-major nq x d).
+ * Validation as annindex.hpp:265-268: k >= 1 and 1 <= nprobe <= nlist, else
+ * CONFIG. Outputs per query q: out_ids[q*k + i], out_dist[q*k + i] for
+ * i < out_count[q] = min(k, candidates), ascending (distance, chunk_id);
+ * out_scanned_vectors[q] = SearchResult::scanned_vectors (may be NULL).
+ * SearchResult::scanned_lists is always nprobe (annindex.hpp:284). */
+int prag_gpu_search(prag_gpu_index* index, const float* queries, uint32_t nq, uint32_t nprobe,
+                    uint32_t k, uint64_t* out_ids, float* out_dist, uint32_t* out_count,
+                    uint64_t* out_scanned_vectors, void* stream);
+
+/* Coarse quantizer only (annindex.hpp:277-281): the first nprobe lists of
+ * each query in (distance, list id) order, out_lists[q*nprobe + p]. */
+int prag_gpu_probe(prag_gpu_index* index, const float* queries, uint32_t nq, uint32_t nprobe,
+                   uint32_t* out_lists, float* out_dist, void* stream);
+
+/* ------------------------------------------------------ multi-GPU pieces */
+/* LPT placement of lists on `world` shards by bytes (|l| * m): lists in
+ * descending size (ties by lower id) each go to the least-loaded shard (ties
+ * by lower rank). Host-only; never touches a GPU. */
+int prag_gpu_plan_shards(const uint64_t* list_sizes, uint32_t nlist, uint32_t world,
+                         uint32_t* out_owner);
+
+/* Exact top-k of the union of `nparts` per-shard top-k lists, per query.
+ * Inputs device or host: ids/dist [nparts][nq][kin], count [nparts][nq];
+ * scanned [nparts][nq] summed into out_scanned (both may be NULL). */
+int prag_gpu_merge_topk(const uint64_t* ids, const float* dist, const uint32_t* count,
+                        const uint64_t* scanned, uint32_t nparts, uint32_t nq, uint32_t kin,
+                        uint32_t k, uint64_t* out_ids, float* out_dist, uint32_t* out_count,
+                        uint64_t* out_scanned, int device, void* stream);
+
+/* ------------------------------------------------- performance model */
+/* Replaces prag::calibrate_retrieval (perfmodel.hpp:92-117) fed with the GPU
+ * latency curve: for each nprobe in grid (sorted, deduplicated; >= 2 values,
+ * repeats >= 3), `warmups` untimed then `repeats` timed batch searches of the
+ * nq host queries; the median batch latency in seconds per point is fitted
+ * with least squares; negative coefficients are clamped to 0.
+ * If out_latency_s is non-NULL it receives the medians (one per unique
+ * grid value, ascending). */
+int prag_gpu_calibrate_retrieval(prag_gpu_index* index, const float* queries, uint32_t nq,
+                                 uint32_t k, const uint32_t* nprobe_grid, uint32_t grid_len,
+                                 int repeats, int warmups, prag_gpu_perf_model* out_model,
+                                 double* out_latency_s);
+
+/* Same fit over caller-supplied timings: `measure(nprobe, ctx)` returns
+ * seconds (the std::function hook of perfmodel.hpp:92). */
+typedef double (*prag_gpu_measure_fn)(uint32_t nprobe, void* ctx);
+int prag_gpu_calibrate_with(prag_gpu_measure_fn measure, void* ctx, const uint32_t* nprobe_grid,
+                            uint32_t grid_len, int repeats, int warmups,
+                            prag_gpu_perf_model* out_model);
+
+/* prag::select_nprobe (perfmodel.hpp:148-157). */
+uint32_t prag_gpu_select_nprobe(const prag_gpu_perf_model* model, double budget_s, uint32_t nlist,
+                                double safety_margin);
+
+/* ------------------------------------------------------------ profiling */
+int prag_gpu_set_profiling(prag_gpu_index* index, int enabled);
+int prag_gpu_last_timings(const prag_gpu_index* index, prag_gpu_timings* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PRAG_GPU_H */

@@ -1,0 +1,887 @@
+// capi.cu -- C ABI of the B200 IVF-PQ search path (include/prag_gpu.h):
+// index lifecycle (PRAGIX01 -> HBM layout), search orchestration on a CUDA
+// stream, shard planning/merge, and the GPU-fed performance model.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <memory>
+#include <numeric>
+
+#include "internal.h"
+
+namespace pg {
+
+static thread_local std::string g_error;
+void set_error(const std::string& msg) { g_error = msg; }
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+int require_device(int device) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        set_error("no CUDA device visible: the prag_gpu search path has no CPU fallback");
+        return PRAG_GPU_NO_DEVICE;
+    }
+    if (device < 0 || device >= n) {
+        set_error("CUDA device " + std::to_string(device) + " out of range (" + std::to_string(n) + " visible)");
+        return PRAG_GPU_CONFIG;
+    }
+    return PRAG_GPU_OK;
+}
+
+bool is_device_ptr(const void* p) {
+    if (p == nullptr) return false;
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+bool is_pinned_host(const void* p) {
+    cudaPointerAttributes a{};
+    if (p == nullptr || cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+template <typename T>
+int dmalloc(T** p, size_t n, uint64_t* acct) {
+    size_t bytes = std::max<size_t>(n * sizeof(T), 16);
+    PG_CUDA(cudaMalloc(reinterpret_cast<void**>(p), bytes));
+    if (acct) *acct += bytes;
+    return PRAG_GPU_OK;
+}
+
+void free_device_index(DeviceIndex& d) {
+    cudaFree(d.centroids);
+    cudaFree(d.centroidsT);
+    cudaFree(d.codewordsT);
+    cudaFree(d.list_off);
+    cudaFree(d.list_len);
+    cudaFree(d.ids);
+    cudaFree(d.codes);
+    d = DeviceIndex{};
+}
+
+// Host SoA (reference logical layout) -> HBM layout:
+//  centroids [nlist][d] and transposed [d][nlist]; codewords transposed to
+//  [nsq][sub_dim][256] so a warp building the ADC table reads consecutive
+//  codes; lists padded to multiples of kListPad entries, 16-byte aligned.
+int upload(prag_gpu_index* ix, const HostIndex& h) {
+    DeviceIndex& d = ix->dev;
+    d.nlist = h.nlist;
+    d.d = h.d;
+    d.nsq = h.nsq;
+    d.sub_dim = h.sub_dim;
+    const uint32_t nl = h.nlist;
+    std::vector<uint64_t> off(size_t(nl) + 1, 0);
+    std::vector<uint32_t> len(nl);
+    ix->host_list_len.assign(nl, 0);
+    uint32_t maxlen = 0;
+    for (uint32_t l = 0; l < nl; ++l) {
+        uint64_t n = h.list_off[l + 1] - h.list_off[l];
+        if (n >= (1ull << 32)) {
+            set_error("list " + std::to_string(l) + " exceeds 2^32 entries");
+            return PRAG_GPU_CONFIG;
+        }
+        len[l] = uint32_t(n);
+        ix->host_list_len[l] = n;
+        maxlen = std::max(maxlen, len[l]);
+        off[l + 1] = off[l] + (n + kListPad - 1) / kListPad * kListPad;
+    }
+    d.ntotal = h.list_off[nl];
+    d.npadded = off[nl];
+    d.max_list_len = maxlen;
+    if (d.npadded >= (1ull << 32)) {
+        set_error("more than 2^32 resident entries on one device; shard the index");
+        return PRAG_GPU_CONFIG;
+    }
+    std::vector<uint64_t> sorted(ix->host_list_len);
+    std::sort(sorted.begin(), sorted.end(), std::greater<uint64_t>());
+    ix->top_prefix.assign(size_t(nl) + 1, 0);
+    for (uint32_t i = 0; i < nl; ++i) ix->top_prefix[i + 1] = ix->top_prefix[i] + sorted[i];
+
+    uint64_t* acct = &ix->device_bytes;
+    PG_TRY(dmalloc(&d.centroids, size_t(nl) * h.d, acct));
+    PG_TRY(dmalloc(&d.centroidsT, size_t(nl) * h.d, acct));
+    PG_TRY(dmalloc(&d.codewordsT, size_t(h.nsq) * 256 * h.sub_dim, acct));
+    PG_TRY(dmalloc(&d.list_off, size_t(nl) + 1, acct));
+    PG_TRY(dmalloc(&d.list_len, nl, acct));
+    PG_TRY(dmalloc(&d.ids, d.npadded, acct));
+    PG_TRY(dmalloc(&d.codes, d.npadded * h.nsq, acct));
+
+    PG_CUDA(cudaMemcpy(d.centroids, h.centroids.data(), h.centroids.size() * 4, cudaMemcpyHostToDevice));
+    {
+        std::vector<float> t(size_t(nl) * h.d);
+        for (uint32_t c = 0; c < nl; ++c)
+            for (uint32_t j = 0; j < h.d; ++j) t[size_t(j) * nl + c] = h.centroids[size_t(c) * h.d + j];
+        PG_CUDA(cudaMemcpy(d.centroidsT, t.data(), t.size() * 4, cudaMemcpyHostToDevice));
+    }
+    {
+        std::vector<float> t(size_t(h.nsq) * 256 * h.sub_dim);
+        for (uint32_t s = 0; s < h.nsq; ++s)
+            for (uint32_t c = 0; c < 256; ++c)
+                for (uint32_t j = 0; j < h.sub_dim; ++j)
+                    t[(size_t(s) * h.sub_dim + j) * 256 + c] = h.codewords[(size_t(s) * 256 + c) * h.sub_dim + j];
+        PG_CUDA(cudaMemcpy(d.codewordsT, t.data(), t.size() * 4, cudaMemcpyHostToDevice));
+    }
+    PG_CUDA(cudaMemcpy(d.list_off, off.data(), off.size() * 8, cudaMemcpyHostToDevice));
+    PG_CUDA(cudaMemcpy(d.list_len, len.data(), len.size() * 4, cudaMemcpyHostToDevice));
+    {
+        // padded ids (pad = ~0) and codes (pad = 0), uploaded list by list group
+        std::vector<uint64_t> pid(d.npadded, ~0ull);
+        std::vector<uint8_t> pcode(d.npadded * h.nsq, 0);
+        for (uint32_t l = 0; l < nl; ++l) {
+            const uint64_t src = h.list_off[l], n = len[l];
+            std::memcpy(&pid[off[l]], &h.ids[src], n * 8);
+            std::memcpy(&pcode[off[l] * h.nsq], &h.codes[src * h.nsq], n * h.nsq);
+        }
+        PG_CUDA(cudaMemcpy(d.ids, pid.data(), pid.size() * 8, cudaMemcpyHostToDevice));
+        PG_CUDA(cudaMemcpy(d.codes, pcode.data(), pcode.size(), cudaMemcpyHostToDevice));
+    }
+    d.code_layout = 0;
+    return PRAG_GPU_OK;
+}
+
+int finish_load(std::unique_ptr<prag_gpu_index>& ix, HostIndex& h, int device, prag_gpu_index** out) {
+    DeviceGuard g(device);
+    ix->device = device;
+    ix->ntotal_global = h.ntotal_global ? h.ntotal_global : h.ids.size();
+    int rc = upload(ix.get(), h);
+    if (rc != PRAG_GPU_OK) {
+        free_device_index(ix->dev);
+        return rc;
+    }
+    *out = ix.release();
+    return PRAG_GPU_OK;
+}
+
+// ------------------------------------------------------------ workspace
+Workspace* acquire_ws(prag_gpu_index* ix, cudaStream_t s) {
+    std::lock_guard<std::mutex> lk(ix->mu);
+    for (Workspace* w : ix->pool) {
+        if (w->busy) continue;
+        if (w->last_stream == s || cudaEventQuery(w->done) == cudaSuccess) {
+            w->busy = true;
+            return w;
+        }
+    }
+    cudaGetLastError();
+    auto* w = new Workspace();
+    w->device = ix->device;
+    cudaEventCreateWithFlags(&w->done, cudaEventDisableTiming);
+    for (auto& e : w->ev) cudaEventCreate(&e);
+    w->busy = true;
+    ix->pool.push_back(w);
+    return w;
+}
+
+void release_ws(prag_gpu_index* ix, Workspace* w, cudaStream_t s) {
+    cudaEventRecord(w->done, s);
+    w->last_stream = s;
+    std::lock_guard<std::mutex> lk(ix->mu);
+    w->busy = false;
+}
+
+int ws_reserve(Workspace* w, size_t bytes, cudaStream_t s) {
+    if (w->buf_bytes >= bytes) return PRAG_GPU_OK;
+    if (w->buf) {
+        PG_CUDA(cudaStreamSynchronize(s));
+        cudaFree(w->buf);
+        w->buf = nullptr;
+        w->buf_bytes = 0;
+    }
+    size_t b = std::max(bytes, w->buf_bytes * 2);
+    if (cudaMalloc(&w->buf, b) != cudaSuccess) {
+        cudaGetLastError();
+        PG_CUDA(cudaMalloc(&w->buf, bytes));
+        b = bytes;
+    }
+    w->buf_bytes = b;
+    return PRAG_GPU_OK;
+}
+
+int ws_reserve_stage(Workspace* w, size_t bytes, cudaStream_t s) {
+    if (w->stage_bytes >= bytes) return PRAG_GPU_OK;
+    if (w->stage) {
+        PG_CUDA(cudaStreamSynchronize(s));
+        cudaFree(w->stage);
+        w->stage = nullptr;
+        w->stage_bytes = 0;
+    }
+    PG_CUDA(cudaMalloc(&w->stage, bytes));
+    w->stage_bytes = bytes;
+    return PRAG_GPU_OK;
+}
+
+int ws_reserve_host(Workspace* w, size_t bytes) {
+    if (w->host_bytes >= bytes) return PRAG_GPU_OK;
+    if (w->host) cudaFreeHost(w->host);
+    w->host = nullptr;
+    size_t b = std::max(bytes, w->host_bytes * 2);
+    PG_CUDA(cudaMallocHost(&w->host, b));
+    w->host_bytes = b;
+    return PRAG_GPU_OK;
+}
+
+struct Carver {
+    char* base;
+    size_t off = 0;
+    template <typename T>
+    T* take(size_t n) {
+        off = (off + 255) & ~size_t(255);
+        T* p = reinterpret_cast<T*>(base + off);
+        off += std::max<size_t>(n * sizeof(T), 16);
+        return p;
+    }
+};
+
+uint32_t pow2_at_least(uint64_t v) {
+    uint64_t p = 1;
+    while (p < v) p <<= 1;
+    return uint32_t(p);
+}
+
+int blocks_per_sm_scan(const prag_gpu_index* ix) {
+    const size_t lut = size_t(ix->dev.nsq) * 1024 + ((ix->dev.d + 3) & ~3u) * 4;
+    int per = lut <= 200 * 1024 ? int((228 * 1024) / (lut + 1024)) : 4;
+    return std::max(1, std::min(per, 8));
+}
+
+// One pass over nq (<= chunk) device-resident queries. Outputs are device
+// pointers. All launches on stream s.
+int search_pass(prag_gpu_index* ix, Workspace* w, const float* dq, uint32_t nq, uint32_t nprobe, uint32_t k,
+                uint64_t* o_ids, float* o_dist, uint32_t* o_count, uint64_t* o_scanned, cudaStream_t s,
+                prag_gpu_timings* tm) {
+    const DeviceIndex& d = ix->dev;
+    const uint64_t max_cand_q = ix->top_prefix[nprobe];
+    const uint64_t cand_cap = std::max<uint64_t>(1, max_cand_q * nq);
+    const uint32_t C = scan_chunk();
+    const uint64_t item_cap = uint64_t(nq) * (nprobe + (max_cand_q + C - 1) / C) + 1;
+    const uint32_t pw_p = pow2_at_least(nprobe);
+    const uint32_t pw_f = pow2_at_least(std::max<uint64_t>(1, std::min<uint64_t>(k, max_cand_q)));
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ix->device);
+    const int per_sm = blocks_per_sm_scan(ix);
+    const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>(item_cap, uint64_t(sms) * per_sm)));
+    const size_t lut_bytes = size_t(d.nsq) * 1024 + ((d.d + 3) & ~3u) * 4;
+    const bool glut = lut_bytes > 200 * 1024;
+
+    size_t need = 0;
+    {
+        Carver c{nullptr};
+        c.take<float>(size_t(nq) * d.nlist);
+        c.take<uint32_t>(size_t(nq) * nprobe);
+        c.take<float>(size_t(nq) * nprobe);
+        c.take<uint32_t>(size_t(nq) * pw_p);
+        c.take<uint64_t>(size_t(nq) * pw_p);
+        c.take<uint64_t>(size_t(nq) + 1);
+        c.take<uint4>(item_cap);
+        c.take<uint32_t>(2);
+        c.take<float>(cand_cap);
+        c.take<uint32_t>(cand_cap);
+        c.take<uint32_t>(size_t(nq) * pw_f);
+        c.take<uint64_t>(size_t(nq) * pw_f);
+        if (glut) c.take<float>(size_t(grid) * d.nsq * 256);
+        need = c.off + 256;
+    }
+    PG_TRY(ws_reserve(w, need, s));
+    Carver c{static_cast<char*>(w->buf)};
+    SearchBuffers b{};
+    b.queries = dq;
+    b.nq = nq;
+    b.nprobe = nprobe;
+    b.k = k;
+    b.out_ids = o_ids;
+    b.out_dist = o_dist;
+    b.out_count = o_count;
+    b.out_scanned = o_scanned;
+    b.coarse_dist = c.take<float>(size_t(nq) * d.nlist);
+    b.probe = c.take<uint32_t>(size_t(nq) * nprobe);
+    b.probe_dist = c.take<float>(size_t(nq) * nprobe);
+    uint32_t* pkey = c.take<uint32_t>(size_t(nq) * pw_p);
+    uint64_t* ptie = c.take<uint64_t>(size_t(nq) * pw_p);
+    b.q_cand_off = c.take<uint64_t>(size_t(nq) + 1);
+    b.items = c.take<uint4>(item_cap);
+    uint32_t* ctr = c.take<uint32_t>(2);
+    b.num_items = ctr;
+    b.item_cursor = ctr + 1;
+    b.cand_dist = c.take<float>(cand_cap);
+    b.cand_entry = c.take<uint32_t>(cand_cap);
+    uint32_t* fkey = c.take<uint32_t>(size_t(nq) * pw_f);
+    uint64_t* ftie = c.take<uint64_t>(size_t(nq) * pw_f);
+    float* gl = glut ? c.take<float>(size_t(grid) * d.nsq * 256) : nullptr;
+    b.item_cap = item_cap;
+    b.cand_cap = cand_cap;
+
+    const bool prof = tm != nullptr;
+    if (prof) cudaEventRecord(w->ev[0], s);
+    PG_TRY(launch_coarse(d, dq, nq, b.coarse_dist, s));
+    if (prof) cudaEventRecord(w->ev[1], s);
+    PG_TRY(launch_select_probe(d, b.coarse_dist, nq, nprobe, b.probe, b.probe_dist, pkey, ptie, s));
+    if (prof) cudaEventRecord(w->ev[2], s);
+    PG_TRY(launch_plan(d, b, s));
+    if (prof) cudaEventRecord(w->ev[3], s);
+    PG_TRY(launch_scan(d, b, s, grid, gl));
+    if (prof) cudaEventRecord(w->ev[4], s);
+    PG_TRY(launch_final(d, b, fkey, ftie, pw_f, s));
+    if (prof) {
+        cudaEventRecord(w->ev[5], s);
+        PG_CUDA(cudaEventSynchronize(w->ev[5]));
+        float t[5];
+        for (int i = 0; i < 5; ++i) cudaEventElapsedTime(&t[i], w->ev[i], w->ev[i + 1]);
+        float tot;
+        cudaEventElapsedTime(&tot, w->ev[0], w->ev[5]);
+        tm->coarse_ms += t[0];
+        tm->select_ms += t[1];
+        tm->plan_ms += t[2];
+        tm->scan_ms += t[3];
+        tm->final_ms += t[4];
+        tm->total_ms += tot;
+        std::vector<uint64_t> sc(nq);
+        PG_CUDA(cudaMemcpy(sc.data(), o_scanned, nq * 8, cudaMemcpyDeviceToHost));
+        for (uint64_t v : sc) tm->scanned_bytes += v * d.nsq;
+        uint32_t ni = 0;
+        PG_CUDA(cudaMemcpy(&ni, b.num_items, 4, cudaMemcpyDeviceToHost));
+        tm->work_items += ni;
+    }
+    return PRAG_GPU_OK;
+}
+
+int validate(const prag_gpu_index* ix, uint32_t nprobe, uint32_t k) {
+    if (k < 1) {  // annindex.hpp:265
+        set_error("search: k must be >= 1");
+        return PRAG_GPU_CONFIG;
+    }
+    if (nprobe < 1 || nprobe > ix->dev.nlist) {  // annindex.hpp:266-268
+        set_error("search: nprobe out of [1, nlist]");
+        return PRAG_GPU_CONFIG;
+    }
+    return PRAG_GPU_OK;
+}
+
+int do_search(prag_gpu_index* ix, const float* queries, uint32_t nq, uint32_t nprobe, uint32_t k,
+              uint64_t* out_ids, float* out_dist, uint32_t* out_count, uint64_t* out_scanned, cudaStream_t s) {
+    PG_TRY(validate(ix, nprobe, k));
+    if (nq == 0) return PRAG_GPU_OK;
+    if (!queries || !out_ids || !out_dist || !out_count) {
+        set_error("search: null query/output pointer");
+        return PRAG_GPU_CONFIG;
+    }
+    DeviceGuard g(ix->device);
+    const DeviceIndex& d = ix->dev;
+    const bool q_dev = is_device_ptr(queries);
+    const bool o_dev = is_device_ptr(out_ids) && is_device_ptr(out_dist) && is_device_ptr(out_count) &&
+                       (out_scanned == nullptr || is_device_ptr(out_scanned));
+    // Bound candidate memory: chunk the batch so a pass holds <= 192M slots.
+    const uint64_t max_cand_q = std::max<uint64_t>(1, ix->top_prefix[nprobe]);
+    const uint64_t kSlots = 192ull << 20;
+    const uint32_t chunk = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(nq, kSlots / max_cand_q)));
+
+    Workspace* w = acquire_ws(ix, s);
+    struct Rel {
+        prag_gpu_index* ix;
+        Workspace* w;
+        cudaStream_t s;
+        ~Rel() { release_ws(ix, w, s); }
+    } rel{ix, w, s};
+
+    // device staging for host queries/outputs (and scanned scratch), kept
+    // in the workspace so it follows the same stream-ordered reuse rules
+    const size_t qbytes = size_t(chunk) * d.d * 4;
+    const size_t obytes = size_t(chunk) * k * 12 + size_t(chunk) * 12 + 1024;
+    PG_TRY(ws_reserve_stage(w, qbytes + obytes + 512, s));
+    float* dq_stage = static_cast<float*>(w->stage);
+    char* do_stage = static_cast<char*>(w->stage) + ((qbytes + 255) & ~size_t(255));
+    if (!q_dev || !o_dev) PG_TRY(ws_reserve_host(w, std::max(qbytes, obytes) + 256));
+    prag_gpu_timings tm{};
+    prag_gpu_timings* tmp = ix->profiling ? &tm : nullptr;
+    const bool q_pinned = !q_dev && is_pinned_host(queries);
+    for (uint32_t q0 = 0; q0 < nq; q0 += chunk) {
+        const uint32_t n = std::min(chunk, nq - q0);
+        const float* dq;
+        if (q_dev) {
+            dq = queries + size_t(q0) * d.d;
+        } else {
+            const float* src = queries + size_t(q0) * d.d;
+            if (q_pinned) {
+                PG_CUDA(cudaMemcpyAsync(dq_stage, src, size_t(n) * d.d * 4, cudaMemcpyHostToDevice, s));
+            } else {
+                std::memcpy(w->host, src, size_t(n) * d.d * 4);
+                PG_CUDA(cudaMemcpyAsync(dq_stage, w->host, size_t(n) * d.d * 4, cudaMemcpyHostToDevice, s));
+            }
+            dq = dq_stage;
+        }
+        uint64_t* oi;
+        float* od;
+        uint32_t* oc;
+        uint64_t* os;
+        if (o_dev) {
+            oi = out_ids + size_t(q0) * k;
+            od = out_dist + size_t(q0) * k;
+            oc = out_count + q0;
+            os = out_scanned ? out_scanned + q0 : reinterpret_cast<uint64_t*>(do_stage);
+        } else {
+            Carver cv{do_stage};
+            oi = cv.take<uint64_t>(size_t(n) * k);
+            od = cv.take<float>(size_t(n) * k);
+            oc = cv.take<uint32_t>(n);
+            os = cv.take<uint64_t>(n);
+        }
+        PG_TRY(search_pass(ix, w, dq, n, nprobe, k, oi, od, oc, os, s, tmp));
+        if (!o_dev) {
+            // device -> pinned -> caller
+            char* h = static_cast<char*>(w->host);
+            Carver hv{h};
+            uint64_t* hi = hv.take<uint64_t>(size_t(n) * k);
+            float* hd = hv.take<float>(size_t(n) * k);
+            uint32_t* hc = hv.take<uint32_t>(n);
+            uint64_t* hs = hv.take<uint64_t>(n);
+            PG_CUDA(cudaMemcpyAsync(hi, oi, size_t(n) * k * 8, cudaMemcpyDeviceToHost, s));
+            PG_CUDA(cudaMemcpyAsync(hd, od, size_t(n) * k * 4, cudaMemcpyDeviceToHost, s));
+            PG_CUDA(cudaMemcpyAsync(hc, oc, size_t(n) * 4, cudaMemcpyDeviceToHost, s));
+            PG_CUDA(cudaMemcpyAsync(hs, os, size_t(n) * 8, cudaMemcpyDeviceToHost, s));
+            PG_CUDA(cudaStreamSynchronize(s));
+            std::memcpy(out_ids + size_t(q0) * k, hi, size_t(n) * k * 8);
+            std::memcpy(out_dist + size_t(q0) * k, hd, size_t(n) * k * 4);
+            std::memcpy(out_count + q0, hc, size_t(n) * 4);
+            if (out_scanned) std::memcpy(out_scanned + q0, hs, size_t(n) * 8);
+        }
+    }
+    if (tmp) {
+        std::lock_guard<std::mutex> lk(ix->mu);
+        ix->last = tm;
+    }
+    return PRAG_GPU_OK;
+}
+
+}  // namespace
+}  // namespace pg
+
+using namespace pg;
+
+extern "C" {
+
+const char* prag_gpu_last_error(void) { return g_error.c_str(); }
+int prag_gpu_version(void) { return 1; }
+
+int prag_gpu_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int prag_gpu_index_load(const char* path, int device, prag_gpu_index** out) {
+    if (!out || !path) {
+        set_error("null argument");
+        return PRAG_GPU_CONFIG;
+    }
+    *out = nullptr;
+    PG_TRY(require_device(device));
+    HostIndex h;
+    PG_TRY(read_pragix01(path, h, nullptr));
+    auto ix = std::make_unique<prag_gpu_index>();
+    return finish_load(ix, h, device, out);
+}
+
+int prag_gpu_index_load_shard(const char* path, int device, int rank, int world, prag_gpu_index** out) {
+    if (!out || !path || world < 1 || rank < 0 || rank >= world) {
+        set_error("invalid shard arguments");
+        return PRAG_GPU_CONFIG;
+    }
+    *out = nullptr;
+    PG_TRY(require_device(device));
+    std::vector<uint64_t> sizes;
+    PG_TRY(read_pragix01_list_sizes(path, sizes));
+    std::vector<uint32_t> owner(sizes.size());
+    plan_shards_lpt(sizes.data(), uint32_t(sizes.size()), uint32_t(world), owner.data());
+    std::vector<uint8_t> keep(sizes.size());
+    for (size_t l = 0; l < sizes.size(); ++l) keep[l] = owner[l] == uint32_t(rank);
+    HostIndex h;
+    PG_TRY(read_pragix01(path, h, &keep));
+    auto ix = std::make_unique<prag_gpu_index>();
+    ix->shard_rank = rank;
+    ix->shard_world = world;
+    return finish_load(ix, h, device, out);
+}
+
+int prag_gpu_index_from_host(uint32_t nlist, uint32_t d, uint32_t nsq, const float* centroids,
+                             const float* codewords, const uint64_t* list_off, const uint64_t* ids,
+                             const uint8_t* codes, int device, prag_gpu_index** out) {
+    if (!out) {
+        set_error("null argument");
+        return PRAG_GPU_CONFIG;
+    }
+    *out = nullptr;
+    if (nsq == 0 || d % nsq != 0) {
+        set_error("invalid n_subquantizers");
+        return PRAG_GPU_CONFIG;
+    }
+    PG_TRY(require_device(device));
+    HostIndex h;
+    h.nlist = nlist;
+    h.d = d;
+    h.nsq = nsq;
+    h.sub_dim = d / nsq;
+    h.centroids.assign(centroids, centroids + size_t(nlist) * d);
+    h.codewords.assign(codewords, codewords + size_t(nsq) * 256 * (d / nsq));
+    h.list_off.assign(list_off, list_off + nlist + 1);
+    const uint64_t n = list_off[nlist];
+    for (uint32_t l = 0; l < nlist; ++l)
+        if (list_off[l + 1] < list_off[l]) {
+            set_error("list_off must be non-decreasing");
+            return PRAG_GPU_CONFIG;
+        }
+    h.ids.assign(ids, ids + n);
+    h.codes.assign(codes, codes + n * nsq);
+    h.ntotal_global = n;
+    auto ix = std::make_unique<prag_gpu_index>();
+    return finish_load(ix, h, device, out);
+}
+
+void prag_gpu_index_free(prag_gpu_index* ix) {
+    if (!ix) return;
+    {
+        DeviceGuard g(ix->device);
+        cudaDeviceSynchronize();
+        for (Workspace* w : ix->pool) {
+            cudaFree(w->buf);
+            cudaFree(w->stage);
+            if (w->host) cudaFreeHost(w->host);
+            cudaEventDestroy(w->done);
+            for (auto& e : w->ev) cudaEventDestroy(e);
+            delete w;
+        }
+        free_device_index(ix->dev);
+    }
+    delete ix;
+}
+
+int prag_gpu_index_describe(const prag_gpu_index* ix, prag_gpu_index_desc* o) {
+    if (!ix || !o) {
+        set_error("null argument");
+        return PRAG_GPU_CONFIG;
+    }
+    std::memset(o, 0, sizeof *o);
+    o->nlist = ix->dev.nlist;
+    o->d = ix->dev.d;
+    o->nsq = ix->dev.nsq;
+    o->sub_dim = ix->dev.sub_dim;
+    o->ntotal = ix->dev.ntotal;
+    o->ntotal_global = ix->ntotal_global;
+    o->max_list_len = ix->dev.max_list_len;
+    o->device = ix->device;
+    o->shard_rank = ix->shard_rank;
+    o->shard_world = ix->shard_world;
+    o->device_bytes = ix->device_bytes;
+    o->code_layout = ix->dev.code_layout;
+    return PRAG_GPU_OK;
+}
+
+uint32_t prag_gpu_index_nlist(const prag_gpu_index* ix) { return ix ? ix->dev.nlist : 0; }
+
+int prag_gpu_index_list_sizes(const prag_gpu_index* ix, uint64_t* out) {
+    if (!ix || !out) {
+        set_error("null argument");
+        return PRAG_GPU_CONFIG;
+    }
+    std::copy(ix->host_list_len.begin(), ix->host_list_len.end(), out);
+    return PRAG_GPU_OK;
+}
+
+int prag_gpu_search(prag_gpu_index* ix, const float* queries, uint32_t nq, uint32_t nprobe, uint32_t k,
+                    uint64_t* out_ids, float* out_dist, uint32_t* out_count, uint64_t* out_scanned,
+                    void* stream) {
+    if (!ix) {
+        set_error("null index");
+        return PRAG_GPU_CONFIG;
+    }
+    return do_search(ix, queries, nq, nprobe, k, out_ids, out_dist, out_count, out_scanned,
+                     static_cast<cudaStream_t>(stream));
+}
+
+int prag_gpu_probe(prag_gpu_index* ix, const float* queries, uint32_t nq, uint32_t nprobe, uint32_t* out_lists,
+                   float* out_dist, void* stream) {
+    if (!ix) {
+        set_error("null index");
+        return PRAG_GPU_CONFIG;
+    }
+    PG_TRY(validate(ix, nprobe, 1));
+    if (nq == 0) return PRAG_GPU_OK;
+    DeviceGuard g(ix->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const DeviceIndex& d = ix->dev;
+    const uint32_t pw = pow2_at_least(nprobe);
+    Workspace* w = acquire_ws(ix, s);
+    struct Rel {
+        prag_gpu_index* ix;
+        Workspace* w;
+        cudaStream_t s;
+        ~Rel() { release_ws(ix, w, s); }
+    } rel{ix, w, s};
+    size_t need;
+    {
+        Carver c{nullptr};
+        c.take<float>(size_t(nq) * d.d);
+        c.take<float>(size_t(nq) * d.nlist);
+        c.take<uint32_t>(size_t(nq) * nprobe);
+        c.take<float>(size_t(nq) * nprobe);
+        c.take<uint32_t>(size_t(nq) * pw);
+        c.take<uint64_t>(size_t(nq) * pw);
+        need = c.off + 256;
+    }
+    PG_TRY(ws_reserve(w, need, s));
+    Carver c{static_cast<char*>(w->buf)};
+    float* dq = c.take<float>(size_t(nq) * d.d);
+    float* coarse = c.take<float>(size_t(nq) * d.nlist);
+    uint32_t* pl = c.take<uint32_t>(size_t(nq) * nprobe);
+    float* pd = c.take<float>(size_t(nq) * nprobe);
+    uint32_t* pk = c.take<uint32_t>(size_t(nq) * pw);
+    uint64_t* pt = c.take<uint64_t>(size_t(nq) * pw);
+    PG_CUDA(cudaMemcpyAsync(dq, queries, size_t(nq) * d.d * 4, cudaMemcpyDefault, s));
+    PG_TRY(launch_coarse(d, dq, nq, coarse, s));
+    PG_TRY(launch_select_probe(d, coarse, nq, nprobe, pl, pd, pk, pt, s));
+    PG_CUDA(cudaMemcpyAsync(out_lists, pl, size_t(nq) * nprobe * 4, cudaMemcpyDefault, s));
+    if (out_dist) PG_CUDA(cudaMemcpyAsync(out_dist, pd, size_t(nq) * nprobe * 4, cudaMemcpyDefault, s));
+    PG_CUDA(cudaStreamSynchronize(s));
+    return PRAG_GPU_OK;
+}
+
+int prag_gpu_plan_shards(const uint64_t* sizes, uint32_t nlist, uint32_t world, uint32_t* owner) {
+    if ((!sizes || !owner) && nlist) {
+        set_error("null argument");
+        return PRAG_GPU_CONFIG;
+    }
+    if (world < 1) {
+        set_error("world must be >= 1");
+        return PRAG_GPU_CONFIG;
+    }
+    plan_shards_lpt(sizes, nlist, world, owner);
+    return PRAG_GPU_OK;
+}
+
+int prag_gpu_merge_topk(const uint64_t* ids, const float* dist, const uint32_t* count, const uint64_t* scanned,
+                        uint32_t nparts, uint32_t nq, uint32_t kin, uint32_t k, uint64_t* out_ids,
+                        float* out_dist, uint32_t* out_count, uint64_t* out_scanned, int device, void* stream) {
+    if (k < 1) {
+        set_error("merge: k must be >= 1");
+        return PRAG_GPU_CONFIG;
+    }
+    if (nq == 0 || nparts == 0) return PRAG_GPU_OK;
+    PG_TRY(require_device(device));
+    DeviceGuard g(device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const size_t cap = size_t(nparts) * kin;
+    const uint32_t pw = pow2_at_least(std::max<uint64_t>(1, std::min<uint64_t>(k, cap)));
+    Carver c{nullptr};
+    c.take<uint64_t>(cap * nq);
+    c.take<float>(cap * nq);
+    c.take<uint32_t>(size_t(nparts) * nq);
+    c.take<uint64_t>(size_t(nparts) * nq);
+    c.take<uint64_t>(size_t(nq) * k);
+    c.take<float>(size_t(nq) * k);
+    c.take<uint32_t>(nq);
+    c.take<uint64_t>(nq);
+    c.take<uint32_t>(cap * nq);
+    c.take<uint64_t>(cap * nq);
+    c.take<uint32_t>(size_t(nq) * pw);
+    c.take<uint64_t>(size_t(nq) * pw);
+    void* buf = nullptr;
+    PG_CUDA(cudaMallocAsync(&buf, c.off + 256, s));
+    Carver v{static_cast<char*>(buf)};
+    uint64_t* di = v.take<uint64_t>(cap * nq);
+    float* dd = v.take<float>(cap * nq);
+    uint32_t* dc = v.take<uint32_t>(size_t(nparts) * nq);
+    uint64_t* ds = v.take<uint64_t>(size_t(nparts) * nq);
+    uint64_t* oi = v.take<uint64_t>(size_t(nq) * k);
+    float* od = v.take<float>(size_t(nq) * k);
+    uint32_t* oc = v.take<uint32_t>(nq);
+    uint64_t* os = v.take<uint64_t>(nq);
+    uint32_t* ck = v.take<uint32_t>(cap * nq);
+    uint64_t* ct = v.take<uint64_t>(cap * nq);
+    uint32_t* gk = v.take<uint32_t>(size_t(nq) * pw);
+    uint64_t* gt = v.take<uint64_t>(size_t(nq) * pw);
+    PG_CUDA(cudaMemcpyAsync(di, ids, cap * nq * 8, cudaMemcpyDefault, s));
+    PG_CUDA(cudaMemcpyAsync(dd, dist, cap * nq * 4, cudaMemcpyDefault, s));
+    PG_CUDA(cudaMemcpyAsync(dc, count, size_t(nparts) * nq * 4, cudaMemcpyDefault, s));
+    if (scanned) PG_CUDA(cudaMemcpyAsync(ds, scanned, size_t(nparts) * nq * 8, cudaMemcpyDefault, s));
+    PG_TRY(launch_merge(di, dd, dc, scanned ? ds : nullptr, nparts, nq, kin, k, oi, od, oc, os, ck, ct, gk, gt, pw,
+                        s));
+    PG_CUDA(cudaMemcpyAsync(out_ids, oi, size_t(nq) * k * 8, cudaMemcpyDefault, s));
+    PG_CUDA(cudaMemcpyAsync(out_dist, od, size_t(nq) * k * 4, cudaMemcpyDefault, s));
+    PG_CUDA(cudaMemcpyAsync(out_count, oc, size_t(nq) * 4, cudaMemcpyDefault, s));
+    if (out_scanned) PG_CUDA(cudaMemcpyAsync(out_scanned, os, size_t(nq) * 8, cudaMemcpyDefault, s));
+    PG_CUDA(cudaFreeAsync(buf, s));
+    if (!(is_device_ptr(out_ids) && is_device_ptr(out_dist) && is_device_ptr(out_count)))
+        PG_CUDA(cudaStreamSynchronize(s));
+    return PRAG_GPU_OK;
+}
+
+// ---------------------------------------------------- performance model
+static void fit_model(const std::vector<double>& xs, const std::vector<double>& ys, prag_gpu_perf_model* m) {
+    // perfmodel.hpp:53-79 least squares + :109-116 clamping
+    const size_t n = xs.size();
+    double sx = 0, sy = 0, sxx = 0, sxy = 0;
+    for (size_t i = 0; i < n; ++i) {
+        sx += xs[i];
+        sy += ys[i];
+        sxx += xs[i] * xs[i];
+        sxy += xs[i] * ys[i];
+    }
+    const double denom = n * sxx - sx * sx;
+    double slope = 0.0, icpt;
+    if (denom == 0.0) {
+        icpt = sy / n;
+    } else {
+        slope = (n * sxy - sx * sy) / denom;
+        icpt = (sy - slope * sx) / n;
+    }
+    double mar = 0.0;
+    for (size_t i = 0; i < n; ++i) mar = std::max(mar, std::abs(ys[i] - (slope * xs[i] + icpt)));
+    m->slope_s = slope;
+    m->intercept_s = icpt;
+    m->fit_residual_s = mar;
+    m->clamped = 0;
+    if (m->slope_s < 0.0) {
+        m->slope_s = 0.0;
+        m->clamped = 1;
+    }
+    if (m->intercept_s < 0.0) {
+        m->intercept_s = 0.0;
+        m->clamped = 1;
+    }
+}
+
+static double median_of(std::vector<double> v) {
+    std::sort(v.begin(), v.end());
+    const size_t n = v.size();
+    return n % 2 ? v[n / 2] : 0.5 * (v[n / 2 - 1] + v[n / 2]);
+}
+
+static int calibrate_core(const std::function<int(uint32_t, double*)>& measure, const uint32_t* grid_in,
+                          uint32_t grid_len, int repeats, int warmups, prag_gpu_perf_model* out,
+                          double* out_lat) {
+    if (!out || (!grid_in && grid_len)) {
+        set_error("null argument");
+        return PRAG_GPU_CONFIG;
+    }
+    std::vector<uint32_t> grid(grid_in, grid_in + grid_len);
+    std::sort(grid.begin(), grid.end());
+    grid.erase(std::unique(grid.begin(), grid.end()), grid.end());
+    if (grid.size() < 2) {  // perfmodel.hpp:98
+        set_error("calibrate_retrieval: need >= 2 distinct nprobe values");
+        return PRAG_GPU_CONFIG;
+    }
+    if (repeats < 3) {  // perfmodel.hpp:99
+        set_error("calibrate_retrieval: repeats must be >= 3");
+        return PRAG_GPU_CONFIG;
+    }
+    std::vector<double> xs, ys;
+    for (uint32_t np : grid) {
+        double t;
+        for (int i = 0; i < warmups; ++i) PG_TRY(measure(np, &t));
+        std::vector<double> runs;
+        for (int r = 0; r < repeats; ++r) {
+            PG_TRY(measure(np, &t));
+            runs.push_back(t);
+        }
+        xs.push_back(double(np));
+        ys.push_back(median_of(runs));
+    }
+    fit_model(xs, ys, out);
+    if (out_lat) std::copy(ys.begin(), ys.end(), out_lat);
+    return PRAG_GPU_OK;
+}
+
+int prag_gpu_calibrate_retrieval(prag_gpu_index* ix, const float* queries, uint32_t nq, uint32_t k,
+                                 const uint32_t* grid, uint32_t grid_len, int repeats, int warmups,
+                                 prag_gpu_perf_model* out, double* out_lat) {
+    if (!ix || !queries || nq == 0) {
+        set_error("calibrate: need an index and >= 1 query");
+        return PRAG_GPU_CONFIG;
+    }
+    std::vector<uint64_t> ids(size_t(nq) * k);
+    std::vector<float> dist(size_t(nq) * k);
+    std::vector<uint32_t> cnt(nq);
+    // The drop-in contract: host queries in, host results out, wall clock
+    // around the whole call (perfmodel_main.cpp:57-63 Stopwatch protocol).
+    auto measure = [&](uint32_t np, double* t) -> int {
+        auto t0 = std::chrono::steady_clock::now();
+        PG_TRY(prag_gpu_search(ix, queries, nq, np, k, ids.data(), dist.data(), cnt.data(), nullptr, nullptr));
+        *t = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        return PRAG_GPU_OK;
+    };
+    for (uint32_t i = 0; i < grid_len; ++i)
+        if (grid[i] < 1 || grid[i] > ix->dev.nlist) {
+            set_error("search: nprobe out of [1, nlist]");
+            return PRAG_GPU_CONFIG;
+        }
+    return calibrate_core(measure, grid, grid_len, repeats, warmups, out, out_lat);
+}
+
+int prag_gpu_calibrate_with(prag_gpu_measure_fn fn, void* ctx, const uint32_t* grid, uint32_t grid_len,
+                            int repeats, int warmups, prag_gpu_perf_model* out) {
+    if (!fn) {
+        set_error("null measure function");
+        return PRAG_GPU_CONFIG;
+    }
+    auto measure = [&](uint32_t np, double* t) -> int {
+        *t = fn(np, ctx);
+        return PRAG_GPU_OK;
+    };
+    return calibrate_core(measure, grid, grid_len, repeats, warmups, out, nullptr);
+}
+
+uint32_t prag_gpu_select_nprobe(const prag_gpu_perf_model* m, double budget_s, uint32_t nlist, double margin) {
+    // perfmodel.hpp:148-157
+    if (budget_s <= 0.0) return 1;
+    const double limit = budget_s * (1.0 - margin);
+    if (m->slope_s * 1 + m->intercept_s > limit) return 1;
+    if (m->slope_s <= 0.0) return nlist;
+    const double max_n = (limit - m->intercept_s) / m->slope_s;
+    if (max_n >= double(nlist)) return nlist;
+    return uint32_t(std::max(1.0, std::floor(max_n + 1e-9)));
+}
+
+int prag_gpu_set_profiling(prag_gpu_index* ix, int enabled) {
+    if (!ix) {
+        set_error("null index");
+        return PRAG_GPU_CONFIG;
+    }
+    ix->profiling = enabled != 0;
+    return PRAG_GPU_OK;
+}
+
+int prag_gpu_last_timings(const prag_gpu_index* ix, prag_gpu_timings* out) {
+    if (!ix || !out) {
+        set_error("null argument");
+        return PRAG_GPU_CONFIG;
+    }
+    std::lock_guard<std::mutex> lk(const_cast<prag_gpu_index*>(ix)->mu);
+    *out = ix->last;
+    return PRAG_GPU_OK;
+}
+
+}  // extern "C"

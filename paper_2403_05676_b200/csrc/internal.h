@@ -1,0 +1,157 @@
+// internal.h -- shared declarations of the prag_gpu library (not public ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "prag_gpu.h"
+
+namespace pg {
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+
+struct Status {
+    int code = PRAG_GPU_OK;
+    static Status ok() { return {}; }
+};
+
+#define PG_CUDA(expr)                                                                      \
+    do {                                                                                   \
+        cudaError_t _e = (expr);                                                           \
+        if (_e != cudaSuccess) {                                                           \
+            ::pg::set_error(std::string("CUDA error: ") + cudaGetErrorString(_e) + " at " + \
+                            __FILE__ + ":" + std::to_string(__LINE__) + " (" #expr ")");  \
+            return _e == cudaErrorMemoryAllocation ? PRAG_GPU_OOM : PRAG_GPU_CUDA;         \
+        }                                                                                  \
+    } while (0)
+
+#define PG_TRY(expr)                      \
+    do {                                  \
+        int _rc = (expr);                 \
+        if (_rc != PRAG_GPU_OK) return _rc; \
+    } while (0)
+
+// ------------------------------------------------------------- host index
+// De-interleaved (SoA, list-major) image of a PRAGIX01 file
+// (annindex.hpp:335-359 AoS -> arrays).
+struct HostIndex {
+    uint32_t nlist = 0, d = 0, nsq = 0, sub_dim = 0;
+    std::vector<float> centroids;   // [nlist][d]
+    std::vector<float> codewords;   // [nsq][256][sub_dim]
+    std::vector<uint64_t> list_off; // [nlist+1]
+    std::vector<uint64_t> ids;      // [ntotal]
+    std::vector<uint8_t> codes;     // [ntotal][nsq]
+    uint64_t ntotal_global = 0;
+};
+
+// Parses PRAGIX01 (annindex.hpp:361-411). keep(list) selects resident lists
+// (sharding); others are kept empty. Returns status, error text set.
+int read_pragix01(const std::string& path, HostIndex& out, const std::vector<uint8_t>* keep);
+int read_pragix01_list_sizes(const std::string& path, std::vector<uint64_t>& sizes);
+void plan_shards_lpt(const uint64_t* sizes, uint32_t nlist, uint32_t world, uint32_t* owner);
+
+// ----------------------------------------------------------- device index
+constexpr uint32_t kListPad = 32;  // lists padded to a multiple of 32 entries
+
+struct DeviceIndex {
+    uint32_t nlist = 0, d = 0, nsq = 0, sub_dim = 0;
+    uint64_t ntotal = 0;       // real resident entries
+    uint64_t npadded = 0;      // padded slots
+    uint32_t max_list_len = 0;
+    float* centroids = nullptr;   // [nlist][d]
+    float* centroidsT = nullptr;  // [d][nlist] (coalesced coarse scan)
+    float* codewordsT = nullptr;  // [nsq][sub_dim][256]
+    uint64_t* list_off = nullptr; // [nlist+1] padded slot offsets
+    uint32_t* list_len = nullptr; // [nlist]
+    uint64_t* ids = nullptr;      // [npadded]
+    uint8_t* codes = nullptr;     // plain: [npadded][nsq]; skewed: see kernels.cu
+    uint32_t code_layout = 0;
+};
+
+// ------------------------------------------------------------ workspace
+struct Workspace {
+    int device = 0;
+    cudaEvent_t done = nullptr;   // recorded after the last kernel using it
+    cudaStream_t last_stream = nullptr;
+    bool busy = false;
+    // device buffers (grown on demand)
+    void* buf = nullptr;
+    size_t buf_bytes = 0;
+    void* stage = nullptr;        // query/output staging
+    size_t stage_bytes = 0;
+    // pinned host staging
+    void* host = nullptr;
+    size_t host_bytes = 0;
+    // profiling events
+    cudaEvent_t ev[8] = {};
+};
+
+struct SearchPlanSizes {
+    uint32_t nq_chunk;     // queries per pass
+    uint64_t cand_cap;     // candidate slots per pass
+    uint64_t item_cap;     // work items per pass
+};
+
+}  // namespace pg
+
+struct prag_gpu_index {
+    int device = 0;
+    int shard_rank = 0, shard_world = 1;
+    uint64_t ntotal_global = 0;
+    pg::DeviceIndex dev;
+    std::vector<uint64_t> host_list_len;          // resident sizes
+    std::vector<uint64_t> top_prefix;             // prefix sums of sizes sorted desc
+    uint64_t device_bytes = 0;
+    bool profiling = false;
+    prag_gpu_timings last{};
+    std::mutex mu;                                // guards pool and `last`
+    std::vector<pg::Workspace*> pool;
+};
+
+namespace pg {
+
+// kernels.cu launchers (all asynchronous on `s`)
+struct SearchBuffers {
+    // inputs
+    const float* queries;   // device [nq][d]
+    uint32_t nq, nprobe, k;
+    // outputs (device)
+    uint64_t* out_ids;
+    float* out_dist;
+    uint32_t* out_count;
+    uint64_t* out_scanned;
+    // scratch (device)
+    float* coarse_dist;     // [nq][nlist]
+    uint32_t* probe;        // [nq][nprobe]
+    float* probe_dist;      // [nq][nprobe]
+    uint64_t* q_cand_off;   // [nq+1]
+    uint4* items;           // [item_cap]
+    uint32_t* num_items;    // [1]
+    uint32_t* item_cursor;  // [1]
+    float* cand_dist;       // [cand_cap]
+    uint32_t* cand_entry;   // [cand_cap]
+    uint32_t* sort_scratch; // generic select scratch
+    uint64_t item_cap, cand_cap;
+};
+
+int launch_coarse(const DeviceIndex& ix, const float* queries, uint32_t nq, float* out, cudaStream_t s);
+int launch_select_probe(const DeviceIndex& ix, const float* coarse, uint32_t nq, uint32_t nprobe,
+                        uint32_t* probe, float* probe_dist, uint32_t* gkey, uint64_t* gtie, cudaStream_t s);
+int launch_plan(const DeviceIndex& ix, const SearchBuffers& b, cudaStream_t s);
+int launch_scan(const DeviceIndex& ix, const SearchBuffers& b, cudaStream_t s, int grid, float* glut);
+int launch_final(const DeviceIndex& ix, const SearchBuffers& b, uint32_t* gkey, uint64_t* gtie, uint32_t pw,
+                 cudaStream_t s);
+int launch_merge(const uint64_t* ids, const float* dist, const uint32_t* count, const uint64_t* scanned,
+                 uint32_t nparts, uint32_t nq, uint32_t kin, uint32_t k, uint64_t* out_ids, float* out_dist,
+                 uint32_t* out_count, uint64_t* out_scanned, uint32_t* ckey, uint64_t* ctie, uint32_t* gkey,
+                 uint64_t* gtie, uint32_t pw, cudaStream_t s);
+uint32_t scan_chunk();
+uint32_t sort_cap();
+size_t select_smem_bytes();
+
+}  // namespace pg

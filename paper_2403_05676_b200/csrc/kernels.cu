@@ -1,0 +1,607 @@
+// kernels.cu -- sm_100a kernels of the IVF-PQ search path.
+//
+// Arithmetic contract: every distance is the
+// reference's strictly sequential IEEE fp32 fold (common.hpp:73-80,
+// annindex.hpp:279, :292-302) built from __fsub_rn/__fmul_rn/__fadd_rn so
+// nvcc can never contract to FFMA or reassociate; results are bit-identical to
+// the x86-64 SSE reference. Selection is exact on the (distance, id) total
+// order of annindex.hpp:55-58 / :281.
+//
+// Kernels (one batch of nq queries):
+//   K1  coarse_exact_kernel     q x centroid distances          annindex.hpp:277-280
+//   K1b select_kernel<Probe>    per-query top-nprobe            annindex.hpp:281
+//   P   plan_kernel             (q, list, tile) work items + scanned_vectors :284-305
+//   K2+K3 scan_kernel           LUT in SMEM + list scan         :285-305
+//   K4  select_kernel<Final>    per-query top-k                 :313, :54-60
+//   K5  merge_kernel            shard merge (multi-GPU)
+#include <cstdint>
+
+#include "internal.h"
+
+namespace pg {
+
+namespace {
+
+constexpr int kSelThreads = 1024;
+constexpr uint32_t kSortCap = 2048;   // elements sorted in SMEM; larger k sorts in global scratch
+constexpr uint32_t kChunk = 4096;     // entries per scan work item
+
+// Monotone float -> uint32 map (total order == float order for non-NaN).
+__device__ __forceinline__ uint32_t ord_key(float f) {
+    uint32_t u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float key_float(uint32_t k) {
+    uint32_t u = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+    return __uint_as_float(u);
+}
+
+// ------------------------------------------------------------------ K1
+// One thread = one centroid x QB queries. Centroids are read transposed
+// ([d][nlist], coalesced across the warp); query rows sit in SMEM and are
+// warp-broadcast. Each (q, c) accumulator is the sequential fold of
+// squared_l2(query, centroid, d) (common.hpp:73-80): diff = q - c.
+template <int QB>
+__global__ void __launch_bounds__(128) coarse_exact_kernel(const float* __restrict__ centT,
+                                                           const float* __restrict__ queries,
+                                                           uint32_t nq, uint32_t nlist, uint32_t d,
+                                                           float* __restrict__ out) {
+    extern __shared__ float sq[];  // [QB][d]
+    const uint32_t q0 = blockIdx.y * QB;
+    for (uint32_t i = threadIdx.x; i < QB * d; i += blockDim.x) {
+        uint32_t qi = i / d, j = i - qi * d;
+        sq[i] = (q0 + qi < nq) ? queries[size_t(q0 + qi) * d + j] : 0.0f;
+    }
+    __syncthreads();
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nlist) return;
+    float acc[QB];
+#pragma unroll
+    for (int qi = 0; qi < QB; ++qi) acc[qi] = 0.0f;
+    const float* col = centT + c;
+#pragma unroll 4
+    for (uint32_t j = 0; j < d; ++j) {
+        const float cv = __ldg(col + size_t(j) * nlist);
+#pragma unroll
+        for (int qi = 0; qi < QB; ++qi) {
+            const float diff = __fsub_rn(sq[qi * d + j], cv);
+            acc[qi] = __fadd_rn(acc[qi], __fmul_rn(diff, diff));
+        }
+    }
+#pragma unroll
+    for (int qi = 0; qi < QB; ++qi)
+        if (q0 + qi < nq) out[size_t(q0 + qi) * nlist + c] = acc[qi];
+}
+
+// ------------------------------------------------- block-wide exact top-k
+// Selects the kk = min(k, n) smallest (key, tie) pairs of a candidate set
+// (keys from ord_key(distance), tie = list id or chunk_id) and writes them
+// sorted ascending. Radix select on the 32-bit key (4 x 8-bit digits), then
+// if the k-th key is shared, radix select on the 64-bit tie among the equal
+// keys; the selected set is then bitonic-sorted on (key, tie).
+struct SelShared {
+    uint32_t hist[256];
+    uint32_t prefix, rank, eq_count, nsel;
+    uint64_t tie_prefix;
+    uint32_t skey[kSortCap];
+    uint64_t stie[kSortCap];
+};
+
+__device__ __forceinline__ void warp_hist_add(uint32_t* hist, uint32_t bucket, bool active) {
+    // Warp-aggregated shared-memory histogram increment (distances share
+    // their top digits, so plain atomics would serialise on one bin).
+    const unsigned amask = __ballot_sync(0xffffffffu, active);
+    if (!active) return;
+    const unsigned peers = __match_any_sync(amask, bucket);
+    const int leader = __ffs(peers) - 1;
+    if ((threadIdx.x & 31) == leader) atomicAdd(&hist[bucket], __popc(peers));
+}
+
+// After a histogram pass: find the bucket holding the rank-th element
+// (1-based) and update prefix/rank. Executed by warp 0.
+__device__ __forceinline__ void hist_pick(SelShared& sm, int shift, bool tie_pass) {
+    if (threadIdx.x >= 32) return;
+    const int lane = threadIdx.x;
+    uint32_t v[8];
+    uint32_t local = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        v[i] = sm.hist[lane * 8 + i];
+        local += v[i];
+    }
+    uint32_t incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    const uint32_t excl = incl - local;
+    const uint32_t rank = sm.rank;
+    const bool mine = excl < rank && rank <= incl;
+    if (mine) {
+        uint32_t c = excl;
+        int b = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            if (c + v[i] >= rank) {
+                b = i;
+                break;
+            }
+            c += v[i];
+        }
+        const uint32_t bucket = lane * 8 + b;
+        sm.rank = rank - c;
+        sm.eq_count = v[b];
+        if (tie_pass)
+            sm.tie_prefix |= uint64_t(bucket) << shift;
+        else
+            sm.prefix |= bucket << shift;
+    }
+}
+
+template <class Src>
+__device__ void block_topk(const Src& src, uint32_t n, uint32_t k, SelShared& sm, uint32_t* gkey,
+                           uint64_t* gtie, float* out_dist, uint64_t* out_tie, uint32_t* out_count) {
+    const uint32_t kk = n < k ? n : k;
+    const uint32_t tid = threadIdx.x, nth = blockDim.x;
+    bool use_tie = false;
+    uint32_t T = 0xffffffffu;
+    uint64_t TI = ~0ull;
+    if (n > k) {
+        if (tid == 0) {
+            sm.prefix = 0;
+            sm.rank = k;
+            sm.tie_prefix = 0;
+        }
+        uint32_t mask = 0;
+        for (int shift = 24; shift >= 0; shift -= 8) {
+            for (uint32_t i = tid; i < 256; i += nth) sm.hist[i] = 0;
+            __syncthreads();
+            const uint32_t prefix = sm.prefix;
+            for (uint32_t base = 0; base < n; base += nth) {
+                const uint32_t i = base + tid;
+                uint32_t key = 0;
+                bool act = false;
+                if (i < n) {
+                    key = src.key(i);
+                    act = (key & mask) == prefix;
+                }
+                warp_hist_add(sm.hist, (key >> shift) & 255u, act);
+            }
+            __syncthreads();
+            hist_pick(sm, shift, false);
+            __syncthreads();
+            mask |= 0xffu << shift;
+        }
+        T = sm.prefix;
+        // sm.rank = how many of the key==T elements are needed; eq_count = how many exist
+        if (sm.eq_count > sm.rank) {
+            use_tie = true;
+            uint64_t tmask = 0;
+            for (int shift = 56; shift >= 0; shift -= 8) {
+                for (uint32_t i = tid; i < 256; i += nth) sm.hist[i] = 0;
+                __syncthreads();
+                const uint64_t tp = sm.tie_prefix;
+                for (uint32_t base = 0; base < n; base += nth) {
+                    const uint32_t i = base + tid;
+                    uint64_t tie = 0;
+                    bool act = false;
+                    if (i < n && src.key(i) == T) {
+                        tie = src.tie(i);
+                        act = (tie & tmask) == tp;
+                    }
+                    warp_hist_add(sm.hist, uint32_t(tie >> shift) & 255u, act);
+                }
+                __syncthreads();
+                hist_pick(sm, shift, true);
+                __syncthreads();
+                tmask |= uint64_t(0xff) << shift;
+            }
+            TI = sm.tie_prefix;
+        }
+    }
+    // gather the selected set
+    uint32_t pw = 1;
+    while (pw < kk) pw <<= 1;
+    const bool in_smem = pw <= kSortCap;
+    uint32_t* keys = in_smem ? sm.skey : gkey;
+    uint64_t* ties = in_smem ? sm.stie : gtie;
+    if (tid == 0) sm.nsel = 0;
+    __syncthreads();
+    for (uint32_t base = 0; base < n; base += nth) {
+        const uint32_t i = base + tid;
+        bool take = false;
+        uint32_t key = 0;
+        uint64_t tie = 0;
+        if (i < n) {
+            key = src.key(i);
+            if (key < T || (n <= k)) {
+                take = true;
+            } else if (key == T) {
+                tie = src.tie(i);
+                take = !use_tie || tie <= TI;
+            }
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, take);
+        uint32_t wbase = 0;
+        if ((tid & 31) == 0 && bal) wbase = atomicAdd(&sm.nsel, __popc(bal));
+        wbase = __shfl_sync(0xffffffffu, wbase, 0);
+        if (take) {
+            const uint32_t pos = wbase + __popc(bal & ((1u << (tid & 31)) - 1));
+            if (pos < kk) {  // duplicate (key, tie) pairs can exceed kk; they are interchangeable
+                if (key != T || n <= k) tie = src.tie(i);
+                keys[pos] = key;
+                ties[pos] = tie;
+            }
+        }
+    }
+    __syncthreads();
+    for (uint32_t i = kk + tid; i < pw; i += nth) {
+        keys[i] = 0xffffffffu;
+        ties[i] = ~0ull;
+    }
+    __syncthreads();
+    // bitonic sort on (key, tie), ascending
+    for (uint32_t size = 2; size <= pw; size <<= 1) {
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+            for (uint32_t t = tid; t < pw / 2; t += nth) {
+                const uint32_t lo = 2 * t - (t & (stride - 1));
+                const uint32_t hi = lo + stride;
+                const bool up = (lo & size) == 0;
+                const uint32_t ka = keys[lo], kb = keys[hi];
+                const uint64_t ta = ties[lo], tb = ties[hi];
+                const bool gt = ka > kb || (ka == kb && ta > tb);
+                if (gt == up) {
+                    keys[lo] = kb;
+                    keys[hi] = ka;
+                    ties[lo] = tb;
+                    ties[hi] = ta;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (uint32_t i = tid; i < kk; i += nth) {
+        if (out_dist) out_dist[i] = key_float(keys[i]);
+        out_tie[i] = ties[i];
+    }
+    if (tid == 0 && out_count) *out_count = kk;
+    __syncthreads();
+}
+
+struct ProbeSrc {
+    const float* d;
+    __device__ uint32_t key(uint32_t i) const { return ord_key(d[i]); }
+    __device__ uint64_t tie(uint32_t i) const { return i; }
+};
+
+struct FinalSrc {
+    const float* d;
+    const uint32_t* entry;
+    const uint64_t* ids;
+    __device__ uint32_t key(uint32_t i) const { return ord_key(d[i]); }
+    __device__ uint64_t tie(uint32_t i) const { return ids[entry[i]]; }
+};
+
+struct MergeSrc {
+    const uint32_t* k;
+    const uint64_t* t;
+    __device__ uint32_t key(uint32_t i) const { return k[i]; }
+    __device__ uint64_t tie(uint32_t i) const { return t[i]; }
+};
+
+// K1b: per-query top-nprobe lists, (distance, list id) order (annindex.hpp:281).
+__global__ void __launch_bounds__(kSelThreads) select_probe_kernel(const float* __restrict__ coarse,
+                                                                   uint32_t nlist, uint32_t nprobe,
+                                                                   uint32_t* __restrict__ probe,
+                                                                   float* __restrict__ probe_dist,
+                                                                   uint32_t* gkey, uint64_t* gtie) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    SelShared& sm = *reinterpret_cast<SelShared*>(smraw);
+    const uint32_t q = blockIdx.x;
+    ProbeSrc src{coarse + size_t(q) * nlist};
+    uint32_t pw = 1;
+    while (pw < nprobe) pw <<= 1;
+    uint64_t* ties = gtie + size_t(q) * pw;
+    block_topk(src, nlist, nprobe, sm, gkey + size_t(q) * pw, ties, probe_dist + size_t(q) * nprobe,
+               ties, nullptr);
+    // ties[] now holds the sorted list ids; narrow to u32
+    for (uint32_t i = threadIdx.x; i < nprobe; i += blockDim.x) probe[size_t(q) * nprobe + i] = uint32_t(ties[i]);
+}
+
+// ------------------------------------------------------------------- plan
+// One CTA. For each (q, p) pair: len = |list|, its candidate slot offset and
+// ceil(len / kChunk) work items {q, list, begin, out_off}. Per-query
+// scanned_vectors is the sum of probed list lengths (annindex.hpp:305);
+// empty lists contribute nothing (:290).
+template <typename T>
+__device__ T block_excl_scan(T v, T* warp_tmp, T& total) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    T incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        T t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) warp_tmp[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+        T x = lane < nw ? warp_tmp[lane] : T(0);
+        T xi = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            T t = __shfl_up_sync(0xffffffffu, xi, o);
+            if (lane >= o) xi += t;
+        }
+        if (lane < nw) warp_tmp[lane] = xi - x;
+        if (lane == nw - 1) warp_tmp[32] = xi;
+    }
+    __syncthreads();
+    T res = warp_tmp[w] + incl - v;
+    total = warp_tmp[32];
+    __syncthreads();
+    return res;
+}
+
+__global__ void __launch_bounds__(1024) plan_kernel(const uint32_t* __restrict__ probe,
+                                                    const uint32_t* __restrict__ list_len, uint32_t nq,
+                                                    uint32_t nprobe, uint64_t* __restrict__ q_cand_off,
+                                                    uint64_t* __restrict__ scanned, uint4* __restrict__ items,
+                                                    uint32_t* __restrict__ num_items,
+                                                    uint32_t* __restrict__ cursor, uint64_t item_cap) {
+    __shared__ uint64_t tmp64[33];
+    __shared__ uint32_t tmp32[33];
+    const uint32_t P = nq * nprobe;
+    uint64_t carry_c = 0;
+    uint32_t carry_i = 0;
+    for (uint32_t base = 0; base < P; base += blockDim.x) {
+        const uint32_t i = base + threadIdx.x;
+        const bool valid = i < P;
+        const uint32_t list = valid ? probe[i] : 0;
+        const uint32_t len = valid ? list_len[list] : 0;
+        const uint32_t nit = (len + kChunk - 1) / kChunk;
+        uint64_t tot_c;
+        uint32_t tot_i;
+        const uint64_t ec = block_excl_scan<uint64_t>(len, tmp64, tot_c);
+        const uint32_t ei = block_excl_scan<uint32_t>(nit, tmp32, tot_i);
+        if (valid) {
+            const uint32_t q = i / nprobe, p = i - q * nprobe;
+            if (p == 0) q_cand_off[q] = carry_c + ec;
+            for (uint32_t j = 0; j < nit; ++j) {
+                const uint64_t slot = carry_i + ei + j;
+                if (slot < item_cap)
+                    items[slot] = make_uint4(q, list, j * kChunk, uint32_t(carry_c + ec + uint64_t(j) * kChunk));
+            }
+        }
+        carry_c += tot_c;
+        carry_i += tot_i;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        q_cand_off[nq] = carry_c;
+        *num_items = carry_i;
+        *cursor = 0;
+    }
+    __syncthreads();
+    for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x) scanned[q] = q_cand_off[q + 1] - q_cand_off[q];
+}
+
+// ---------------------------------------------------------------- K2 + K3
+// Persistent CTAs pull (q, list, begin) work items. On a new (q, list):
+// residual r = q - c_list (annindex.hpp:292) and the ADC table
+// T[sq][code] = squared_l2(r_sq, w[sq][code], sub_dim) (:293-299) are built
+// in SMEM; then each thread folds one entry at a time:
+// dist = ((0 + T[0][c0]) + T[1][c1]) + ... (:300-302).
+template <bool kSmemLut>
+__global__ void __launch_bounds__(256) scan_kernel(
+    const float* __restrict__ queries, const float* __restrict__ centroids,
+    const float* __restrict__ codewordsT, const uint64_t* __restrict__ list_off,
+    const uint32_t* __restrict__ list_len, const uint8_t* __restrict__ codes, uint32_t d, uint32_t nsq,
+    uint32_t sub_dim, const uint4* __restrict__ items, const uint32_t* __restrict__ num_items,
+    uint32_t* __restrict__ cursor, float* __restrict__ cand_dist, uint32_t* __restrict__ cand_entry,
+    float* __restrict__ glut) {
+    extern __shared__ __align__(16) float smf[];
+    float* resid = smf;                                   // [d]
+    float* lut = kSmemLut ? smf + ((d + 3) & ~3u) : glut + size_t(blockIdx.x) * nsq * 256;
+    __shared__ uint32_t s_item;
+    const uint32_t total = *num_items;
+    uint32_t cur_q = 0xffffffffu, cur_list = 0xffffffffu;
+    for (;;) {
+        if (threadIdx.x == 0) s_item = atomicAdd(cursor, 1u);
+        __syncthreads();
+        const uint32_t it = s_item;
+        if (it >= total) break;
+        const uint4 w = items[it];
+        const uint32_t q = w.x, list = w.y, begin = w.z, out_off = w.w;
+        if (q != cur_q || list != cur_list) {
+            const float* qv = queries + size_t(q) * d;
+            const float* cv = centroids + size_t(list) * d;
+            for (uint32_t j = threadIdx.x; j < d; j += blockDim.x) resid[j] = __fsub_rn(qv[j], cv[j]);
+            __syncthreads();
+            for (uint32_t t = threadIdx.x; t < nsq * 256; t += blockDim.x) {
+                const uint32_t s = t >> 8, code = t & 255u;
+                const float* r = resid + s * sub_dim;
+                const float* wv = codewordsT + size_t(s) * sub_dim * 256 + code;
+                float acc = 0.0f;
+                for (uint32_t j = 0; j < sub_dim; ++j) {
+                    const float diff = __fsub_rn(r[j], __ldg(wv + j * 256));
+                    acc = __fadd_rn(acc, __fmul_rn(diff, diff));
+                }
+                lut[t] = acc;
+            }
+            cur_q = q;
+            cur_list = list;
+            __syncthreads();
+        }
+        const uint32_t len = list_len[list];
+        const uint32_t end = min(len, begin + kChunk);
+        const uint64_t lbase = list_off[list];
+        for (uint32_t e = begin + threadIdx.x; e < end; e += blockDim.x) {
+            const uint64_t slot = lbase + e;
+            const uint8_t* c = codes + slot * nsq;
+            float dist = 0.0f;
+            if ((nsq & 3u) == 0) {
+                for (uint32_t s4 = 0; s4 < nsq; s4 += 4) {
+                    const uint32_t wd = *reinterpret_cast<const uint32_t*>(c + s4);
+                    dist = __fadd_rn(dist, lut[(s4 + 0) * 256 + (wd & 255u)]);
+                    dist = __fadd_rn(dist, lut[(s4 + 1) * 256 + ((wd >> 8) & 255u)]);
+                    dist = __fadd_rn(dist, lut[(s4 + 2) * 256 + ((wd >> 16) & 255u)]);
+                    dist = __fadd_rn(dist, lut[(s4 + 3) * 256 + (wd >> 24)]);
+                }
+            } else {
+                for (uint32_t s = 0; s < nsq; ++s) dist = __fadd_rn(dist, lut[s * 256 + c[s]]);
+            }
+            const uint32_t o = out_off + (e - begin);
+            cand_dist[o] = dist;
+            cand_entry[o] = uint32_t(slot);
+        }
+        __syncthreads();
+    }
+}
+
+// K4: per-query exact top-k over all candidates of the query.
+__global__ void __launch_bounds__(kSelThreads) select_final_kernel(
+    const float* __restrict__ cand_dist, const uint32_t* __restrict__ cand_entry,
+    const uint64_t* __restrict__ ids, const uint64_t* __restrict__ q_cand_off, uint32_t k,
+    uint64_t* __restrict__ out_ids, float* __restrict__ out_dist, uint32_t* __restrict__ out_count,
+    uint32_t* gkey, uint64_t* gtie, uint32_t pw) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    SelShared& sm = *reinterpret_cast<SelShared*>(smraw);
+    const uint32_t q = blockIdx.x;
+    const uint64_t b = q_cand_off[q], e = q_cand_off[q + 1];
+    FinalSrc src{cand_dist + b, cand_entry + b, ids};
+    block_topk(src, uint32_t(e - b), k, sm, gkey + size_t(q) * pw, gtie + size_t(q) * pw,
+               out_dist + size_t(q) * k, out_ids + size_t(q) * k, out_count + q);
+}
+
+// K5: exact top-k of the union of per-shard top-k lists.
+__global__ void __launch_bounds__(kSelThreads) merge_kernel(
+    const uint64_t* __restrict__ ids, const float* __restrict__ dist, const uint32_t* __restrict__ count,
+    const uint64_t* __restrict__ scanned, uint32_t nparts, uint32_t nq, uint32_t kin, uint32_t k,
+    uint64_t* __restrict__ out_ids, float* __restrict__ out_dist, uint32_t* __restrict__ out_count,
+    uint64_t* __restrict__ out_scanned, uint32_t* ckey, uint64_t* ctie, uint32_t* gkey, uint64_t* gtie,
+    uint32_t pw) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    SelShared& sm = *reinterpret_cast<SelShared*>(smraw);
+    __shared__ uint32_t s_n;
+    const uint32_t q = blockIdx.x;
+    const size_t cap = size_t(nparts) * kin;
+    uint32_t* ck = ckey + q * cap;
+    uint64_t* ct = ctie + q * cap;
+    if (threadIdx.x == 0) {
+        uint32_t n = 0;
+        uint64_t sc = 0;
+        for (uint32_t p = 0; p < nparts; ++p) {
+            const uint32_t c = min(count[size_t(p) * nq + q], kin);
+            n += c;
+            if (scanned) sc += scanned[size_t(p) * nq + q];
+        }
+        s_n = n;
+        if (out_scanned) out_scanned[q] = sc;
+    }
+    __syncthreads();
+    // compact valid entries (per part, the first count[p][q] of kin slots)
+    for (uint32_t p = 0; p < nparts; ++p) {
+        uint32_t before = 0;
+        for (uint32_t pp = 0; pp < p; ++pp) before += min(count[size_t(pp) * nq + q], kin);
+        const uint32_t c = min(count[size_t(p) * nq + q], kin);
+        const size_t src = (size_t(p) * nq + q) * kin;
+        for (uint32_t i = threadIdx.x; i < c; i += blockDim.x) {
+            ck[before + i] = ord_key(dist[src + i]);
+            ct[before + i] = ids[src + i];
+        }
+    }
+    __syncthreads();
+    MergeSrc s{ck, ct};
+    block_topk(s, s_n, k, sm, gkey + size_t(q) * pw, gtie + size_t(q) * pw, out_dist + size_t(q) * k,
+               out_ids + size_t(q) * k, out_count + q);
+}
+
+}  // namespace
+
+size_t select_smem_bytes() { return sizeof(SelShared); }
+
+static int check_launch(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error(std::string("CUDA launch failed (") + what + "): " + cudaGetErrorString(e));
+        return PRAG_GPU_CUDA;
+    }
+    return PRAG_GPU_OK;
+}
+
+int launch_coarse(const DeviceIndex& ix, const float* queries, uint32_t nq, float* out, cudaStream_t s) {
+    constexpr int QB = 8;
+    dim3 grid((ix.nlist + 127) / 128, (nq + QB - 1) / QB);
+    size_t smem = size_t(QB) * ix.d * sizeof(float);
+    if (smem > 48 * 1024)
+        PG_CUDA(cudaFuncSetAttribute(coarse_exact_kernel<QB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(smem)));
+    coarse_exact_kernel<QB><<<grid, 128, smem, s>>>(ix.centroidsT, queries, nq, ix.nlist, ix.d, out);
+    return check_launch("coarse");
+}
+
+static int set_sel_smem(const void* fn) {
+    static_assert(sizeof(SelShared) < 227 * 1024, "selection smem");
+    PG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(SelShared))));
+    return PRAG_GPU_OK;
+}
+
+int launch_select_probe(const DeviceIndex& ix, const float* coarse, uint32_t nq, uint32_t nprobe,
+                        uint32_t* probe, float* probe_dist, uint32_t* gkey, uint64_t* gtie, cudaStream_t s) {
+    PG_TRY(set_sel_smem(reinterpret_cast<const void*>(select_probe_kernel)));
+    select_probe_kernel<<<nq, kSelThreads, sizeof(SelShared), s>>>(coarse, ix.nlist, nprobe, probe, probe_dist,
+                                                                   gkey, gtie);
+    return check_launch("select_probe");
+}
+
+int launch_plan(const DeviceIndex& ix, const SearchBuffers& b, cudaStream_t s) {
+    plan_kernel<<<1, 1024, 0, s>>>(b.probe, ix.list_len, b.nq, b.nprobe, b.q_cand_off, b.out_scanned, b.items,
+                                   b.num_items, b.item_cursor, b.item_cap);
+    return check_launch("plan");
+}
+
+int launch_scan(const DeviceIndex& ix, const SearchBuffers& b, cudaStream_t s, int grid, float* glut) {
+    const size_t lut_bytes = size_t(ix.nsq) * 256 * sizeof(float);
+    const size_t res_bytes = ((ix.d + 3) & ~3u) * sizeof(float);
+    const bool smem_lut = lut_bytes + res_bytes <= 200 * 1024;
+    if (smem_lut) {
+        const size_t smem = lut_bytes + res_bytes;
+        PG_CUDA(cudaFuncSetAttribute(scan_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        scan_kernel<true><<<grid, 256, smem, s>>>(b.queries, ix.centroids, ix.codewordsT, ix.list_off, ix.list_len,
+                                                  ix.codes, ix.d, ix.nsq, ix.sub_dim, b.items, b.num_items,
+                                                  b.item_cursor, b.cand_dist, b.cand_entry, nullptr);
+    } else {
+        const size_t smem = res_bytes;
+        PG_CUDA(cudaFuncSetAttribute(scan_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        scan_kernel<false><<<grid, 256, smem, s>>>(b.queries, ix.centroids, ix.codewordsT, ix.list_off,
+                                                   ix.list_len, ix.codes, ix.d, ix.nsq, ix.sub_dim, b.items,
+                                                   b.num_items, b.item_cursor, b.cand_dist, b.cand_entry, glut);
+    }
+    return check_launch("scan");
+}
+
+int launch_final(const DeviceIndex& ix, const SearchBuffers& b, uint32_t* gkey, uint64_t* gtie, uint32_t pw,
+                 cudaStream_t s) {
+    PG_TRY(set_sel_smem(reinterpret_cast<const void*>(select_final_kernel)));
+    select_final_kernel<<<b.nq, kSelThreads, sizeof(SelShared), s>>>(b.cand_dist, b.cand_entry, ix.ids,
+                                                                      b.q_cand_off, b.k, b.out_ids, b.out_dist,
+                                                                      b.out_count, gkey, gtie, pw);
+    return check_launch("final");
+}
+
+int launch_merge(const uint64_t* ids, const float* dist, const uint32_t* count, const uint64_t* scanned,
+                 uint32_t nparts, uint32_t nq, uint32_t kin, uint32_t k, uint64_t* out_ids, float* out_dist,
+                 uint32_t* out_count, uint64_t* out_scanned, uint32_t* ckey, uint64_t* ctie, uint32_t* gkey,
+                 uint64_t* gtie, uint32_t pw, cudaStream_t s) {
+    PG_TRY(set_sel_smem(reinterpret_cast<const void*>(merge_kernel)));
+    merge_kernel<<<nq, kSelThreads, sizeof(SelShared), s>>>(ids, dist, count, scanned, nparts, nq, kin, k, out_ids,
+                                                             out_dist, out_count, out_scanned, ckey, ctie, gkey,
+                                                             gtie, pw);
+    return check_launch("merge");
+}
+
+uint32_t scan_chunk() { return kChunk; }
+uint32_t sort_cap() { return kSortCap; }
+
+}  // namespace pg

@@ -1,0 +1,331 @@
+"""Python mirror of the reference retrieval API over the B200 C ABI.
+
+Names, argument meaning and error behaviour follow the reference C++ API
+(/root/reference/proj/include/prag/annindex.hpp:35-50, :262-315 and
+perfmodel.hpp:19-26, :92-157), so the parity tests read like the reference's
+own tests (test_annindex.cpp, test_perfmodel.cpp). Compute happens only in
+libprag_gpu.so (hand-written sm_100a kernels); this module moves pointers.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+from dataclasses import dataclass, field
+from typing import Callable, Iterable, List, Optional, Sequence
+
+import numpy as np
+
+from ._lib import (ConfigError, FormatError, IndexDesc, MEASURE_FN, PerfModelC, Timings, check, lib)
+
+try:  # torch is plumbing only (device buffers / streams); optional here
+    import torch
+except Exception:  # pragma: no cover
+    torch = None
+
+
+# ------------------------------------------------------------------ types
+@dataclass
+class SearchParams:
+    """annindex.hpp:35-39."""
+    nprobe: int = 1
+    k: int = 2
+    exact_rerank: bool = False
+
+
+@dataclass
+class ScoredId:
+    """annindex.hpp:41-44."""
+    chunk_id: int = 0
+    distance: float = 0.0
+
+
+@dataclass
+class SearchResult:
+    """annindex.hpp:46-50: ascending distance, ties by lower id."""
+    neighbors: List[ScoredId] = field(default_factory=list)
+    scanned_vectors: int = 0
+    scanned_lists: int = 0
+
+
+@dataclass
+class BatchResult:
+    ids: object        # [nq, k] uint64 (numpy) / int64 view (torch)
+    dist: object       # [nq, k] float32
+    count: object      # [nq] uint32 / int32
+    scanned: object    # [nq] uint64 / int64
+
+    def result(self, q: int, nprobe: int) -> SearchResult:
+        ids = np.asarray(_to_numpy(self.ids))
+        dist = np.asarray(_to_numpy(self.dist))
+        c = int(np.asarray(_to_numpy(self.count))[q])
+        return SearchResult([ScoredId(int(ids[q, i]), float(dist[q, i])) for i in range(c)],
+                            int(np.asarray(_to_numpy(self.scanned))[q]), nprobe)
+
+
+def _to_numpy(a):
+    if torch is not None and isinstance(a, torch.Tensor):
+        t = a.detach().cpu()
+        if t.dtype == torch.int64:
+            return t.numpy().view(np.uint64)
+        if t.dtype == torch.int32:
+            return t.numpy().view(np.uint32)
+        return t.numpy()
+    return a
+
+
+def _ptr(a) -> C.c_void_p:
+    if a is None:
+        return C.c_void_p(0)
+    if torch is not None and isinstance(a, torch.Tensor):
+        return C.c_void_p(a.data_ptr())
+    return C.c_void_p(a.ctypes.data)
+
+
+def _stream_ptr(stream) -> C.c_void_p:
+    if stream is None:
+        return C.c_void_p(0)
+    if torch is not None and isinstance(stream, torch.cuda.Stream):
+        return C.c_void_p(stream.cuda_stream)
+    return C.c_void_p(int(stream))
+
+
+def device_count() -> int:
+    return lib().prag_gpu_device_count()
+
+
+# ------------------------------------------------------------------ index
+class GpuIndex:
+    """HBM-resident IVF-PQ index (replaces the IvfIndex + PqCodebook pair)."""
+
+    def __init__(self, handle: C.c_void_p):
+        self._h = handle
+        d = IndexDesc()
+        check(lib().prag_gpu_index_describe(self._h, C.byref(d)))
+        self.desc = d
+        self.nlist, self.d, self.nsq, self.sub_dim = d.nlist, d.d, d.nsq, d.sub_dim
+        self.ntotal, self.device = d.ntotal, d.device
+
+    # constructors ------------------------------------------------------
+    @classmethod
+    def load(cls, path: str, device: int = 0) -> "GpuIndex":
+        """prag::load_index (annindex.hpp:361-411) straight into HBM."""
+        h = C.c_void_p()
+        check(lib().prag_gpu_index_load(str(path).encode(), device, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def load_shard(cls, path: str, rank: int, world: int, device: int = 0) -> "GpuIndex":
+        h = C.c_void_p()
+        check(lib().prag_gpu_index_load_shard(str(path).encode(), device, rank, world, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def from_host(cls, centroids, codewords, list_off, ids, codes, device: int = 0) -> "GpuIndex":
+        centroids = np.ascontiguousarray(centroids, dtype=np.float32)
+        codewords = np.ascontiguousarray(codewords, dtype=np.float32)
+        list_off = np.ascontiguousarray(list_off, dtype=np.uint64)
+        ids = np.ascontiguousarray(ids, dtype=np.uint64)
+        codes = np.ascontiguousarray(codes, dtype=np.uint8)
+        nlist, d = centroids.shape
+        nsq = codewords.shape[0]
+        h = C.c_void_p()
+        check(lib().prag_gpu_index_from_host(nlist, d, nsq, _ptr(centroids), _ptr(codewords), _ptr(list_off),
+                                             _ptr(ids), _ptr(codes), device, C.byref(h)))
+        return cls(h)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib().prag_gpu_index_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # queries -------------------------------------------------------------
+    def list_sizes(self) -> np.ndarray:
+        out = np.zeros(self.nlist, dtype=np.uint64)
+        check(lib().prag_gpu_index_list_sizes(self._h, _ptr(out)))
+        return out
+
+    def search_batch(self, queries, k: int, nprobe: int, stream=None, out: Optional[BatchResult] = None
+                     ) -> BatchResult:
+        """Batch prag::search: queries [nq, d] float32, host (numpy / CPU tensor)
+        or device (CUDA tensor). Device queries -> device outputs, asynchronous
+        on `stream` (default: torch's current stream)."""
+        on_dev = torch is not None and isinstance(queries, torch.Tensor) and queries.is_cuda
+        if on_dev:
+            q = queries.contiguous()
+            if q.dtype != torch.float32:
+                raise ConfigError("queries must be float32")
+            nq = q.shape[0] if q.dim() == 2 else 1
+            if out is None:
+                out = BatchResult(torch.empty((nq, k), dtype=torch.int64, device=q.device),
+                                  torch.empty((nq, k), dtype=torch.float32, device=q.device),
+                                  torch.empty((nq,), dtype=torch.int32, device=q.device),
+                                  torch.empty((nq,), dtype=torch.int64, device=q.device))
+            if stream is None:
+                stream = torch.cuda.current_stream(q.device)
+        else:
+            if torch is not None and isinstance(queries, torch.Tensor):
+                queries = queries.numpy()
+            q = np.ascontiguousarray(queries, dtype=np.float32).reshape(-1, self.d)
+            nq = q.shape[0]
+            if out is None:
+                out = BatchResult(np.zeros((nq, k), dtype=np.uint64), np.zeros((nq, k), dtype=np.float32),
+                                  np.zeros(nq, dtype=np.uint32), np.zeros(nq, dtype=np.uint64))
+        if (not on_dev) and q.shape[1] != self.d:
+            raise ConfigError(f"query dimension {q.shape[1]} != index d {self.d}")
+        check(lib().prag_gpu_search(self._h, _ptr(q), nq, nprobe, k, _ptr(out.ids), _ptr(out.dist),
+                                    _ptr(out.count), _ptr(out.scanned), _stream_ptr(stream)))
+        return out
+
+    def probe(self, queries, nprobe: int):
+        """Coarse quantizer only (annindex.hpp:277-281)."""
+        q = np.ascontiguousarray(queries, dtype=np.float32).reshape(-1, self.d)
+        lists = np.zeros((q.shape[0], nprobe), dtype=np.uint32)
+        dist = np.zeros((q.shape[0], nprobe), dtype=np.float32)
+        check(lib().prag_gpu_probe(self._h, _ptr(q), q.shape[0], nprobe, _ptr(lists), _ptr(dist), None))
+        return lists, dist
+
+    # profiling -------------------------------------------------------------
+    def set_profiling(self, on: bool) -> None:
+        check(lib().prag_gpu_set_profiling(self._h, 1 if on else 0))
+
+    def last_timings(self) -> dict:
+        t = Timings()
+        check(lib().prag_gpu_last_timings(self._h, C.byref(t)))
+        return {f: getattr(t, f) for f, _ in Timings._fields_}
+
+
+def load_index(path: str, device: int = 0) -> GpuIndex:
+    return GpuIndex.load(path, device)
+
+
+def search(index: GpuIndex, query, params: SearchParams, embeddings=None) -> SearchResult:
+    """prag::search (annindex.hpp:262-315) for one query."""
+    if params.exact_rerank:
+        # annindex.hpp:269-271 error path; rerank is off on the hot path
+        # (pipeline.hpp:228) and not offered by the GPU build.
+        if embeddings is None:
+            raise ConfigError("search: exact_rerank requires raw embeddings")
+        raise ConfigError("search: exact_rerank is not supported by the GPU path")
+    r = index.search_batch(np.asarray(query, dtype=np.float32).reshape(1, -1), params.k, params.nprobe)
+    return r.result(0, params.nprobe)
+
+
+# ------------------------------------------------------------ multi-GPU
+def plan_shards(list_sizes: Sequence[int], world: int) -> np.ndarray:
+    s = np.ascontiguousarray(list_sizes, dtype=np.uint64)
+    owner = np.zeros(len(s), dtype=np.uint32)
+    check(lib().prag_gpu_plan_shards(_ptr(s), len(s), world, _ptr(owner)))
+    return owner
+
+
+def merge_topk(ids, dist, count, scanned, k: int, device: int = 0, stream=None, out=None):
+    """K5: exact top-k of the union of per-shard results.
+    ids/dist [nparts, nq, kin], count/scanned [nparts, nq]; numpy or CUDA tensors."""
+    on_dev = torch is not None and isinstance(ids, torch.Tensor) and ids.is_cuda
+    nparts, nq, kin = ids.shape
+    if out is None:
+        if on_dev:
+            out = BatchResult(torch.empty((nq, k), dtype=torch.int64, device=ids.device),
+                              torch.empty((nq, k), dtype=torch.float32, device=ids.device),
+                              torch.empty((nq,), dtype=torch.int32, device=ids.device),
+                              torch.empty((nq,), dtype=torch.int64, device=ids.device))
+        else:
+            ids = np.ascontiguousarray(ids, dtype=np.uint64)
+            dist = np.ascontiguousarray(dist, dtype=np.float32)
+            count = np.ascontiguousarray(count, dtype=np.uint32)
+            scanned = None if scanned is None else np.ascontiguousarray(scanned, dtype=np.uint64)
+            out = BatchResult(np.zeros((nq, k), dtype=np.uint64), np.zeros((nq, k), dtype=np.float32),
+                              np.zeros(nq, dtype=np.uint32), np.zeros(nq, dtype=np.uint64))
+    if on_dev and stream is None:
+        stream = torch.cuda.current_stream(ids.device)
+    check(lib().prag_gpu_merge_topk(_ptr(ids), _ptr(dist), _ptr(count), _ptr(scanned), nparts, nq, kin, k,
+                                    _ptr(out.ids), _ptr(out.dist), _ptr(out.count), _ptr(out.scanned), device,
+                                    _stream_ptr(stream)))
+    return out
+
+
+# ------------------------------------------------------ performance model
+@dataclass
+class RetrievalPerfModel:
+    """perfmodel.hpp:19-26."""
+    slope_s: float = 0.0
+    intercept_s: float = 0.0
+    fit_residual_s: float = 0.0
+    clamped: bool = False
+
+    def predict(self, nprobe: int) -> float:
+        return self.slope_s * nprobe + self.intercept_s
+
+    def _c(self) -> PerfModelC:
+        return PerfModelC(self.slope_s, self.intercept_s, self.fit_residual_s, int(self.clamped), 0)
+
+    @classmethod
+    def _from_c(cls, m: PerfModelC) -> "RetrievalPerfModel":
+        return cls(m.slope_s, m.intercept_s, m.fit_residual_s, bool(m.clamped))
+
+
+def calibrate_retrieval(retrieve: Callable[[int], float], nprobe_grid: Iterable[int], repeats: int = 5,
+                        warmups: int = 2) -> RetrievalPerfModel:
+    """perfmodel.hpp:92-117 over a caller-supplied timer (its std::function hook)."""
+    grid = np.ascontiguousarray(list(nprobe_grid), dtype=np.uint32)
+    errors = []
+
+    def cb(nprobe, _ctx):
+        try:
+            return float(retrieve(int(nprobe)))
+        except Exception as e:  # surface Python errors after the C call returns
+            errors.append(e)
+            return 0.0
+
+    fn = MEASURE_FN(cb)
+    m = PerfModelC()
+    check(lib().prag_gpu_calibrate_with(fn, None, _ptr(grid), len(grid), repeats, warmups, C.byref(m)))
+    if errors:
+        raise errors[0]
+    return RetrievalPerfModel._from_c(m)
+
+
+def calibrate_gpu(index: GpuIndex, queries, k: int, nprobe_grid: Iterable[int], repeats: int = 5,
+                  warmups: int = 2):
+    """calibrate_retrieval fed with the GPU batch-latency curve (host queries in,
+    host results out, wall clock per batch). Returns (model, {nprobe: median_s})."""
+    q = np.ascontiguousarray(queries, dtype=np.float32).reshape(-1, index.d)
+    grid = np.ascontiguousarray(list(nprobe_grid), dtype=np.uint32)
+    uniq = np.unique(grid)
+    lat = np.zeros(max(1, len(uniq)), dtype=np.float64)
+    m = PerfModelC()
+    check(lib().prag_gpu_calibrate_retrieval(index._h, _ptr(q), q.shape[0], k, _ptr(grid), len(grid), repeats,
+                                             warmups, C.byref(m), _ptr(lat)))
+    return RetrievalPerfModel._from_c(m), {int(n): float(t) for n, t in zip(uniq, lat)}
+
+
+def select_nprobe(model: RetrievalPerfModel, budget_s: float, nlist: int, safety_margin: float = 0.10) -> int:
+    """perfmodel.hpp:148-157."""
+    m = model._c()
+    return int(lib().prag_gpu_select_nprobe(C.byref(m), budget_s, nlist, safety_margin))
+
+
+def store_perf_model(model: RetrievalPerfModel, path: str, inference_buckets=()) -> None:
+    """Same JSON schema as perfmodel.hpp:190-202 (clamped is not serialised)."""
+    j = {"slope_s": model.slope_s, "intercept_s": model.intercept_s, "fit_residual_s": model.fit_residual_s,
+         "inference_buckets": [dict(b) for b in inference_buckets]}
+    with open(path, "w") as f:
+        f.write(json.dumps(j, indent=2) + "\n")
+
+
+def load_perf_model(path: str) -> RetrievalPerfModel:
+    """perfmodel.hpp:204-223 (retrieval part)."""
+    try:
+        with open(path) as f:
+            j = json.load(f)
+    except OSError:
+        raise FormatError("cannot open for reading: " + path)
+    except json.JSONDecodeError as e:
+        raise FormatError(f"invalid perf model JSON in {path}: {e}")
+    return RetrievalPerfModel(float(j["slope_s"]), float(j["intercept_s"]), float(j["fit_residual_s"]))

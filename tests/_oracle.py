@@ -115,9 +115,12 @@ class OracleIndex:
         self.nlist, self.d, self.nsq, self.sub_dim = hdr[0], hdr[1], hdr[2], hdr[3]
 
     def __del__(self):
-        if getattr(self, "h", None):
-            lib().ora_free_index(self.h)
-            self.h = None
+        try:
+            if getattr(self, "h", None):
+                lib().ora_free_index(self.h)
+                self.h = None
+        except Exception:
+            pass
 
     def search(self, queries: np.ndarray, nprobe: int, k: int, threads: int = 0):
         q = np.ascontiguousarray(queries, dtype=np.float32).reshape(-1, self.d)

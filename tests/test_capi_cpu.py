@@ -1,0 +1,133 @@
+"""CPU-side checks of the C ABI library (no GPU needed): it loads, exports
+every symbol include/prag_gpu.h declares, refuses to compute without a device
+(no CPU fallback), and its host-only logic (shard planning, performance
+model) matches the reference behaviour (test_perfmodel.cpp KATs)."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2403_05676_b200 as pg
+from paper_2403_05676_b200 import _lib
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    src = open(os.path.join(REPO, "include", "prag_gpu.h")).read()
+    return sorted(set(re.findall(r"\b(prag_gpu_[a-z_]+)\s*\(", src)) - {"prag_gpu_measure_fn"})
+
+
+def test_library_exports_every_header_symbol():
+    L = C.CDLL(_lib.LIB_PATH)
+    syms = header_symbols()
+    assert len(syms) >= 18
+    for s in syms:
+        assert hasattr(L, s), s
+    bound = {n for n, _, _ in _lib.SYMBOLS}
+    assert set(syms) <= bound
+
+
+def test_no_cpu_fallback_without_device(tmp_path):
+    if pg.device_count() > 0:
+        pytest.skip("GPU present")
+    p = os.path.join(REPO, "tests", "golden", "four_points.pragix")
+    with pytest.raises(pg.NoDeviceError):
+        pg.GpuIndex.load(p)
+    with pytest.raises(pg.NoDeviceError):
+        pg.merge_topk(np.zeros((1, 1, 1), np.uint64), np.zeros((1, 1, 1), np.float32),
+                      np.zeros((1, 1), np.uint32), None, 1)
+
+
+def test_plan_shards_lpt():
+    rng = np.random.default_rng(0)
+    sizes = rng.integers(0, 5000, size=1000).astype(np.uint64)
+    for world in (1, 2, 4, 8):
+        owner = pg.plan_shards(sizes, world)
+        assert owner.max() < world
+        loads = np.bincount(owner, weights=sizes.astype(np.float64), minlength=world)
+        # LPT bound: max load <= mean + largest item
+        assert loads.max() <= sizes.sum() / world + sizes.max()
+        # restatement: descending size (stable), least-loaded shard (lowest rank on ties)
+        order = sorted(range(len(sizes)), key=lambda l: (-int(sizes[l]), l))
+        load = [0] * world
+        ref = np.zeros(len(sizes), np.uint32)
+        for l in order:
+            r = min(range(world), key=lambda i: (load[i], i))
+            ref[l] = r
+            load[r] += int(sizes[l])
+        np.testing.assert_array_equal(owner, ref)
+    with pytest.raises(pg.ConfigError):
+        pg.plan_shards(sizes, 0)
+
+
+def test_select_nprobe_kats():
+    """test_perfmodel.cpp:54-68."""
+    m = pg.RetrievalPerfModel(0.5e-3, 2e-3, 0.0, False)
+    assert pg.select_nprobe(m, 10e-3, 1024, 0.0) == 16
+    assert pg.select_nprobe(m, 10e-3, 1024) == 14
+    assert pg.select_nprobe(m, 10e-3, 8, 0.0) == 8
+    assert pg.select_nprobe(m, 1e-3, 1024) == 1
+    assert pg.select_nprobe(m, 0.0, 1024) == 1
+    assert pg.select_nprobe(pg.RetrievalPerfModel(0.0, 2e-3), 10e-3, 64) == 64
+
+
+def test_select_nprobe_monotone():
+    """test_perfmodel.cpp:70-79."""
+    m = pg.RetrievalPerfModel(0.3e-3, 1e-3)
+    prev = 0
+    for b in np.arange(0.0, 50e-3 + 1e-12, 0.5e-3):
+        n = pg.select_nprobe(m, float(b), 128)
+        assert n >= max(prev, 1) and n <= 128
+        prev = n
+
+
+def test_calibrate_exact_line():
+    """test_perfmodel.cpp:11-19."""
+    m = pg.calibrate_retrieval(lambda n: 2e-3 + 0.5e-3 * n, [1, 2, 4, 8, 16, 32])
+    assert m.slope_s == pytest.approx(0.5e-3, rel=0.01)
+    assert m.intercept_s == pytest.approx(2e-3, rel=0.01)
+    assert m.fit_residual_s < 1e-9 and not m.clamped
+    assert m.predict(10) == pytest.approx(7e-3)
+
+
+def test_calibrate_median_robust():
+    """test_perfmodel.cpp:21-32."""
+    calls = [0]
+
+    def timer(n):
+        calls[0] += 1
+        t = 1e-3 * n
+        if calls[0] % 5 == 0:
+            t += 50e-3
+        return t
+    m = pg.calibrate_retrieval(timer, [1, 2, 4, 8], 5)
+    assert m.slope_s == pytest.approx(1e-3, rel=0.05)
+
+
+def test_calibrate_clamp_and_validation():
+    """test_perfmodel.cpp:34-52."""
+    m = pg.calibrate_retrieval(lambda n: 5e-3, [1, 4, 16])
+    assert abs(m.slope_s) < 1e-12 and m.intercept_s == pytest.approx(5e-3) and not m.clamped
+    m = pg.calibrate_retrieval(lambda n: 10e-3 - 0.1e-3 * n, [1, 4, 16])
+    assert m.slope_s == 0.0 and m.clamped
+    with pytest.raises(pg.ConfigError):
+        pg.calibrate_retrieval(lambda n: 1e-3, [4])
+    with pytest.raises(pg.ConfigError):
+        pg.calibrate_retrieval(lambda n: 1e-3, [4, 4, 4])
+    with pytest.raises(pg.ConfigError):
+        pg.calibrate_retrieval(lambda n: 1e-3, [1, 2], 2)
+
+
+def test_perf_model_json_roundtrip(tmp_path):
+    """perfmodel.hpp:190-223 schema (clamped not serialised)."""
+    m = pg.RetrievalPerfModel(1.25e-4, 3e-5, 1e-6, True)
+    p = str(tmp_path / "perf.json")
+    pg.store_perf_model(m, p)
+    back = pg.load_perf_model(p)
+    assert (back.slope_s, back.intercept_s, back.fit_residual_s) == (m.slope_s, m.intercept_s, m.fit_residual_s)
+    assert back.clamped is False
+    with pytest.raises(pg.FormatError):
+        pg.load_perf_model(str(tmp_path / "missing.json"))
