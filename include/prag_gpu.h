@@ -176,6 +176,10 @@ uint32_t prag_gpu_select_nprobe(const prag_gpu_perf_model* model, double budget_
                                 double safety_margin);
 
 /* ------------------------------------------------------------ profiling */
+/* Scan-path selection: 0 = automatic (lane-skewed fused fast path for
+ * m = 32 / 64 and k <= 32, generic otherwise), 1 = always the generic path
+ * (used by the parity suite to check both paths against each other). */
+int prag_gpu_set_scan_path(prag_gpu_index* index, int path);
 int prag_gpu_set_profiling(prag_gpu_index* index, int enabled);
 int prag_gpu_last_timings(const prag_gpu_index* index, prag_gpu_timings* out);
 

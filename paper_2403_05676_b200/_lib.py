@@ -90,6 +90,7 @@ SYMBOLS = [
     ("prag_gpu_calibrate_with", C.c_int,
      [MEASURE_FN, P, P, C.c_uint32, C.c_int, C.c_int, C.POINTER(PerfModelC)]),
     ("prag_gpu_select_nprobe", C.c_uint32, [C.POINTER(PerfModelC), C.c_double, C.c_uint32, C.c_double]),
+    ("prag_gpu_set_scan_path", C.c_int, [P, C.c_int]),
     ("prag_gpu_set_profiling", C.c_int, [P, C.c_int]),
     ("prag_gpu_last_timings", C.c_int, [P, C.POINTER(Timings)]),
 ]

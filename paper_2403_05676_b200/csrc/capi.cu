@@ -74,11 +74,15 @@ int dmalloc(T** p, size_t n, uint64_t* acct) {
 void free_device_index(DeviceIndex& d) {
     cudaFree(d.centroids);
     cudaFree(d.centroidsT);
+    cudaFree(d.centroids4);
     cudaFree(d.codewordsT);
     cudaFree(d.list_off);
     cudaFree(d.list_len);
     cudaFree(d.ids);
     cudaFree(d.codes);
+    cudaFree(d.codewords);
+    cudaFree(d.skew_off);
+    cudaFree(d.skew_codes);
     d = DeviceIndex{};
 }
 
@@ -144,6 +148,13 @@ int upload(prag_gpu_index* ix, const HostIndex& h) {
                     t[(size_t(s) * h.sub_dim + j) * 256 + c] = h.codewords[(size_t(s) * 256 + c) * h.sub_dim + j];
         PG_CUDA(cudaMemcpy(d.codewordsT, t.data(), t.size() * 4, cudaMemcpyHostToDevice));
     }
+    if (h.d % 4 == 0) {
+        std::vector<float> t(size_t(nl) * h.d);
+        for (uint32_t c = 0; c < nl; ++c)
+            for (uint32_t j = 0; j < h.d; ++j) t[(size_t(j / 4) * nl + c) * 4 + (j % 4)] = h.centroids[size_t(c) * h.d + j];
+        PG_TRY(dmalloc(&d.centroids4, t.size(), acct));
+        PG_CUDA(cudaMemcpy(d.centroids4, t.data(), t.size() * 4, cudaMemcpyHostToDevice));
+    }
     PG_CUDA(cudaMemcpy(d.list_off, off.data(), off.size() * 8, cudaMemcpyHostToDevice));
     PG_CUDA(cudaMemcpy(d.list_len, len.data(), len.size() * 4, cudaMemcpyHostToDevice));
     {
@@ -159,6 +170,18 @@ int upload(prag_gpu_index* ix, const HostIndex& h) {
         PG_CUDA(cudaMemcpy(d.codes, pcode.data(), pcode.size(), cudaMemcpyHostToDevice));
     }
     d.code_layout = 0;
+    PG_TRY(dmalloc(&d.codewords, h.codewords.size(), acct));
+    PG_CUDA(cudaMemcpy(d.codewords, h.codewords.data(), h.codewords.size() * 4, cudaMemcpyHostToDevice));
+    if ((h.nsq == 32 || h.nsq == 64) && h.sub_dim <= 16) {
+        std::vector<uint64_t> soff;
+        std::vector<uint8_t> scodes;
+        build_skew_layout(h, h.nsq, soff, scodes);
+        PG_TRY(dmalloc(&d.skew_off, soff.size(), acct));
+        PG_TRY(dmalloc(&d.skew_codes, scodes.size(), acct));
+        PG_CUDA(cudaMemcpy(d.skew_off, soff.data(), soff.size() * 8, cudaMemcpyHostToDevice));
+        PG_CUDA(cudaMemcpy(d.skew_codes, scodes.data(), scodes.size(), cudaMemcpyHostToDevice));
+        d.code_layout = 1;
+    }
     return PRAG_GPU_OK;
 }
 
@@ -267,12 +290,109 @@ int blocks_per_sm_scan(const prag_gpu_index* ix) {
     return std::max(1, std::min(per, 8));
 }
 
+// Fast path (m = 32 / 64, k <= 32): coarse -> top-nprobe -> plan -> LUT
+// images -> fused conflict-free scan + warp top-k -> pool select.
+int search_pass_skew(prag_gpu_index* ix, Workspace* w, const float* dq, uint32_t nq, uint32_t nprobe, uint32_t k,
+                     uint64_t* o_ids, float* o_dist, uint32_t* o_count, uint64_t* o_scanned, cudaStream_t s,
+                     prag_gpu_timings* tm) {
+    const DeviceIndex& d = ix->dev;
+    const uint32_t R = d.nsq / 32;
+    const uint32_t IT = skew_item_tiles();
+    const uint64_t max_tiles_q = (ix->top_prefix[nprobe] + 31) / 32 + nprobe;
+    const uint64_t item_cap = uint64_t(nq) * (nprobe + max_tiles_q / IT + 1) + 1;
+    const uint32_t warps = skew_warps(d.nsq);
+    const uint64_t pool_cap = item_cap * warps * k;
+    const uint32_t pw_p = pow2_at_least(nprobe);
+    const uint32_t pw_f = pow2_at_least(std::max<uint64_t>(1, std::min<uint64_t>(k, pool_cap)));
+    const uint64_t img_floats = uint64_t(nq) * nprobe * d.nsq * 256;  // compact LUTs [pair][sq][256]
+    (void)R;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ix->device);
+    const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>(item_cap, uint64_t(sms) * skew_ctas_per_sm(d.nsq))));
+    size_t need;
+    {
+        Carver c{nullptr};
+        c.take<float>(size_t(nq) * d.nlist);
+        c.take<uint32_t>(size_t(nq) * nprobe);
+        c.take<float>(size_t(nq) * nprobe);
+        c.take<uint32_t>(size_t(nq) * pw_p);
+        c.take<uint64_t>(size_t(nq) * pw_p);
+        c.take<uint4>(item_cap);
+        c.take<uint32_t>(2);
+        c.take<uint32_t>(size_t(nq) + 1);
+        c.take<uint32_t>(nq);
+        c.take<uint32_t>(nq);
+        c.take<uint32_t>(pool_cap);
+        c.take<uint64_t>(pool_cap);
+        c.take<uint32_t>(size_t(nq) * pw_f);
+        c.take<uint64_t>(size_t(nq) * pw_f);
+        c.take<float>(img_floats);
+        need = c.off + 1024;
+    }
+    PG_TRY(ws_reserve(w, need, s));
+    Carver c{static_cast<char*>(w->buf)};
+    float* coarse = c.take<float>(size_t(nq) * d.nlist);
+    uint32_t* probe = c.take<uint32_t>(size_t(nq) * nprobe);
+    float* probe_dist = c.take<float>(size_t(nq) * nprobe);
+    uint32_t* pkey = c.take<uint32_t>(size_t(nq) * pw_p);
+    uint64_t* ptie = c.take<uint64_t>(size_t(nq) * pw_p);
+    uint4* items = c.take<uint4>(item_cap);
+    uint32_t* ctr = c.take<uint32_t>(2);
+    uint32_t* q_item_off = c.take<uint32_t>(size_t(nq) + 1);
+    uint32_t* gthr = c.take<uint32_t>(nq);
+    uint32_t* pool_cnt = c.take<uint32_t>(nq);
+    uint32_t* pool_key = c.take<uint32_t>(pool_cap);
+    uint64_t* pool_id = c.take<uint64_t>(pool_cap);
+    uint32_t* fkey = c.take<uint32_t>(size_t(nq) * pw_f);
+    uint64_t* ftie = c.take<uint64_t>(size_t(nq) * pw_f);
+    float* images = c.take<float>(img_floats);
+
+    const bool prof = tm != nullptr;
+    if (prof) cudaEventRecord(w->ev[0], s);
+    PG_TRY(launch_coarse(d, dq, nq, coarse, s));
+    if (prof) cudaEventRecord(w->ev[1], s);
+    PG_TRY(launch_select_probe(d, coarse, nq, nprobe, probe, probe_dist, pkey, ptie, s));
+    if (prof) cudaEventRecord(w->ev[2], s);
+    PG_TRY(launch_plan_skew(d, probe, nq, nprobe, o_scanned, items, ctr, ctr + 1, q_item_off, gthr, pool_cnt,
+                            item_cap, s));
+    PG_TRY(launch_lut_images(d, dq, probe, nq, nprobe, images, s));
+    if (prof) cudaEventRecord(w->ev[3], s);
+    PG_TRY(launch_scan_skew(d, items, ctr, ctr + 1, probe, images, nprobe, k, gthr, q_item_off, pool_cnt, pool_key,
+                            pool_id, grid, s));
+    if (prof) cudaEventRecord(w->ev[4], s);
+    PG_TRY(launch_select_pool(pool_key, pool_id, pool_cnt, q_item_off, warps, nq, k, o_ids, o_dist, o_count, fkey,
+                              ftie, pw_f, s));
+    if (prof) {
+        cudaEventRecord(w->ev[5], s);
+        PG_CUDA(cudaEventSynchronize(w->ev[5]));
+        float t[5];
+        for (int i = 0; i < 5; ++i) cudaEventElapsedTime(&t[i], w->ev[i], w->ev[i + 1]);
+        float tot;
+        cudaEventElapsedTime(&tot, w->ev[0], w->ev[5]);
+        tm->coarse_ms += t[0];
+        tm->select_ms += t[1];
+        tm->plan_ms += t[2];  // plan + LUT images
+        tm->scan_ms += t[3];
+        tm->final_ms += t[4];
+        tm->total_ms += tot;
+        std::vector<uint64_t> sc(nq);
+        PG_CUDA(cudaMemcpy(sc.data(), o_scanned, nq * 8, cudaMemcpyDeviceToHost));
+        for (uint64_t v : sc) tm->scanned_bytes += v * d.nsq;
+        uint32_t ni = 0;
+        PG_CUDA(cudaMemcpy(&ni, ctr, 4, cudaMemcpyDeviceToHost));
+        tm->work_items += ni;
+    }
+    return PRAG_GPU_OK;
+}
+
 // One pass over nq (<= chunk) device-resident queries. Outputs are device
 // pointers. All launches on stream s.
 int search_pass(prag_gpu_index* ix, Workspace* w, const float* dq, uint32_t nq, uint32_t nprobe, uint32_t k,
                 uint64_t* o_ids, float* o_dist, uint32_t* o_count, uint64_t* o_scanned, cudaStream_t s,
                 prag_gpu_timings* tm) {
     const DeviceIndex& d = ix->dev;
+    if (d.code_layout == 1 && k <= 32 && ix->scan_path == 0)
+        return search_pass_skew(ix, w, dq, nq, nprobe, k, o_ids, o_dist, o_count, o_scanned, s, tm);
     const uint64_t max_cand_q = ix->top_prefix[nprobe];
     const uint64_t cand_cap = std::max<uint64_t>(1, max_cand_q * nq);
     const uint32_t C = scan_chunk();
@@ -395,7 +515,12 @@ int do_search(prag_gpu_index* ix, const float* queries, uint32_t nq, uint32_t np
     // Bound candidate memory: chunk the batch so a pass holds <= 192M slots.
     const uint64_t max_cand_q = std::max<uint64_t>(1, ix->top_prefix[nprobe]);
     const uint64_t kSlots = 192ull << 20;
-    const uint32_t chunk = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(nq, kSlots / max_cand_q)));
+    uint32_t chunk = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(nq, kSlots / max_cand_q)));
+    if (d.code_layout == 1 && k <= 32 && ix->scan_path == 0) {
+        // fast path: bound the per-pass LUT images (nq * nprobe * m KB * 2) to ~1 GiB
+        const uint64_t img_q = uint64_t(nprobe) * d.nsq * 1024;
+        chunk = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(nq, (1ull << 30) / img_q)));
+    }
 
     Workspace* w = acquire_ws(ix, s);
     struct Rel {
@@ -863,6 +988,15 @@ uint32_t prag_gpu_select_nprobe(const prag_gpu_perf_model* m, double budget_s, u
     const double max_n = (limit - m->intercept_s) / m->slope_s;
     if (max_n >= double(nlist)) return nlist;
     return uint32_t(std::max(1.0, std::floor(max_n + 1e-9)));
+}
+
+int prag_gpu_set_scan_path(prag_gpu_index* ix, int path) {
+    if (!ix || path < 0 || path > 1) {
+        set_error("scan path must be 0 (auto) or 1 (generic)");
+        return PRAG_GPU_CONFIG;
+    }
+    ix->scan_path = path;
+    return PRAG_GPU_OK;
 }
 
 int prag_gpu_set_profiling(prag_gpu_index* ix, int enabled) {

@@ -65,12 +65,16 @@ struct DeviceIndex {
     uint32_t max_list_len = 0;
     float* centroids = nullptr;   // [nlist][d]
     float* centroidsT = nullptr;  // [d][nlist] (coalesced coarse scan)
+    float* centroids4 = nullptr;  // [d/4][nlist][4] (vectorised coarse scan, d % 4 == 0)
     float* codewordsT = nullptr;  // [nsq][sub_dim][256]
     uint64_t* list_off = nullptr; // [nlist+1] padded slot offsets
     uint32_t* list_len = nullptr; // [nlist]
     uint64_t* ids = nullptr;      // [npadded]
     uint8_t* codes = nullptr;     // plain: [npadded][nsq]; skewed: see kernels.cu
-    uint32_t code_layout = 0;
+    uint32_t code_layout = 0;     // 1: skew_codes present (m = 32 / 64 fast path)
+    float* codewords = nullptr;   // [nsq][256][sub_dim] (LUT-image kernel)
+    uint64_t* skew_off = nullptr; // [nlist+1] tile offsets into skew_codes
+    uint8_t* skew_codes = nullptr;
 };
 
 // ------------------------------------------------------------ workspace
@@ -108,6 +112,7 @@ struct prag_gpu_index {
     std::vector<uint64_t> top_prefix;             // prefix sums of sizes sorted desc
     uint64_t device_bytes = 0;
     bool profiling = false;
+    int scan_path = 0;                            // 0 auto, 1 force generic
     prag_gpu_timings last{};
     std::mutex mu;                                // guards pool and `last`
     std::vector<pg::Workspace*> pool;
@@ -151,6 +156,24 @@ int launch_merge(const uint64_t* ids, const float* dist, const uint32_t* count, 
                  uint32_t* out_count, uint64_t* out_scanned, uint32_t* ckey, uint64_t* ctie, uint32_t* gkey,
                  uint64_t* gtie, uint32_t pw, cudaStream_t s);
 uint32_t scan_chunk();
+// fast path (scan_skew.cu)
+int launch_plan_skew(const DeviceIndex& ix, const uint32_t* probe, uint32_t nq, uint32_t nprobe,
+                     uint64_t* scanned, uint4* items, uint32_t* num_items, uint32_t* cursor, uint32_t* q_item_off,
+                     uint32_t* gthr, uint32_t* pool_cnt, uint64_t item_cap, cudaStream_t s);
+int launch_lut_images(const DeviceIndex& ix, const float* queries, const uint32_t* probe, uint32_t nq,
+                      uint32_t nprobe, float* images, cudaStream_t s);
+int launch_scan_skew(const DeviceIndex& ix, const uint4* items, const uint32_t* num_items, uint32_t* cursor,
+                     const uint32_t* probe, const float* images, uint32_t nprobe, uint32_t k, uint32_t* gthr,
+                     const uint32_t* q_item_off, uint32_t* pool_cnt, uint32_t* pool_key, uint64_t* pool_id,
+                     int grid, cudaStream_t s);
+int launch_select_pool(const uint32_t* pool_key, const uint64_t* pool_id, const uint32_t* pool_cnt,
+                       const uint32_t* q_item_off, uint32_t warps, uint32_t nq, uint32_t k, uint64_t* out_ids,
+                       float* out_dist, uint32_t* out_count, uint32_t* gkey, uint64_t* gtie, uint32_t pw,
+                       cudaStream_t s);
+uint32_t skew_item_tiles();
+uint32_t skew_warps(uint32_t m);
+uint32_t skew_ctas_per_sm(uint32_t m);
+void build_skew_layout(const HostIndex& h, uint32_t m, std::vector<uint64_t>& skew_off, std::vector<uint8_t>& out);
 uint32_t sort_cap();
 size_t select_smem_bytes();
 

@@ -73,6 +73,62 @@ __global__ void __launch_bounds__(128) coarse_exact_kernel(const float* __restri
         if (q0 + qi < nq) out[size_t(q0 + qi) * nlist + c] = acc[qi];
 }
 
+// Same fold, vectorised for d % 4 == 0: centroids as float4 per thread from
+// [d/4][nlist] (one LDG.128 per 4 dims), queries as [d][4] in SMEM (one
+// LDS.128 broadcast per dim), q - c for two queries per FADD2 (exact: one
+// rounding per difference); squares and the fold stay scalar FMUL/FADD.
+__device__ __forceinline__ void sub2_bc(float a0, float a1, float b, float& d0, float& d1) {
+    unsigned long long out;
+    asm("{.reg .b64 A, B;\n"
+        " mov.b64 A, {%1, %2};\n"
+        " mov.b64 B, {%3, %3};\n"
+        " sub.rn.f32x2 %0, A, B;}"
+        : "=l"(out)
+        : "f"(a0), "f"(a1), "f"(b));
+    d0 = __uint_as_float(uint32_t(out));
+    d1 = __uint_as_float(uint32_t(out >> 32));
+}
+
+// Thread = one centroid x 2 queries (more warps than a wider query block:
+// the kernel is latency-bound on the centroid stream from L2).
+__global__ void __launch_bounds__(128) coarse_exact4_kernel(const float4* __restrict__ cent4,
+                                                            const float* __restrict__ queries, uint32_t nq,
+                                                            uint32_t nlist, uint32_t d, float* __restrict__ out) {
+    extern __shared__ __align__(16) float sq2[];  // [d][2]
+    const uint32_t q0 = blockIdx.y * 2;
+    for (uint32_t i = threadIdx.x; i < 2 * d; i += blockDim.x) {
+        const uint32_t qi = i & 1u, j = i >> 1;
+        sq2[i] = (q0 + qi < nq) ? queries[size_t(q0 + qi) * d + j] : 0.0f;
+    }
+    __syncthreads();
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nlist) return;
+    float a0 = 0.0f, a1 = 0.0f;
+    const float4* colp = cent4 + c;
+    const uint32_t d4 = d >> 2;
+#pragma unroll 8
+    for (uint32_t jj = 0; jj < d4; ++jj) {
+        const float4 cv = __ldg(colp + size_t(jj) * nlist);
+        const float4 qa = *reinterpret_cast<const float4*>(sq2 + jj * 8);      // dims 4jj, 4jj+1
+        const float4 qb = *reinterpret_cast<const float4*>(sq2 + jj * 8 + 4);  // dims 4jj+2, 4jj+3
+        float d0, d1;
+        sub2_bc(qa.x, qa.y, cv.x, d0, d1);
+        a0 = __fadd_rn(a0, __fmul_rn(d0, d0));
+        a1 = __fadd_rn(a1, __fmul_rn(d1, d1));
+        sub2_bc(qa.z, qa.w, cv.y, d0, d1);
+        a0 = __fadd_rn(a0, __fmul_rn(d0, d0));
+        a1 = __fadd_rn(a1, __fmul_rn(d1, d1));
+        sub2_bc(qb.x, qb.y, cv.z, d0, d1);
+        a0 = __fadd_rn(a0, __fmul_rn(d0, d0));
+        a1 = __fadd_rn(a1, __fmul_rn(d1, d1));
+        sub2_bc(qb.z, qb.w, cv.w, d0, d1);
+        a0 = __fadd_rn(a0, __fmul_rn(d0, d0));
+        a1 = __fadd_rn(a1, __fmul_rn(d1, d1));
+    }
+    out[size_t(q0) * nlist + c] = a0;
+    if (q0 + 1 < nq) out[size_t(q0 + 1) * nlist + c] = a1;
+}
+
 // ------------------------------------------------- block-wide exact top-k
 // Selects the kk = min(k, n) smallest (key, tie) pairs of a candidate set
 // (keys from ord_key(distance), tie = list id or chunk_id) and writes them
@@ -517,7 +573,39 @@ __global__ void __launch_bounds__(kSelThreads) merge_kernel(
                out_ids + size_t(q) * k, out_count + q);
 }
 
+// K4 (fast path): exact top-k over the per-query candidate pool the fused
+// scan filled (each warp's exact top-k of its share of the lists).
+__global__ void __launch_bounds__(kSelThreads) select_pool_kernel(
+    const uint32_t* __restrict__ pool_key, const uint64_t* __restrict__ pool_id,
+    const uint32_t* __restrict__ pool_cnt, const uint32_t* __restrict__ q_item_off, uint32_t warps, uint32_t k,
+    uint64_t* __restrict__ out_ids, float* __restrict__ out_dist, uint32_t* __restrict__ out_count,
+    uint32_t* gkey, uint64_t* gtie, uint32_t pw) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    SelShared& sm = *reinterpret_cast<SelShared*>(smraw);
+    const uint32_t q = blockIdx.x;
+    const size_t off = size_t(q_item_off[q]) * warps * k;
+    MergeSrc src{pool_key + off, pool_id + off};
+    block_topk(src, pool_cnt[q], k, sm, gkey + size_t(q) * pw, gtie + size_t(q) * pw, out_dist + size_t(q) * k,
+               out_ids + size_t(q) * k, out_count + q);
+}
+
 }  // namespace
+
+int launch_select_pool(const uint32_t* pool_key, const uint64_t* pool_id, const uint32_t* pool_cnt,
+                       const uint32_t* q_item_off, uint32_t warps, uint32_t nq, uint32_t k, uint64_t* out_ids,
+                       float* out_dist, uint32_t* out_count, uint32_t* gkey, uint64_t* gtie, uint32_t pw,
+                       cudaStream_t s) {
+    PG_CUDA(cudaFuncSetAttribute(select_pool_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(sizeof(SelShared))));
+    select_pool_kernel<<<nq, kSelThreads, sizeof(SelShared), s>>>(pool_key, pool_id, pool_cnt, q_item_off, warps, k,
+                                                                   out_ids, out_dist, out_count, gkey, gtie, pw);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error(std::string("CUDA launch failed (select_pool): ") + cudaGetErrorString(e));
+        return PRAG_GPU_CUDA;
+    }
+    return PRAG_GPU_OK;
+}
 
 size_t select_smem_bytes() { return sizeof(SelShared); }
 
@@ -531,6 +619,15 @@ static int check_launch(const char* what) {
 }
 
 int launch_coarse(const DeviceIndex& ix, const float* queries, uint32_t nq, float* out, cudaStream_t s) {
+    if (ix.centroids4 != nullptr) {
+        dim3 grid((ix.nlist + 127) / 128, (nq + 1) / 2);
+        const size_t smem = size_t(2) * ix.d * sizeof(float);
+        if (smem > 48 * 1024)
+            PG_CUDA(cudaFuncSetAttribute(coarse_exact4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        coarse_exact4_kernel<<<grid, 128, smem, s>>>(reinterpret_cast<const float4*>(ix.centroids4), queries, nq,
+                                                     ix.nlist, ix.d, out);
+        return check_launch("coarse4");
+    }
     constexpr int QB = 8;
     dim3 grid((ix.nlist + 127) / 128, (nq + QB - 1) / QB);
     size_t smem = size_t(QB) * ix.d * sizeof(float);

@@ -190,6 +190,10 @@ class GpuIndex:
         check(lib().prag_gpu_probe(self._h, _ptr(q), q.shape[0], nprobe, _ptr(lists), _ptr(dist), None))
         return lists, dist
 
+    def set_scan_path(self, path: int) -> None:
+        """0 = automatic (fast lane-skewed path when eligible), 1 = generic."""
+        check(lib().prag_gpu_set_scan_path(self._h, path))
+
     # profiling -------------------------------------------------------------
     def set_profiling(self, on: bool) -> None:
         check(lib().prag_gpu_set_profiling(self._h, 1 if on else 0))

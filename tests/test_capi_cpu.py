@@ -131,3 +131,27 @@ def test_perf_model_json_roundtrip(tmp_path):
     assert back.clamped is False
     with pytest.raises(pg.FormatError):
         pg.load_perf_model(str(tmp_path / "missing.json"))
+
+
+def test_no_fma_contraction_in_sass():
+    """Exactness guard: the reference folds are
+    separately rounded mul/add; no kernel may contract them into FFMA. The
+    only fused op allowed is the scan's explicit FFMA2 with 0/1 masks
+    (x*1 + acc == acc + x exactly)."""
+    import shutil
+    import subprocess
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(exe):
+        pytest.skip("cuobjdump not available")
+    sass = subprocess.run([exe, "-sass", _lib.LIB_PATH], capture_output=True, text=True, check=True).stdout
+    func = None
+    ffma2_funcs = set()
+    for line in sass.splitlines():
+        if "Function :" in line:
+            func = line.split("Function :")[1].strip()
+        toks = line.split()
+        if any(t == "FFMA" or t.startswith("FFMA.") for t in toks):
+            raise AssertionError(f"FFMA in {func}: {line.strip()}")
+        if any(t.startswith("FFMA2") for t in toks):
+            ffma2_funcs.add(func)
+    assert ffma2_funcs and all("scan_skew_kernel" in f for f in ffma2_funcs), ffma2_funcs

@@ -39,10 +39,12 @@ def gpu():
     return 0
 
 
+@pytest.mark.parametrize("path_mode", [0, 1], ids=["auto", "generic"])
 @pytest.mark.parametrize("case", GOLDEN_CASES)
-def test_golden_reference_parity(gpu, case):
+def test_golden_reference_parity(gpu, case, path_mode):
     path, z, grid = load_golden(case)
     ix = pg.GpuIndex.load(path, gpu)
+    ix.set_scan_path(path_mode)
     q = z["queries"]
     for nprobe, k in grid:
         key = f"p{nprobe}_k{k}"
@@ -125,12 +127,15 @@ def synth(gpu, tmp_path_factory):
     return out
 
 
+@pytest.mark.parametrize("path_mode", [0, 1], ids=["auto", "generic"])
 @pytest.mark.parametrize("nsq", [32, 64])
-def test_synthetic_oracle_parity(synth, nsq):
+def test_synthetic_oracle_parity(synth, nsq, path_mode):
     p, q = synth[nsq]
     ix = pg.GpuIndex.load(p, 0)
+    ix.set_scan_path(path_mode)
+    assert ix.desc.code_layout == 1
     oi = O.OracleIndex(p)
-    for nprobe, k in [(1, 10), (16, 10), (16, 1), (64, 100), (7, 2), (256, 10)]:
+    for nprobe, k in [(1, 10), (16, 10), (16, 1), (64, 100), (7, 2), (256, 10), (16, 32), (16, 33), (3, 31)]:
         r = ix.search_batch(q, k, nprobe)
         o = oi.search(q, nprobe, k)
         assert_same(f"synth{nsq}/p{nprobe}k{k}", r.ids, r.dist, r.count, r.scanned, *o)
