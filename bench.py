@@ -215,22 +215,13 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     nq, k, nprobe = cfg["nq"], cfg["k"], cfg["nprobe"]
     qdev = torch.from_numpy(queries[:nq]).to(dev)
-    if world > 1:
-        g_ids = torch.empty((world, nq, k), dtype=torch.int64, device=dev)
-        g_dist = torch.empty((world, nq, k), dtype=torch.float32, device=dev)
-        g_cnt = torch.empty((world, nq), dtype=torch.int32, device=dev)
-        g_sc = torch.empty((world, nq), dtype=torch.int64, device=dev)
+    from paper_2403_05676_b200 import distributed as PD
 
     def step_dev(qd, nprobe_, k_):
         with torch.cuda.stream(stream):
             r = ix.search_batch(qd, k_, nprobe_, stream=stream)
-            if world > 1:
-                dist.all_gather_into_tensor(g_ids, r.ids)
-                dist.all_gather_into_tensor(g_dist, r.dist)
-                dist.all_gather_into_tensor(g_cnt, r.count)
-                dist.all_gather_into_tensor(g_sc, r.scanned)
-                if rank == 0:
-                    r = pg.merge_topk(g_ids, g_dist, g_cnt, g_sc, k_, device=local, stream=stream)
+            if world > 1:  # one packed NCCL all-gather of the per-shard top-k, exact merge on rank 0
+                r = PD.gather_merge(r, k_)
         return r
 
     def timed(fn, steps, warmup):

@@ -76,14 +76,15 @@ typedef struct prag_gpu_perf_model {
 /* Per-phase device time of the most recent search on an index with
  * profiling enabled (CUDA events on the search stream), milliseconds. */
 typedef struct prag_gpu_timings {
-    float coarse_ms;   /* K1: queries x centroids exact distances          */
-    float select_ms;   /* K1b: per-query top-nprobe                         */
+    float coarse_ms;   /* K1: queries x centroids (tcgen05 GEMM or exact SIMT) */
+    float select_ms;   /* K1b: per-query top-nprobe (window rescoring / select) */
     float plan_ms;     /* work-item plan (list sizes, prefix sums)          */
     float scan_ms;     /* K2+K3+K4: fused LUT build + list scan + top-k      */
     float final_ms;    /* per-query merge of partial top-k                  */
     float total_ms;    /* first event to last event                         */
     uint64_t scanned_bytes; /* algorithmic code bytes: sum scanned_vectors * m */
     uint64_t work_items;
+    uint64_t coarse_window; /* lists rescored exactly by K1b (tensor-core path), summed over queries */
 } prag_gpu_timings;
 
 /* ---------------------------------------------------------------- errors */
@@ -180,6 +181,11 @@ uint32_t prag_gpu_select_nprobe(const prag_gpu_perf_model* model, double budget_
  * m = 32 / 64 and k <= 32, generic otherwise), 1 = always the generic path
  * (used by the parity suite to check both paths against each other). */
 int prag_gpu_set_scan_path(prag_gpu_index* index, int path);
+/* Coarse-quantizer selection: 0 = automatic (tcgen05 tensor-core pre-filter
+ * + exact rescoring of the boundary window when nlist % 128 == 0,
+ * d % 32 == 0 and nprobe <= 256), 1 = always the exact SIMT scan of every
+ * centroid. Both return identical probe lists. */
+int prag_gpu_set_coarse_path(prag_gpu_index* index, int path);
 int prag_gpu_set_profiling(prag_gpu_index* index, int enabled);
 int prag_gpu_last_timings(const prag_gpu_index* index, prag_gpu_timings* out);
 

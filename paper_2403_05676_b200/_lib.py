@@ -61,7 +61,7 @@ class PerfModelC(C.Structure):
 class Timings(C.Structure):
     _fields_ = [("coarse_ms", C.c_float), ("select_ms", C.c_float), ("plan_ms", C.c_float),
                 ("scan_ms", C.c_float), ("final_ms", C.c_float), ("total_ms", C.c_float),
-                ("scanned_bytes", C.c_uint64), ("work_items", C.c_uint64)]
+                ("scanned_bytes", C.c_uint64), ("work_items", C.c_uint64), ("coarse_window", C.c_uint64)]
 
 
 MEASURE_FN = C.CFUNCTYPE(C.c_double, C.c_uint32, C.c_void_p)
@@ -91,6 +91,7 @@ SYMBOLS = [
      [MEASURE_FN, P, P, C.c_uint32, C.c_int, C.c_int, C.POINTER(PerfModelC)]),
     ("prag_gpu_select_nprobe", C.c_uint32, [C.POINTER(PerfModelC), C.c_double, C.c_uint32, C.c_double]),
     ("prag_gpu_set_scan_path", C.c_int, [P, C.c_int]),
+    ("prag_gpu_set_coarse_path", C.c_int, [P, C.c_int]),
     ("prag_gpu_set_profiling", C.c_int, [P, C.c_int]),
     ("prag_gpu_last_timings", C.c_int, [P, C.POINTER(Timings)]),
 ]

@@ -83,6 +83,8 @@ void free_device_index(DeviceIndex& d) {
     cudaFree(d.codewords);
     cudaFree(d.skew_off);
     cudaFree(d.skew_codes);
+    cudaFree(d.cent_tc);
+    cudaFree(d.cent_norm);
     d = DeviceIndex{};
 }
 
@@ -181,6 +183,15 @@ int upload(prag_gpu_index* ix, const HostIndex& h) {
         PG_CUDA(cudaMemcpy(d.skew_off, soff.data(), soff.size() * 8, cudaMemcpyHostToDevice));
         PG_CUDA(cudaMemcpy(d.skew_codes, scodes.data(), scodes.size(), cudaMemcpyHostToDevice));
         d.code_layout = 1;
+    }
+    if (tc_coarse_supported(nl, h.d)) {
+        std::vector<float> tc, norms;
+        build_tc_centroids(h.centroids.data(), nl, h.d, tc, norms);
+        PG_TRY(dmalloc(&d.cent_tc, tc.size(), acct));
+        PG_TRY(dmalloc(&d.cent_norm, norms.size(), acct));
+        PG_CUDA(cudaMemcpy(d.cent_tc, tc.data(), tc.size() * 4, cudaMemcpyHostToDevice));
+        PG_CUDA(cudaMemcpy(d.cent_norm, norms.data(), norms.size() * 4, cudaMemcpyHostToDevice));
+        d.tc_ok = true;
     }
     return PRAG_GPU_OK;
 }
@@ -290,29 +301,62 @@ int blocks_per_sm_scan(const prag_gpu_index* ix) {
     return std::max(1, std::min(per, 8));
 }
 
+// K1 + K1b: the first nprobe lists of each query in (distance, list id)
+// order. Tensor-core pre-filter + exact window rescoring when the shape
+// allows (coarse_tc.cu), else the exact SIMT scan of every centroid.
+// Scratch: coarse holds coarse_scratch_floats() (K1's per-slice partial dot
+// products, or the exact distances); pkey/ptie nq * pw.
+bool use_tc_coarse(const prag_gpu_index* ix, uint32_t nprobe) {
+    return ix->dev.tc_ok && ix->coarse_path == 0 && nprobe <= kTcMaxNprobe;
+}
+
+size_t coarse_scratch_floats(const prag_gpu_index* ix, uint32_t nq) {
+    return size_t(nq) * ix->dev.nlist * (ix->dev.tc_ok ? std::max<uint32_t>(1, tc_slices(ix->dev.d)) : 1);
+}
+
+int run_coarse(const prag_gpu_index* ix, const float* dq, uint32_t nq, uint32_t nprobe, float* coarse,
+               uint32_t* probe, float* probe_dist, uint32_t* pkey, uint64_t* ptie, cudaStream_t s,
+               Workspace* prof_ws = nullptr) {
+    const DeviceIndex& d = ix->dev;
+    unsigned long long* win_stat = nullptr;
+    if (prof_ws) {  // profiling: event between K1 and K1b, window-size counter
+        if (!prof_ws->win_stat) PG_CUDA(cudaMalloc(&prof_ws->win_stat, 8));
+        PG_CUDA(cudaMemsetAsync(prof_ws->win_stat, 0, 8, s));
+        win_stat = prof_ws->win_stat;
+    }
+    if (use_tc_coarse(ix, nprobe)) {
+        PG_TRY(launch_coarse_tc(d, dq, nq, coarse, s));
+        if (prof_ws) cudaEventRecord(prof_ws->ev[1], s);
+        return launch_select_window(d, coarse, dq, nq, nprobe, probe, probe_dist, win_stat, s);
+    }
+    PG_TRY(launch_coarse(d, dq, nq, coarse, s));
+    if (prof_ws) cudaEventRecord(prof_ws->ev[1], s);
+    return launch_select_probe(d, coarse, nq, nprobe, probe, probe_dist, pkey, ptie, s);
+}
+
 // Fast path (m = 32 / 64, k <= 32): coarse -> top-nprobe -> plan -> LUT
 // images -> fused conflict-free scan + warp top-k -> pool select.
 int search_pass_skew(prag_gpu_index* ix, Workspace* w, const float* dq, uint32_t nq, uint32_t nprobe, uint32_t k,
                      uint64_t* o_ids, float* o_dist, uint32_t* o_count, uint64_t* o_scanned, cudaStream_t s,
                      prag_gpu_timings* tm) {
     const DeviceIndex& d = ix->dev;
-    const uint32_t R = d.nsq / 32;
-    const uint32_t IT = skew_item_tiles();
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ix->device);
+    const int grid = sms;  // persistent: one CTA per SM
+    // item size from the worst-case tile count of this shape (host-side, so a
+    // given (nq, nprobe) always plans the same way)
     const uint64_t max_tiles_q = (ix->top_prefix[nprobe] + 31) / 32 + nprobe;
+    const uint32_t IT = skew_item_tiles(uint64_t(nq) * max_tiles_q, uint32_t(grid));
     const uint64_t item_cap = uint64_t(nq) * (nprobe + max_tiles_q / IT + 1) + 1;
     const uint32_t warps = skew_warps(d.nsq);
     const uint64_t pool_cap = item_cap * warps * k;
     const uint32_t pw_p = pow2_at_least(nprobe);
     const uint32_t pw_f = pow2_at_least(std::max<uint64_t>(1, std::min<uint64_t>(k, pool_cap)));
-    const uint64_t img_floats = uint64_t(nq) * nprobe * d.nsq * 256;  // compact LUTs [pair][sq][256]
-    (void)R;
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ix->device);
-    const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>(item_cap, uint64_t(sms) * skew_ctas_per_sm(d.nsq))));
+    const uint64_t img_floats = uint64_t(nq) * nprobe * (skew_lut_bytes(d.nsq) / 4);  // K3 LUT images
     size_t need;
     {
         Carver c{nullptr};
-        c.take<float>(size_t(nq) * d.nlist);
+        c.take<float>(coarse_scratch_floats(ix, nq));
         c.take<uint32_t>(size_t(nq) * nprobe);
         c.take<float>(size_t(nq) * nprobe);
         c.take<uint32_t>(size_t(nq) * pw_p);
@@ -331,7 +375,7 @@ int search_pass_skew(prag_gpu_index* ix, Workspace* w, const float* dq, uint32_t
     }
     PG_TRY(ws_reserve(w, need, s));
     Carver c{static_cast<char*>(w->buf)};
-    float* coarse = c.take<float>(size_t(nq) * d.nlist);
+    float* coarse = c.take<float>(coarse_scratch_floats(ix, nq));
     uint32_t* probe = c.take<uint32_t>(size_t(nq) * nprobe);
     float* probe_dist = c.take<float>(size_t(nq) * nprobe);
     uint32_t* pkey = c.take<uint32_t>(size_t(nq) * pw_p);
@@ -349,11 +393,9 @@ int search_pass_skew(prag_gpu_index* ix, Workspace* w, const float* dq, uint32_t
 
     const bool prof = tm != nullptr;
     if (prof) cudaEventRecord(w->ev[0], s);
-    PG_TRY(launch_coarse(d, dq, nq, coarse, s));
-    if (prof) cudaEventRecord(w->ev[1], s);
-    PG_TRY(launch_select_probe(d, coarse, nq, nprobe, probe, probe_dist, pkey, ptie, s));
+    PG_TRY(run_coarse(ix, dq, nq, nprobe, coarse, probe, probe_dist, pkey, ptie, s, prof ? w : nullptr));
     if (prof) cudaEventRecord(w->ev[2], s);
-    PG_TRY(launch_plan_skew(d, probe, nq, nprobe, o_scanned, items, ctr, ctr + 1, q_item_off, gthr, pool_cnt,
+    PG_TRY(launch_plan_skew(d, probe, nq, nprobe, IT, o_scanned, items, ctr, ctr + 1, q_item_off, gthr, pool_cnt,
                             item_cap, s));
     PG_TRY(launch_lut_images(d, dq, probe, nq, nprobe, images, s));
     if (prof) cudaEventRecord(w->ev[3], s);
@@ -381,6 +423,9 @@ int search_pass_skew(prag_gpu_index* ix, Workspace* w, const float* dq, uint32_t
         uint32_t ni = 0;
         PG_CUDA(cudaMemcpy(&ni, ctr, 4, cudaMemcpyDeviceToHost));
         tm->work_items += ni;
+        unsigned long long wsum = 0;
+        if (use_tc_coarse(ix, nprobe)) PG_CUDA(cudaMemcpy(&wsum, w->win_stat, 8, cudaMemcpyDeviceToHost));
+        tm->coarse_window += wsum;
     }
     return PRAG_GPU_OK;
 }
@@ -409,7 +454,7 @@ int search_pass(prag_gpu_index* ix, Workspace* w, const float* dq, uint32_t nq, 
     size_t need = 0;
     {
         Carver c{nullptr};
-        c.take<float>(size_t(nq) * d.nlist);
+        c.take<float>(coarse_scratch_floats(ix, nq));
         c.take<uint32_t>(size_t(nq) * nprobe);
         c.take<float>(size_t(nq) * nprobe);
         c.take<uint32_t>(size_t(nq) * pw_p);
@@ -435,7 +480,7 @@ int search_pass(prag_gpu_index* ix, Workspace* w, const float* dq, uint32_t nq, 
     b.out_dist = o_dist;
     b.out_count = o_count;
     b.out_scanned = o_scanned;
-    b.coarse_dist = c.take<float>(size_t(nq) * d.nlist);
+    b.coarse_dist = c.take<float>(coarse_scratch_floats(ix, nq));
     b.probe = c.take<uint32_t>(size_t(nq) * nprobe);
     b.probe_dist = c.take<float>(size_t(nq) * nprobe);
     uint32_t* pkey = c.take<uint32_t>(size_t(nq) * pw_p);
@@ -455,9 +500,7 @@ int search_pass(prag_gpu_index* ix, Workspace* w, const float* dq, uint32_t nq, 
 
     const bool prof = tm != nullptr;
     if (prof) cudaEventRecord(w->ev[0], s);
-    PG_TRY(launch_coarse(d, dq, nq, b.coarse_dist, s));
-    if (prof) cudaEventRecord(w->ev[1], s);
-    PG_TRY(launch_select_probe(d, b.coarse_dist, nq, nprobe, b.probe, b.probe_dist, pkey, ptie, s));
+    PG_TRY(run_coarse(ix, dq, nq, nprobe, b.coarse_dist, b.probe, b.probe_dist, pkey, ptie, s, prof ? w : nullptr));
     if (prof) cudaEventRecord(w->ev[2], s);
     PG_TRY(launch_plan(d, b, s));
     if (prof) cudaEventRecord(w->ev[3], s);
@@ -483,6 +526,9 @@ int search_pass(prag_gpu_index* ix, Workspace* w, const float* dq, uint32_t nq, 
         uint32_t ni = 0;
         PG_CUDA(cudaMemcpy(&ni, b.num_items, 4, cudaMemcpyDeviceToHost));
         tm->work_items += ni;
+        unsigned long long wsum = 0;
+        if (use_tc_coarse(ix, nprobe)) PG_CUDA(cudaMemcpy(&wsum, w->win_stat, 8, cudaMemcpyDeviceToHost));
+        tm->coarse_window += wsum;
     }
     return PRAG_GPU_OK;
 }
@@ -517,8 +563,8 @@ int do_search(prag_gpu_index* ix, const float* queries, uint32_t nq, uint32_t np
     const uint64_t kSlots = 192ull << 20;
     uint32_t chunk = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(nq, kSlots / max_cand_q)));
     if (d.code_layout == 1 && k <= 32 && ix->scan_path == 0) {
-        // fast path: bound the per-pass LUT images (nq * nprobe * m KB * 2) to ~1 GiB
-        const uint64_t img_q = uint64_t(nprobe) * d.nsq * 1024;
+        // fast path: bound the per-pass LUT images (nq * nprobe * m * 2 KiB) to ~1 GiB
+        const uint64_t img_q = uint64_t(nprobe) * skew_lut_bytes(d.nsq);
         chunk = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(nq, (1ull << 30) / img_q)));
     }
 
@@ -694,6 +740,7 @@ void prag_gpu_index_free(prag_gpu_index* ix) {
         for (Workspace* w : ix->pool) {
             cudaFree(w->buf);
             cudaFree(w->stage);
+            cudaFree(w->win_stat);
             if (w->host) cudaFreeHost(w->host);
             cudaEventDestroy(w->done);
             for (auto& e : w->ev) cudaEventDestroy(e);
@@ -770,7 +817,7 @@ int prag_gpu_probe(prag_gpu_index* ix, const float* queries, uint32_t nq, uint32
     {
         Carver c{nullptr};
         c.take<float>(size_t(nq) * d.d);
-        c.take<float>(size_t(nq) * d.nlist);
+        c.take<float>(coarse_scratch_floats(ix, nq));
         c.take<uint32_t>(size_t(nq) * nprobe);
         c.take<float>(size_t(nq) * nprobe);
         c.take<uint32_t>(size_t(nq) * pw);
@@ -780,14 +827,13 @@ int prag_gpu_probe(prag_gpu_index* ix, const float* queries, uint32_t nq, uint32
     PG_TRY(ws_reserve(w, need, s));
     Carver c{static_cast<char*>(w->buf)};
     float* dq = c.take<float>(size_t(nq) * d.d);
-    float* coarse = c.take<float>(size_t(nq) * d.nlist);
+    float* coarse = c.take<float>(coarse_scratch_floats(ix, nq));
     uint32_t* pl = c.take<uint32_t>(size_t(nq) * nprobe);
     float* pd = c.take<float>(size_t(nq) * nprobe);
     uint32_t* pk = c.take<uint32_t>(size_t(nq) * pw);
     uint64_t* pt = c.take<uint64_t>(size_t(nq) * pw);
     PG_CUDA(cudaMemcpyAsync(dq, queries, size_t(nq) * d.d * 4, cudaMemcpyDefault, s));
-    PG_TRY(launch_coarse(d, dq, nq, coarse, s));
-    PG_TRY(launch_select_probe(d, coarse, nq, nprobe, pl, pd, pk, pt, s));
+    PG_TRY(run_coarse(ix, dq, nq, nprobe, coarse, pl, pd, pk, pt, s));
     PG_CUDA(cudaMemcpyAsync(out_lists, pl, size_t(nq) * nprobe * 4, cudaMemcpyDefault, s));
     if (out_dist) PG_CUDA(cudaMemcpyAsync(out_dist, pd, size_t(nq) * nprobe * 4, cudaMemcpyDefault, s));
     PG_CUDA(cudaStreamSynchronize(s));
@@ -996,6 +1042,15 @@ int prag_gpu_set_scan_path(prag_gpu_index* ix, int path) {
         return PRAG_GPU_CONFIG;
     }
     ix->scan_path = path;
+    return PRAG_GPU_OK;
+}
+
+int prag_gpu_set_coarse_path(prag_gpu_index* ix, int path) {
+    if (!ix || path < 0 || path > 1) {
+        set_error("coarse path must be 0 (auto) or 1 (exact SIMT)");
+        return PRAG_GPU_CONFIG;
+    }
+    ix->coarse_path = path;
     return PRAG_GPU_OK;
 }
 

@@ -75,6 +75,9 @@ struct DeviceIndex {
     float* codewords = nullptr;   // [nsq][256][sub_dim] (LUT-image kernel)
     uint64_t* skew_off = nullptr; // [nlist+1] tile offsets into skew_codes
     uint8_t* skew_codes = nullptr;
+    float* cent_tc = nullptr;     // K1 A operand: centroids pre-split hi/lo in UMMA core-matrix order
+    float* cent_norm = nullptr;   // [nlist] ||c||^2
+    bool tc_ok = false;           // tensor-core coarse quantizer usable for this shape
 };
 
 // ------------------------------------------------------------ workspace
@@ -93,6 +96,7 @@ struct Workspace {
     size_t host_bytes = 0;
     // profiling events
     cudaEvent_t ev[8] = {};
+    unsigned long long* win_stat = nullptr;  // profiling: sum of K1b window sizes
 };
 
 struct SearchPlanSizes {
@@ -113,6 +117,7 @@ struct prag_gpu_index {
     uint64_t device_bytes = 0;
     bool profiling = false;
     int scan_path = 0;                            // 0 auto, 1 force generic
+    int coarse_path = 0;                          // 0 auto (tensor cores when eligible), 1 force exact SIMT
     prag_gpu_timings last{};
     std::mutex mu;                                // guards pool and `last`
     std::vector<pg::Workspace*> pool;
@@ -157,7 +162,7 @@ int launch_merge(const uint64_t* ids, const float* dist, const uint32_t* count, 
                  uint64_t* gtie, uint32_t pw, cudaStream_t s);
 uint32_t scan_chunk();
 // fast path (scan_skew.cu)
-int launch_plan_skew(const DeviceIndex& ix, const uint32_t* probe, uint32_t nq, uint32_t nprobe,
+int launch_plan_skew(const DeviceIndex& ix, const uint32_t* probe, uint32_t nq, uint32_t nprobe, uint32_t it_tiles,
                      uint64_t* scanned, uint4* items, uint32_t* num_items, uint32_t* cursor, uint32_t* q_item_off,
                      uint32_t* gthr, uint32_t* pool_cnt, uint64_t item_cap, cudaStream_t s);
 int launch_lut_images(const DeviceIndex& ix, const float* queries, const uint32_t* probe, uint32_t nq,
@@ -170,11 +175,23 @@ int launch_select_pool(const uint32_t* pool_key, const uint64_t* pool_id, const 
                        const uint32_t* q_item_off, uint32_t warps, uint32_t nq, uint32_t k, uint64_t* out_ids,
                        float* out_dist, uint32_t* out_count, uint32_t* gkey, uint64_t* gtie, uint32_t pw,
                        cudaStream_t s);
-uint32_t skew_item_tiles();
+uint32_t skew_item_tiles(uint64_t est_tiles, uint32_t grid);
+uint32_t skew_min_item_tiles();
+size_t skew_lut_bytes(uint32_t m);
 uint32_t skew_warps(uint32_t m);
-uint32_t skew_ctas_per_sm(uint32_t m);
 void build_skew_layout(const HostIndex& h, uint32_t m, std::vector<uint64_t>& skew_off, std::vector<uint8_t>& out);
 uint32_t sort_cap();
+// tensor-core coarse quantizer (coarse_tc.cu)
+bool tc_coarse_supported(uint32_t nlist, uint32_t d);
+float tc_bound_c(uint32_t d);
+void build_tc_centroids(const float* cent, uint32_t nlist, uint32_t d, std::vector<float>& out,
+                        std::vector<float>& norms);
+uint32_t tc_slices(uint32_t d);
+// K1 writes partial[tc_slices(d)][nq][nlist]; K1b consumes it (and uses slice 0 as scratch)
+int launch_coarse_tc(const DeviceIndex& ix, const float* queries, uint32_t nq, float* partial, cudaStream_t s);
+int launch_select_window(const DeviceIndex& ix, float* partial, const float* queries, uint32_t nq, uint32_t nprobe,
+                         uint32_t* probe, float* probe_dist, unsigned long long* win_stat, cudaStream_t s);
+constexpr uint32_t kTcMaxNprobe = 256;
 size_t select_smem_bytes();
 
 }  // namespace pg

@@ -573,8 +573,41 @@ __global__ void __launch_bounds__(kSelThreads) merge_kernel(
                out_ids + size_t(q) * k, out_count + q);
 }
 
+// k-th smallest (1-based rank) of the CTA's register-resident keys (VPT per
+// thread, slot i*blockDim + tid valid when < n); 8-bit radix passes over SMEM
+// histograms.
+template <int VPT>
+__device__ uint32_t block_kth_reg(const uint32_t (&key)[VPT], uint32_t n, uint32_t rank, SelShared& sm) {
+    const uint32_t tid = threadIdx.x, nth = blockDim.x;
+    __syncthreads();
+    if (tid == 0) {
+        sm.prefix = 0;
+        sm.rank = rank;
+    }
+    uint32_t mask = 0;
+    for (int shift = 24; shift >= 0; shift -= 8) {
+        for (uint32_t i = tid; i < 256; i += nth) sm.hist[i] = 0;
+        __syncthreads();
+        const uint32_t prefix = sm.prefix;
+#pragma unroll
+        for (int i = 0; i < VPT; ++i) {
+            const bool act = i * nth + tid < n && (key[i] & mask) == prefix;
+            warp_hist_add(sm.hist, (key[i] >> shift) & 255u, act);
+        }
+        __syncthreads();
+        hist_pick(sm, shift, false);
+        __syncthreads();
+        mask |= 0xffu << shift;
+    }
+    return sm.prefix;
+}
+
 // K4 (fast path): exact top-k over the per-query candidate pool the fused
-// scan filled (each warp's exact top-k of its share of the lists).
+// scan filled (each warp's exact top-k of its share of the lists). Pools of
+// up to 8 * 1024 candidates are selected from registers in one read (radix
+// select of the k-th key, then the <= kSortCap survivors ranked by
+// (distance, chunk_id)); larger pools, or more than kSortCap survivors tied
+// at the k-th distance, take the general multi-pass block_topk.
 __global__ void __launch_bounds__(kSelThreads) select_pool_kernel(
     const uint32_t* __restrict__ pool_key, const uint64_t* __restrict__ pool_id,
     const uint32_t* __restrict__ pool_cnt, const uint32_t* __restrict__ q_item_off, uint32_t warps, uint32_t k,
@@ -582,10 +615,59 @@ __global__ void __launch_bounds__(kSelThreads) select_pool_kernel(
     uint32_t* gkey, uint64_t* gtie, uint32_t pw) {
     extern __shared__ __align__(16) unsigned char smraw[];
     SelShared& sm = *reinterpret_cast<SelShared*>(smraw);
-    const uint32_t q = blockIdx.x;
+    const uint32_t q = blockIdx.x, tid = threadIdx.x;
     const size_t off = size_t(q_item_off[q]) * warps * k;
+    const uint32_t n = pool_cnt[q];
+    constexpr int VPT = 8;
+    if (n <= VPT * kSelThreads) {
+        uint32_t key[VPT];
+#pragma unroll
+        for (int i = 0; i < VPT; ++i) {
+            const uint32_t idx = i * kSelThreads + tid;
+            key[i] = idx < n ? pool_key[off + idx] : 0xffffffffu;
+        }
+        const uint32_t T = n > k ? block_kth_reg<VPT>(key, n, k, sm) : 0xffffffffu;
+        if (tid == 0) sm.nsel = 0;
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < VPT; ++i) {
+            const uint32_t idx = i * kSelThreads + tid;
+            const bool take = idx < n && key[i] <= T;
+            const unsigned bal = __ballot_sync(0xffffffffu, take);
+            uint32_t base = 0;
+            if ((tid & 31) == 0 && bal) base = atomicAdd(&sm.nsel, __popc(bal));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (take) {
+                const uint32_t pos = base + __popc(bal & ((1u << (tid & 31)) - 1));
+                if (pos < kSortCap) {
+                    sm.skey[pos] = key[i];
+                    sm.stie[pos] = pool_id[off + idx];
+                }
+            }
+        }
+        __syncthreads();
+        const uint32_t c = sm.nsel;
+        if (c <= kSortCap) {
+            for (uint32_t i = tid; i < c; i += kSelThreads) {
+                const uint32_t ki = sm.skey[i];
+                const uint64_t ti = sm.stie[i];
+                uint32_t r = 0;
+                for (uint32_t j = 0; j < c; ++j) {
+                    const uint32_t kj = sm.skey[j];
+                    r += kj < ki || (kj == ki && sm.stie[j] < ti);
+                }
+                if (r < k) {
+                    out_dist[size_t(q) * k + r] = key_float(ki);
+                    out_ids[size_t(q) * k + r] = ti;
+                }
+            }
+            if (tid == 0) out_count[q] = min(n, k);
+            return;
+        }
+        __syncthreads();
+    }
     MergeSrc src{pool_key + off, pool_id + off};
-    block_topk(src, pool_cnt[q], k, sm, gkey + size_t(q) * pw, gtie + size_t(q) * pw, out_dist + size_t(q) * k,
+    block_topk(src, n, k, sm, gkey + size_t(q) * pw, gtie + size_t(q) * pw, out_dist + size_t(q) * k,
                out_ids + size_t(q) * k, out_count + q);
 }
 

@@ -33,7 +33,8 @@ namespace pg {
 namespace {
 
 constexpr uint32_t kTileEntries = 32;
-constexpr uint32_t kItemTiles = 512;  // tiles per scan work item (16384 entries)
+constexpr uint32_t kMaxItemTiles = 512;  // tiles per scan work item (16384 entries) at most
+constexpr uint32_t kMinItemTiles = 32;   // and at least (small batches: more, smaller items)
 constexpr uint32_t kLutPairs = 8;     // (query, list) pairs per LUT-kernel CTA
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -49,15 +50,17 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                  : "memory");
 }
 
+// Blocking wait: try_wait with a suspend-time hint, so a waiting warp is
+// descheduled until the phase completes instead of spinning on issue slots.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
     asm volatile(
         "{\n"
         ".reg .pred p;\n"
         "LAB_WAIT:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
         "@!p bra LAB_WAIT;\n"
         "}\n" ::"r"(smem_u32(bar)),
-        "r"(phase)
+        "r"(phase), "r"(0x989680u)
         : "memory");
 }
 
@@ -114,21 +117,35 @@ __device__ __forceinline__ void sub2_bcast(float r0, float r1, float w, float& d
     d1 = __uint_as_float(uint32_t(out >> 32));
 }
 
+// SMEM image of one (query, list) ADC table, as K3 gathers it: R = m/32
+// images of [256 codes][64 columns] fp32 (64 KiB each). Lane t at fold step
+// s reads column s - t + 32 of image s/32, so with
+//   image 0:      column c holds T[(c - 32) mod m]
+//   image r >= 1: column c holds T[c + 32 (r - 1)]
+// every step's 32 lanes hit 32 distinct banks whatever the code bytes are.
+// The LUT kernel writes the compact table T[sq][256] (coalesced); K3's
+// expander warps build the image from it in SMEM.
+template <int M>
+constexpr uint32_t image_floats() {
+    return uint32_t(M / 32) * 256u * 64u;
+}
+
 // Grid: (ceil(npairs / kLutPairs), m / 8). CTA: 256 threads = 256 codes; it
 // computes subquantizers [8*blockIdx.y, +8) of T[sq][code] =
 // squared_l2(r_sq, w[sq][code], sub_dim) (annindex.hpp:292-297, residual
-// r = q - c_list) for kLutPairs pairs and writes the compact table
-// luts[pair][sq][256] (coalesced; the scan CTA expands it into its SMEM
-// image). Residuals sit in SMEM as [sq][j][pair] so one LDS.128 broadcasts
+// r = q - c_list, annindex.hpp:287-289) for kLutPairs pairs and writes them
+// as the compact table luts[pair][sq][256]. Codewords come from the transposed [sq][j][256] copy
+// (coalesced), the next subquantizer's prefetched while the current one is
+// folded. Residuals sit in SMEM as [sq][j][pair] so one LDS.128 broadcasts
 // four pairs' values.
 template <int M, int SUBC>  // SUBC: compile-time sub_dim (0 = runtime `sub`, <= 16)
-__global__ void __launch_bounds__(256, 2) lut_kernel(const float* __restrict__ queries,
-                                                     const float* __restrict__ centroids,
-                                                     const float* __restrict__ codewords,
-                                                     const uint32_t* __restrict__ probe,
-                                                     const uint32_t* __restrict__ list_len, uint32_t nq,
-                                                     uint32_t nprobe, uint32_t d, uint32_t sub,
-                                                     float* __restrict__ luts) {
+__global__ void __launch_bounds__(256, 1) lut_image_kernel(const float* __restrict__ queries,
+                                                           const float* __restrict__ centroids,
+                                                           const float* __restrict__ codewordsT,
+                                                           const uint32_t* __restrict__ probe,
+                                                           const uint32_t* __restrict__ list_len, uint32_t nq,
+                                                           uint32_t nprobe, uint32_t d, uint32_t sub,
+                                                           float* __restrict__ luts) {
     constexpr int P = kLutPairs;  // 8
     constexpr int JMAX = SUBC ? SUBC : 16;
     if (SUBC) sub = SUBC;
@@ -137,6 +154,15 @@ __global__ void __launch_bounds__(256, 2) lut_kernel(const float* __restrict__ q
     const uint32_t npairs = nq * nprobe;
     const uint32_t p0 = blockIdx.x * P;
     const uint32_t sq0 = blockIdx.y * 8;
+    const uint32_t code = threadIdx.x;
+    // all 8 subquantizers' codewords requested before anything else (one
+    // memory round trip instead of one per subquantizer)
+    float wall[8][JMAX];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < JMAX; ++j)
+            if (j < int(sub)) wall[i][j] = __ldg(codewordsT + (size_t(sq0 + i) * sub + j) * 256 + code);
     if (threadIdx.x < P) {
         const uint32_t pair = p0 + threadIdx.x;
         uint32_t list = 0xffffffffu;
@@ -152,7 +178,7 @@ __global__ void __launch_bounds__(256, 2) lut_kernel(const float* __restrict__ q
 #pragma unroll
     for (int p = 0; p < P; ++p) live |= (s_list[p] != 0xffffffffu) << p;
     if (!live) return;
-    // residual r = q - c_list (annindex.hpp:292) for this CTA's 8 subquantizers
+    // residual r = q - c_list (annindex.hpp:288) for this CTA's 8 subquantizers
     const uint32_t span = 8 * sub;  // contiguous dims [sq0*sub, +span)
     for (uint32_t t = threadIdx.x; t < span * P; t += blockDim.x) {
         const uint32_t p = t / span, k = t - p * span;
@@ -165,15 +191,10 @@ __global__ void __launch_bounds__(256, 2) lut_kernel(const float* __restrict__ q
         resid[(sl * 16 + j) * P + p] = v;
     }
     __syncthreads();
-    const uint32_t code = threadIdx.x;
-#pragma unroll 1
-    for (uint32_t i = 0; i < 8; ++i) {
-        const uint32_t sq = sq0 + i;
-        float w[JMAX];
-        const float* wp = codewords + (size_t(sq) * 256 + code) * sub;
+    float tv[8][P];  // T[sq0 + i][code] for each pair
 #pragma unroll
-        for (int j = 0; j < JMAX; ++j)
-            if (j < int(sub)) w[j] = __ldg(wp + j);
+    for (int i = 0; i < 8; ++i) {
+        const float* w = wall[i];
         float acc[P];
 #pragma unroll
         for (int p = 0; p < P; ++p) acc[p] = 0.0f;
@@ -193,8 +214,15 @@ __global__ void __launch_bounds__(256, 2) lut_kernel(const float* __restrict__ q
             }
         }
 #pragma unroll
-        for (int p = 0; p < P; ++p)
-            if (live >> p & 1u) luts[(size_t(p0 + p) * M + sq) * 256 + code] = acc[p];
+        for (int p = 0; p < P; ++p) tv[i][p] = acc[p];
+    }
+    // compact table luts[pair][sq][256]: each store is 32 consecutive codes
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        if (!(live >> p & 1u)) continue;
+        float* dst = luts + (size_t(p0 + p) * M + sq0) * 256 + code;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dst[i * 256] = tv[i][p];
     }
 }
 
@@ -203,22 +231,55 @@ template <int M>
 struct SkewCfg;
 template <>
 struct SkewCfg<32> {
-    static constexpr int kWarps = 8;      // 2 CTAs per SM
-    static constexpr int kDepth = 4;      // code tiles in flight per warp (TMA ring, power of 2)
-    static constexpr int kMinBlocks = 2;
+    static constexpr int kWarps = 13;  // consumer warps; + 1 producer + 2 expander warps, 1 CTA per SM
+    static constexpr int kDepth = 4;   // code tiles in flight per consumer warp (TMA ring)
+    static constexpr int kBufs = 2;    // SMEM images: item i+1's is built while item i is scanned
 };
 template <>
 struct SkewCfg<64> {
-    static constexpr int kWarps = 16;     // 1 CTA per SM (128 KB LUT image)
+    static constexpr int kWarps = 8;
     static constexpr int kDepth = 2;
-    static constexpr int kMinBlocks = 1;
+    static constexpr int kBufs = 1;    // 128 KiB image: single-buffered
+};
+constexpr int kExpWarps = 2;
+
+constexpr uint32_t kEndItem = 0xffffffffu;
+constexpr uint32_t kMinWarpTiles = 4;  // a warp re-reads one tail tile per range: keep ranges >= 4 tiles
+
+struct ItemSlot {
+    uint32_t pair, tb, te, len, q, pad;
+    uint64_t tile_byte_off;  // skew_off[list] * tile bytes
+    uint64_t lbase;          // list_off[list]: padded entry slot of the list's entry 0
+};
+
+// SMEM plan of K3 (runtime: it depends on where the dynamic window starts).
+// The LUT images sit at a 64 KiB-aligned shared address, so a gather address
+// is exactly PRMT(code byte -> bits 8..15, lane column -> bits 0..7, image
+// base -> bits 16..31) plus a compile-time offset: LDS [R + imm], no add.
+// The alignment pad in front of the images holds as many of the consumer
+// warps' TMA rings as fit; the staging buffer, the remaining rings, the
+// mbarriers and the item slots follow the images.
+template <int M>
+struct SkewSmem {
+    static constexpr int W = SkewCfg<M>::kWarps, D = SkewCfg<M>::kDepth, NB = SkewCfg<M>::kBufs;
+    static constexpr uint32_t kImg = image_floats<M>() * 4;  // R x 64 KiB
+    static constexpr uint32_t kStage = 32768;                // 32 subquantizers of T[sq][256] fp32
+    static constexpr uint32_t kTile = 32u * M;
+    static constexpr uint32_t kRing = uint32_t(D) * kTile;   // per consumer warp
+    // img_full[NB], img_empty[NB], stg_full, stg_empty, ring[W*D]
+    static constexpr uint32_t nbars = 2 * NB + 2 + W * D;
+    static constexpr uint32_t kTail = 8 * nbars + (NB + 1) * uint32_t(sizeof(ItemSlot));
+    static constexpr uint32_t bytes = 232448;                // 227 KiB: the opt-in maximum
+    // worst case: a pad just below one ring (nothing fits in it)
+    static constexpr uint32_t worst = (kRing - 16) + NB * kImg + kStage + W * kRing + kTail;
+    static constexpr int threads = (W + 1 + kExpWarps) * 32;
 };
 
 template <int M>
 constexpr size_t skew_smem_bytes() {
-    return size_t(M / 32) * 65536 + size_t(SkewCfg<M>::kWarps) * SkewCfg<M>::kDepth * 32 * M +
-           8 * (1 + SkewCfg<M>::kWarps * SkewCfg<M>::kDepth) + 32;
+    return SkewSmem<M>::bytes;
 }
+static_assert(SkewSmem<32>::worst <= 232448 && SkewSmem<64>::worst <= 232448, "K3 SMEM exceeds 227 KiB");
 
 // LUT gather: 32-bit shared::cta address (uniform base folded by ptxas into
 // LDS [R + UR + imm]) plus a compile-time offset.
@@ -235,13 +296,17 @@ __device__ __forceinline__ uint4 lds_u4(uint32_t addr) {
     return v;
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 // One step of the skewed fold: lane's code byte S -> table column, gather,
 // and the masked {cur, prev} update (steps >= 32 always belong to `cur`).
 template <int M, int S>
-__device__ __forceinline__ void skew_step(const uint32_t* w, uint32_t bt, uint32_t lutb, float& cur, float& prev,
-                                          const float* mk, const float* nk) {
+__device__ __forceinline__ void skew_step(const uint32_t* w, uint32_t bt, float& cur, float& prev, const float* mk,
+                                          const float* nk) {
     constexpr int r = S >> 5;
-    const uint32_t addr = __byte_perm(w[S >> 2], bt, 0x7604u | (uint32_t(S & 3) << 4)) + lutb;
+    const uint32_t addr = __byte_perm(w[S >> 2], bt, 0x7604u | (uint32_t(S & 3) << 4));
     const float t = lds_lut<r * 65536 + (S - 32 * r) * 4>(addr);
     if constexpr (S < 32) {
         fma2_bcast(cur, prev, t, mk[S], nk[S]);
@@ -251,9 +316,9 @@ __device__ __forceinline__ void skew_step(const uint32_t* w, uint32_t bt, uint32
 }
 
 template <int M, int... S>
-__device__ __forceinline__ void skew_round(const uint32_t* w, uint32_t bt, uint32_t lutb, float& cur, float& prev,
-                                           const float* mk, const float* nk, std::integer_sequence<int, S...>) {
-    (skew_step<M, S>(w, bt, lutb, cur, prev, mk, nk), ...);
+__device__ __forceinline__ void skew_round(const uint32_t* w, uint32_t bt, float& cur, float& prev, const float* mk,
+                                           const float* nk, std::integer_sequence<int, S...>) {
+    (skew_step<M, S>(w, bt, cur, prev, mk, nk), ...);
 }
 
 __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
@@ -262,17 +327,160 @@ __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
     return v;
 }
 
-struct WarpTopK {
-    uint32_t key;  // raw float bits of the distance (distances are >= +0)
-    uint64_t id;
+// One consumer warp's share [a, e_end] of an item: stream the tiles through
+// the warp's TMA ring, fold them against the SMEM image at byte offset IMG
+// (compile-time, so the gather is LDS [R + UR + imm]), keep the warp top-k and
+// publish it to the query's candidate pool.
+struct ScanCtx {
+    unsigned char* wring;
+    uint64_t* wbar;
+    uint32_t ring_s, lane, bt, k;  // bt: column offset | image page (see SkewSmem)
+    const uint8_t* skew_codes;
+    const uint64_t* ids;
+    uint32_t* gthr;
+    const uint32_t* q_item_off;
+    uint32_t* pool_cnt;
+    uint32_t* pool_key;
+    uint64_t* pool_id;
 };
 
-// Persistent CTAs pull work items {pair, tile_begin, tile_end} (largest
-// first). Per item: TMA bulk-copy the pair's LUT image into SMEM; each warp
-// scans a contiguous tile range, its code tiles streamed through a per-warp
-// ring of kDepth TMA bulk copies (one elected lane, one mbarrier per slot).
 template <int M>
-__global__ void __launch_bounds__(SkewCfg<M>::kWarps * 32, SkewCfg<M>::kMinBlocks)
+__device__ __forceinline__ void scan_range(const ScanCtx& cx, const ItemSlot& sl, uint32_t a, uint32_t e_end,
+                                           uint32_t& consumed, const float* mk, const float* nk) {
+    constexpr int W = SkewCfg<M>::kWarps, D = SkewCfg<M>::kDepth;
+    constexpr int kChunks = M / 16;
+    constexpr uint32_t kTileBytes = 32u * M;
+    const uint32_t lane = cx.lane, bt = cx.bt, k = cx.k, ring_s = cx.ring_s;
+    unsigned char* wring = cx.wring;
+    uint64_t* wbar = cx.wbar;
+    const uint64_t* __restrict__ ids = cx.ids;
+    uint32_t* gthr = cx.gthr;
+    const uint8_t* skew_codes = cx.skew_codes;
+    const uint32_t* q_item_off = cx.q_item_off;
+    uint32_t* pool_cnt = cx.pool_cnt;
+    uint32_t* pool_key = cx.pool_key;
+    uint64_t* pool_id = cx.pool_id;
+    const uint32_t q = sl.q;
+    const unsigned char* tiles = skew_codes + sl.tile_byte_off;
+    // this warp streams tiles a..e_end inclusive: tile e_end holds the
+    // tails of the range's last entries
+    if (lane == 0) {
+        for (uint32_t t = 0; t < uint32_t(D) && a + t <= e_end; ++t) {
+            const uint32_t slot = (consumed + t) % D;
+            mbar_expect_tx(wbar + slot, kTileBytes);
+            bulk_g2s(wring + slot * kTileBytes, tiles + size_t(a + t) * kTileBytes, kTileBytes, wbar + slot);
+        }
+    }
+    uint32_t tk_key = 0xffffffffu;  // warp top-k: lane i holds the i-th (distance bits, entry slot)
+    uint32_t tk_pos = 0xffffffffu;
+    uint32_t thr_key = 0xffffffffu;
+    uint32_t g_thr = ld_relaxed(gthr + q), g_next = 0xffffffffu;
+    float cur = 0.0f, prev = 0.0f;
+    for (uint32_t j = a; j <= e_end; ++j, ++consumed) {
+        const uint32_t slot = consumed % D;
+        mbar_wait(wbar + slot, (consumed / D) & 1u);
+        uint32_t wd[M / 4];
+#pragma unroll
+        for (int c = 0; c < kChunks; ++c) {
+            const uint4 v = lds_u4(ring_s + slot * kTileBytes + c * 512 + lane * 16);
+            wd[4 * c] = v.x;
+            wd[4 * c + 1] = v.y;
+            wd[4 * c + 2] = v.z;
+            wd[4 * c + 3] = v.w;
+        }
+        // refresh the query's shared threshold (a pruning hint only): the load
+        // issued every 8th tile is consumed a tile later
+        g_thr = min(g_thr, g_next);
+        if (((j - a) & 7u) == 0u) g_next = __ldcg(gthr + q);
+        skew_round<M>(wd, bt, cur, prev, mk, nk, std::make_integer_sequence<int, M>{});
+        // the codes of this slot are consumed (every lane's LDS.128 result
+        // was used by the steps above): refill it with tile j + D
+        __syncwarp();
+        if (lane == 0 && j + D <= e_end) {
+            mbar_expect_tx(wbar + slot, kTileBytes);
+            bulk_g2s(wring + slot * kTileBytes, tiles + size_t(j + D) * kTileBytes, kTileBytes, wbar + slot);
+        }
+        // entry 32(j-1)+lane is complete in `prev`
+        const uint32_t e = (j - 1) * kTileEntries + lane;
+        const bool valid = j > a && e < sl.len;
+        const uint32_t key = __float_as_uint(prev);
+        prev = cur;
+        cur = 0.0f;
+        const uint32_t lim = min(thr_key, g_thr);
+        const bool pass = valid && key <= lim;
+        unsigned bal = __ballot_sync(0xffffffffu, pass);
+        if (bal) {
+            const uint32_t mypos = uint32_t(sl.lbase) + e;
+            while (bal) {
+                const int src = __ffs(bal) - 1;
+                bal &= bal - 1;
+                const uint32_t ck = __shfl_sync(0xffffffffu, key, src);
+                const uint32_t cp = __shfl_sync(0xffffffffu, mypos, src);
+                if (ck > thr_key) continue;  // threshold tightened by an earlier insertion
+                // lanes whose element sorts after the candidate, by
+                // (distance, chunk_id) (annindex.hpp:55-58)
+                bool gt = tk_key > ck;
+                if (__any_sync(0xffffffffu, tk_key == ck)) {  // exact distance tie: compare ids
+                    const uint64_t cid = ids[cp];
+                    const uint64_t mid = tk_key == ck ? ids[tk_pos] : 0ull;
+                    gt = gt || (tk_key == ck && mid > cid);
+                }
+                const unsigned gm = __ballot_sync(0xffffffffu, gt);
+                const int pos = gm ? __ffs(gm) - 1 : 32;
+                if (pos < int(k)) {
+                    const uint32_t uk = __shfl_up_sync(0xffffffffu, tk_key, 1);
+                    const uint32_t up = __shfl_up_sync(0xffffffffu, tk_pos, 1);
+                    if (int(lane) > pos) {
+                        tk_key = uk;
+                        tk_pos = up;
+                    } else if (int(lane) == pos) {
+                        tk_key = ck;
+                        tk_pos = cp;
+                    }
+                    thr_key = __shfl_sync(0xffffffffu, tk_key, k - 1);
+                }
+            }
+            if (thr_key < g_thr) {
+                if (lane == 0) atomicMin(gthr + q, thr_key);
+                g_thr = thr_key;
+            }
+        }
+    }
+    // publish this warp's list into the query's candidate pool
+    const unsigned have = __ballot_sync(0xffffffffu, lane < k && tk_key != 0xffffffffu);
+    const uint32_t cnt = __popc(have);
+    if (cnt) {
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(pool_cnt + q, cnt);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        const size_t poff = size_t(q_item_off[q]) * W * k;
+        if (lane < cnt) {
+            pool_key[poff + base + lane] = ord_key(__uint_as_float(tk_key));
+            pool_id[poff + base + lane] = ids[tk_pos];
+        }
+    }
+}
+
+// Persistent, one CTA per SM, warp-specialised:
+//  * producer warp (one lane): pulls work items {pair, tile_begin,
+//    tile_end} (largest first), resolves the list's metadata and TMA-copies
+//    the pair's compact table T[m][256] into a staging buffer;
+//  * kExpWarps expander warps: transpose the staged table into the
+//    conflict-free image (diagonal walk: lane L moves T[(s0+L) mod m][c0+L],
+//    so both the LDS and the STS of every step hit 32 distinct banks) in one
+//    of kBufs image buffers -- item i+1's image is built while item i is
+//    scanned;
+//  * kWarps consumer warps: each scans a contiguous tile range of the item,
+//    its code tiles streamed through a per-warp ring of kDepth TMA bulk
+//    copies (one elected lane, one mbarrier per slot), keeps an exact top-k
+//    (k <= 32) in registers by (distance, chunk_id), prunes with a per-query
+//    threshold shared through global memory (atomicMin on the k-th distance),
+//    and publishes its list into the query's candidate pool.
+// Stages hand off through full/empty mbarrier pairs; no CTA-wide barrier
+// after setup. Candidates are held as (distance bits, entry slot); chunk ids
+// are loaded only on an exact distance tie and when a list is published.
+template <int M>
+__global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
     scan_skew_kernel(const uint4* __restrict__ items, const uint32_t* __restrict__ num_items,
                      uint32_t* __restrict__ cursor, const uint32_t* __restrict__ probe,
                      const uint32_t* __restrict__ list_len, const uint64_t* __restrict__ skew_off,
@@ -281,29 +489,139 @@ __global__ void __launch_bounds__(SkewCfg<M>::kWarps * 32, SkewCfg<M>::kMinBlock
                      uint32_t k, uint32_t* __restrict__ gthr, const uint32_t* __restrict__ q_item_off,
                      uint32_t* __restrict__ pool_cnt, uint32_t* __restrict__ pool_key,
                      uint64_t* __restrict__ pool_id) {
-    constexpr int R = M / 32;
-    constexpr int kWarps = SkewCfg<M>::kWarps;
-    constexpr int D = SkewCfg<M>::kDepth;
-    constexpr int kChunks = M / 16;              // uint4 per lane per round
-    constexpr uint32_t kTileBytes = 32u * M;     // bytes per tile
-    constexpr uint32_t kImgBytes = R * 65536u;
+    using L = SkewSmem<M>;
+    constexpr int W = L::W, D = L::D, NB = L::NB;
+    constexpr uint32_t kImgBytes = L::kImg;
+    constexpr uint32_t kStageBytes = L::kStage;
+    constexpr uint32_t kHalves = M / 32;  // staging rounds per item (32 subquantizers each)
     extern __shared__ __align__(1024) unsigned char smem[];
-    unsigned char* ring = smem + kImgBytes;                                   // [warps][D][tile]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(ring + size_t(kWarps) * D * kTileBytes);  // [0]=LUT
-    uint32_t* s_item = reinterpret_cast<uint32_t*>(bars + 1 + kWarps * D);
-    uint32_t* s_thr = s_item + 1;  // the CTA's view of the query threshold
+    const uint32_t base = smem_u32(smem);
+    const uint32_t pad = ((base + 0xffffu) & ~0xffffu) - base;  // images start 64 KiB-aligned
+    const uint32_t img_off = pad;
+    const uint32_t stage_off = img_off + NB * kImgBytes;
+    const uint32_t rings_in_pad = min(uint32_t(W), pad / L::kRing);
+    const uint32_t after_off = stage_off + kStageBytes;  // rings not in the pad, then the tail
+    const uint32_t tail_off = after_off + (W - rings_in_pad) * L::kRing;
+    if (tail_off + L::kTail > L::bytes) __trap();
+    float* stage = reinterpret_cast<float*>(smem + stage_off);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + tail_off);
+    uint64_t* img_full = bars;
+    uint64_t* img_empty = bars + NB;
+    uint64_t* stg_full = bars + 2 * NB;
+    uint64_t* stg_empty = bars + 2 * NB + 1;
+    uint64_t* rbar = bars + 2 * NB + 2;
+    ItemSlot* slots = reinterpret_cast<ItemSlot*>(smem + tail_off + 8 * L::nbars);  // [NB] image slots
+    ItemSlot* stg_slot = slots + NB;                                                 // staging slot
 
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t bt = (32u - lane) * 4u;  // lane's column offset (bytes), byte 0 of the address
-    const uint32_t lut_s = smem_u32(smem);  // shared::cta address of the LUT image
-    unsigned char* wring = ring + size_t(warp) * D * kTileBytes;
-    uint64_t* wbar = bars + 1 + warp * D;
     if (threadIdx.x == 0) {
-        for (int i = 0; i < 1 + kWarps * D; ++i) mbar_init(bars + i, 1);
+        for (int i = 0; i < NB; ++i) {
+            mbar_init(img_full + i, kExpWarps);
+            mbar_init(img_empty + i, W);
+        }
+        mbar_init(stg_full, 1);
+        mbar_init(stg_empty, kExpWarps);
+        for (int i = 0; i < W * D; ++i) mbar_init(rbar + i, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     const uint32_t total = *num_items;
+
+    if (warp == uint32_t(W)) {
+        // ------------------------------------------------------ producer
+        if (lane == 0) {
+            uint32_t nx = atomicAdd(cursor, 1u);
+            uint32_t round = 0;  // staging rounds issued (kHalves per item)
+            for (;;) {
+                ItemSlot sl{};
+                sl.pair = kEndItem;
+                if (nx < total) {
+                    const uint4 w4 = items[nx];
+                    const uint32_t list = probe[w4.x];
+                    sl.pair = w4.x;
+                    sl.tb = w4.y;
+                    sl.te = w4.z;
+                    sl.len = list_len[list];
+                    sl.q = w4.x / nprobe;
+                    sl.tile_byte_off = skew_off[list] * L::kTile;
+                    sl.lbase = list_off[list];
+                    nx = atomicAdd(cursor, 1u);  // next item's index, fetched ahead
+                }
+                if (sl.pair == kEndItem) {
+                    mbar_wait(stg_empty, (round & 1u) ^ 1u);
+                    *stg_slot = sl;
+                    mbar_arrive(stg_full);
+                    break;
+                }
+                const unsigned char* src = reinterpret_cast<const unsigned char*>(luts) + size_t(sl.pair) * M * 1024;
+                for (uint32_t h = 0; h < kHalves; ++h, ++round) {
+                    mbar_wait(stg_empty, (round & 1u) ^ 1u);
+                    if (h == 0) *stg_slot = sl;
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    mbar_expect_tx(stg_full, kStageBytes);
+                    bulk_g2s(stage, src + h * kStageBytes, kStageBytes, stg_full);
+                }
+            }
+        }
+        return;
+    }
+    if (warp > uint32_t(W)) {
+        // ------------------------------------------------------ expanders
+        const uint32_t ew = warp - W - 1;
+        uint32_t round = 0;
+        for (uint32_t i = 0;; ++i) {
+            const uint32_t b = NB == 1 ? 0u : i % NB;
+            mbar_wait(stg_full, round & 1u);
+            const ItemSlot sl = *stg_slot;
+            mbar_wait(img_empty + b, ((NB == 1 ? i : i / NB) & 1u) ^ 1u);
+            if (sl.pair == kEndItem) {
+                __syncwarp();
+                if (lane == 0) {
+                    if (ew == 0) slots[b] = sl;
+                    mbar_arrive(img_full + b);
+                }
+                break;
+            }
+            float* img = reinterpret_cast<float*>(smem + img_off + b * kImgBytes);
+            for (uint32_t h = 0; h < kHalves; ++h, ++round) {
+                if (h > 0) mbar_wait(stg_full, round & 1u);
+                // diagonal walk: lane L moves T[32h + (s0+L) mod 32][c0+L]; the LDS
+                // (bank = code) and both STS (bank = column mod 32) are conflict-free
+#pragma unroll 2
+                for (uint32_t c0 = ew * 32; c0 < 256; c0 += 32 * kExpWarps) {
+                    const uint32_t code = c0 + lane;
+                    float* row = img + code * 64;
+#pragma unroll 8
+                    for (uint32_t s0 = 0; s0 < 32; ++s0) {
+                        const uint32_t sl_ = (s0 + lane) & 31u;
+                        const float v = stage[sl_ * 256 + code];
+                        const uint32_t sq = 32 * h + sl_;
+                        if (M == 32) {  // image 0, column c = T[c mod 32]: columns sq and sq + 32
+                            row[sq] = v;
+                            row[sq + 32] = v;
+                        } else {        // image 0 at (sq + 32) mod 64, image 1 at sq
+                            row[(sq + 32) & (M - 1)] = v;
+                            row[16384 + sq] = v;
+                        }
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(stg_empty);
+            }
+            if (lane == 0) {
+                if (ew == 0) slots[b] = sl;
+                mbar_arrive(img_full + b);
+            }
+        }
+        return;
+    }
+
+    // -------------------------------------------------------- consumers
+    // lane's column offset (bytes) in byte 0, the image's 64 KiB page in bytes 2-3
+    const uint32_t bt0 = (32u - lane) * 4u | ((base + img_off) & 0xffff0000u);
+    unsigned char* wring = smem + (warp < rings_in_pad ? warp * L::kRing : after_off + (warp - rings_in_pad) * L::kRing);
+    uint64_t* wbar = rbar + warp * D;
+    const uint32_t ring_s = smem_u32(wring);
     uint32_t consumed = 0;  // tiles this warp has taken from its ring (slot/parity bookkeeping)
     // step masks: {1, 0} where step s >= lane (the starting entry), {0, 1}
     // before (the finishing entry); one FFMA2 updates {cur, prev}.
@@ -314,162 +632,36 @@ __global__ void __launch_bounds__(SkewCfg<M>::kWarps * 32, SkewCfg<M>::kMinBlock
         nk[s] = (uint32_t(s) >= lane) ? 0.0f : 1.0f;
     }
 
-    uint32_t prev_q = 0xffffffffu;
-    for (;;) {
-        __syncthreads();  // every warp is done with the previous item (LUT image, s_thr)
-        if (threadIdx.x == 0) {
-            if (prev_q != 0xffffffffu) atomicMin(gthr + prev_q, *s_thr);  // publish to other CTAs
-            const uint32_t nx = atomicAdd(cursor, 1u);
-            *s_item = nx;
-            if (nx < total) *s_thr = ld_relaxed(gthr + items[nx].x / nprobe);
+    for (uint32_t i = 0;; ++i) {
+        const uint32_t b = NB == 1 ? 0u : i % NB;
+        mbar_wait(img_full + b, (NB == 1 ? i : i / NB) & 1u);
+        const ItemSlot sl = slots[b];
+        if (sl.pair == kEndItem) break;
+        const uint32_t ntile = sl.te - sl.tb;
+        const uint32_t nw = min(uint32_t(W), (ntile + kMinWarpTiles - 1) / kMinWarpTiles);
+        const uint32_t per = (ntile + nw - 1) / nw;
+        const uint32_t a = sl.tb + warp * per;
+        const uint32_t e_end = min(sl.te, a + per);
+        if (warp < nw && a < e_end) {
+            const ScanCtx cx{wring, wbar, ring_s, lane, bt0 + b * (kImgBytes & 0xffff0000u), k, skew_codes, ids, gthr,
+                             q_item_off, pool_cnt, pool_key, pool_id};
+            scan_range<M>(cx, sl, a, e_end, consumed, mk, nk);
         }
-        __syncthreads();
-        const uint32_t it = *s_item;
-        if (it >= total) break;
-        const uint4 w4 = items[it];
-        const uint32_t pair = w4.x, tb = w4.y, te = w4.z;
-        const uint32_t q = pair / nprobe;
-        prev_q = q;
-        const uint32_t list = probe[pair];
-        const uint32_t len = list_len[list];
-        // expand the pair's compact table T[sq][256] (L2) into the SMEM image:
-        // lane = subquantizer (bank = column mod 32 = sq: conflict-free STS),
-        // warps stride over groups of 4 codes (one LDG.128 each)
-        {
-            const float4* src = reinterpret_cast<const float4*>(luts + size_t(pair) * M * 256);
-            float* img = reinterpret_cast<float*>(smem);
-#pragma unroll 1
-            for (uint32_t sqb = 0; sqb < uint32_t(M); sqb += 32) {
-                const uint32_t sq = sqb + lane;
-#pragma unroll 4
-                for (uint32_t g = warp; g < 64; g += kWarps) {
-                    const float4 v = src[sq * 64 + g];
-                    const float vv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        float* row = img + (g * 4 + i) * 64;
-                        // table 0: cur column sq + 32 (sq < 32), finishing column sq - (m - 32)
-                        if (sq < 32) row[32 + sq] = vv[i];
-                        if (sq + 32 >= uint32_t(M)) row[sq + 32 - M] = vv[i];
-#pragma unroll
-                        for (int r_ = 1; r_ < R; ++r_) {
-                            const int c = int(sq) - 32 * (r_ - 1);
-                            if (c >= 0 && c <= 63) row[r_ * 16384 + c] = vv[i];
-                        }
-                    }
-                }
-            }
-        }
-        // this warp's share of tiles [tb, te); it also reads tile b (the tail
-        // of its last entries), so it streams b - a + 1 tiles
-        const uint32_t ntile = te - tb;
-        const uint32_t per = (ntile + kWarps - 1) / kWarps;
-        const uint32_t a = tb + warp * per;
-        const uint32_t b = min(te, a + per);
-        const unsigned char* tiles = skew_codes + skew_off[list] * kTileBytes;
-        const uint64_t lbase = list_off[list];
-        if (a < b && lane == 0) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            for (uint32_t i = 0; i < uint32_t(D) && a + i <= b; ++i) {
-                const uint32_t slot = (consumed + i) % D;
-                mbar_expect_tx(wbar + slot, kTileBytes);
-                bulk_g2s(wring + slot * kTileBytes, tiles + size_t(a + i) * kTileBytes, kTileBytes, wbar + slot);
-            }
-        }
-        __syncthreads();  // SMEM image complete
-        if (a >= b) continue;
-
-        WarpTopK tk{0xffffffffu, ~0ull};
-        uint32_t thr_key = 0xffffffffu;
-        uint32_t g_thr = *reinterpret_cast<volatile uint32_t*>(s_thr);
-        float cur = 0.0f, prev = 0.0f;
-        const uint32_t ring_s = smem_u32(wring);
-        for (uint32_t j = a; j <= b; ++j, ++consumed) {
-            const uint32_t slot = consumed % D;
-            mbar_wait(wbar + slot, (consumed / D) & 1u);
-            uint32_t wd[M / 4];
-#pragma unroll
-            for (int c = 0; c < kChunks; ++c) {
-                const uint4 v = lds_u4(ring_s + slot * kTileBytes + c * 512 + lane * 16);
-                wd[4 * c] = v.x;
-                wd[4 * c + 1] = v.y;
-                wd[4 * c + 2] = v.z;
-                wd[4 * c + 3] = v.w;
-            }
-            const uint32_t g_cta = *reinterpret_cast<volatile uint32_t*>(s_thr);  // used after the steps
-            skew_round<M>(wd, bt, lut_s, cur, prev, mk, nk, std::make_integer_sequence<int, M>{});
-            // the codes of this slot are consumed (every lane's LDS.128 result
-            // was used by the steps above): refill it with tile j + D
-            __syncwarp();
-            if (lane == 0 && j + D <= b) {
-                mbar_expect_tx(wbar + slot, kTileBytes);
-                bulk_g2s(wring + slot * kTileBytes, tiles + size_t(j + D) * kTileBytes, kTileBytes, wbar + slot);
-            }
-            g_thr = min(g_thr, g_cta);
-            // entry 32(j-1)+lane is complete in `prev`
-            const uint32_t e = (j - 1) * kTileEntries + lane;
-            const bool valid = j > a && e < len;
-            const uint32_t key = __float_as_uint(prev);
-            prev = cur;
-            cur = 0.0f;
-            const uint32_t lim = min(thr_key, g_thr);
-            bool pass = valid && key <= lim;
-            unsigned bal = __ballot_sync(0xffffffffu, pass);
-            if (bal) {
-                const uint64_t myid = pass ? ids[lbase + e] : 0ull;
-                while (bal) {
-                    const int src = __ffs(bal) - 1;
-                    bal &= bal - 1;
-                    const uint32_t ck = __shfl_sync(0xffffffffu, key, src);
-                    const uint64_t ci = __shfl_sync(0xffffffffu, myid, src);
-                    if (ck > thr_key) continue;  // threshold tightened by an earlier insertion
-                    // lanes whose element sorts after the candidate
-                    const bool gt = tk.key > ck || (tk.key == ck && tk.id > ci);
-                    const unsigned gm = __ballot_sync(0xffffffffu, gt);
-                    const int pos = gm ? __ffs(gm) - 1 : 32;
-                    if (pos < int(k)) {
-                        const uint32_t uk = __shfl_up_sync(0xffffffffu, tk.key, 1);
-                        const uint64_t ui = __shfl_up_sync(0xffffffffu, tk.id, 1);
-                        if (int(lane) > pos) {
-                            tk.key = uk;
-                            tk.id = ui;
-                        } else if (int(lane) == pos) {
-                            tk.key = ck;
-                            tk.id = ci;
-                        }
-                        thr_key = __shfl_sync(0xffffffffu, tk.key, k - 1);
-                    }
-                }
-                if (thr_key < g_thr) {
-                    if (lane == 0) atomicMin(s_thr, thr_key);
-                    g_thr = thr_key;
-                }
-            }
-        }
-        // publish this warp's list into the query's candidate pool
-        const unsigned have = __ballot_sync(0xffffffffu, lane < k && tk.key != 0xffffffffu);
-        const uint32_t cnt = __popc(have);
-        if (cnt) {
-            uint32_t base = 0;
-            if (lane == 0) base = atomicAdd(pool_cnt + q, cnt);
-            base = __shfl_sync(0xffffffffu, base, 0);
-            const size_t poff = size_t(q_item_off[q]) * kWarps * k;
-            if (lane < cnt) {
-                pool_key[poff + base + lane] = ord_key(__uint_as_float(tk.key));
-                pool_id[poff + base + lane] = tk.id;
-            }
-        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(img_empty + b);
     }
 }
 
 // Work items for the fast path: per (q, p) pair, ceil(len/32) tiles cut into
-// items of <= kItemTiles tiles, emitted largest-first (log2 size buckets) so
+// items of <= it_tiles tiles, emitted largest-first (log2 size buckets) so
 // the big lists set each query's threshold early and the small ones fill the
 // tail. q_item_off[q] = prefix of per-query item counts (candidate-pool
-// offsets). Also resets the per-query threshold and pool counters.
+// offsets). Also resets the per-query threshold and pool counters, and
+// writes scanned_vectors (annindex.hpp:305: the sum of probed list sizes).
 __global__ void __launch_bounds__(1024) plan_skew_kernel(const uint32_t* __restrict__ probe,
                                                          const uint32_t* __restrict__ list_len, uint32_t nq,
-                                                         uint32_t nprobe, uint64_t* __restrict__ scanned,
+                                                         uint32_t nprobe, uint32_t it_tiles,
+                                                         uint64_t* __restrict__ scanned,
                                                          uint4* __restrict__ items, uint32_t* __restrict__ num_items,
                                                          uint32_t* __restrict__ cursor, uint32_t* __restrict__ q_item_off,
                                                          uint32_t* __restrict__ gthr, uint32_t* __restrict__ pool_cnt,
@@ -478,6 +670,7 @@ __global__ void __launch_bounds__(1024) plan_skew_kernel(const uint32_t* __restr
     __shared__ uint32_t bucket_cnt[32], bucket_pos[32];
     const uint32_t P = nq * nprobe;
     if (threadIdx.x < 32) bucket_cnt[threadIdx.x] = 0;
+    for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x) scanned[q] = 0;
     __syncthreads();
     // pass 1: per-query item counts (prefix) and bucket histogram
     uint32_t carry = 0;
@@ -485,10 +678,11 @@ __global__ void __launch_bounds__(1024) plan_skew_kernel(const uint32_t* __restr
         const uint32_t i = base + threadIdx.x;
         const bool valid = i < P;
         const uint32_t len = valid ? list_len[probe[i]] : 0;
+        if (len) atomicAdd(reinterpret_cast<unsigned long long*>(scanned + i / nprobe), (unsigned long long)len);
         const uint32_t tiles = (len + kTileEntries - 1) / kTileEntries;
-        const uint32_t nit = (tiles + kItemTiles - 1) / kItemTiles;
+        const uint32_t nit = (tiles + it_tiles - 1) / it_tiles;
         for (uint32_t j = 0; j < nit; ++j) {
-            const uint32_t t = min(tiles, (j + 1) * kItemTiles) - j * kItemTiles;
+            const uint32_t t = min(tiles, (j + 1) * it_tiles) - j * it_tiles;
             atomicAdd(&bucket_cnt[31 - __clz(t)], 1u);
         }
         const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -530,11 +724,11 @@ __global__ void __launch_bounds__(1024) plan_skew_kernel(const uint32_t* __restr
     for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
         const uint32_t len = list_len[probe[i]];
         const uint32_t tiles = (len + kTileEntries - 1) / kTileEntries;
-        const uint32_t nit = (tiles + kItemTiles - 1) / kItemTiles;
+        const uint32_t nit = (tiles + it_tiles - 1) / it_tiles;
         for (uint32_t j = 0; j < nit; ++j) {
-            const uint32_t te = min(tiles, (j + 1) * kItemTiles);
-            const uint32_t slot = atomicAdd(&bucket_pos[31 - __clz(te - j * kItemTiles)], 1u);
-            if (slot < item_cap) items[slot] = make_uint4(i, j * kItemTiles, te, 0u);
+            const uint32_t te = min(tiles, (j + 1) * it_tiles);
+            const uint32_t slot = atomicAdd(&bucket_pos[31 - __clz(te - j * it_tiles)], 1u);
+            if (slot < item_cap) items[slot] = make_uint4(i, j * it_tiles, te, 0u);
         }
     }
     if (threadIdx.x == 0) {
@@ -545,17 +739,21 @@ __global__ void __launch_bounds__(1024) plan_skew_kernel(const uint32_t* __restr
     for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x) {
         gthr[q] = 0xffffffffu;
         pool_cnt[q] = 0;
-        uint64_t s = 0;
-        for (uint32_t p = 0; p < nprobe; ++p) s += list_len[probe[q * nprobe + p]];
-        scanned[q] = s;
     }
 }
 
 }  // namespace
 
-uint32_t skew_item_tiles() { return kItemTiles; }
+uint32_t skew_item_tiles(uint64_t est_tiles, uint32_t grid) {
+    // enough items for ~3 per CTA, within [kMinItemTiles, kMaxItemTiles]
+    uint64_t want = est_tiles / (uint64_t(grid) * 3 + 1);
+    uint32_t it = kMinItemTiles;
+    while (it < kMaxItemTiles && uint64_t(it) * 2 <= want) it *= 2;
+    return it;
+}
+uint32_t skew_min_item_tiles() { return kMinItemTiles; }
 uint32_t skew_warps(uint32_t m) { return m == 32 ? SkewCfg<32>::kWarps : SkewCfg<64>::kWarps; }
-uint32_t skew_ctas_per_sm(uint32_t m) { return m == 32 ? 2 : 1; }
+size_t skew_lut_bytes(uint32_t m) { return size_t(m) * 1024; }  // compact T[m][256] per pair
 
 static int check(const char* what) {
     cudaError_t e = cudaGetLastError();
@@ -566,10 +764,10 @@ static int check(const char* what) {
     return PRAG_GPU_OK;
 }
 
-int launch_plan_skew(const DeviceIndex& ix, const uint32_t* probe, uint32_t nq, uint32_t nprobe,
+int launch_plan_skew(const DeviceIndex& ix, const uint32_t* probe, uint32_t nq, uint32_t nprobe, uint32_t it_tiles,
                      uint64_t* scanned, uint4* items, uint32_t* num_items, uint32_t* cursor, uint32_t* q_item_off,
                      uint32_t* gthr, uint32_t* pool_cnt, uint64_t item_cap, cudaStream_t s) {
-    plan_skew_kernel<<<1, 1024, 0, s>>>(probe, ix.list_len, nq, nprobe, scanned, items, num_items, cursor,
+    plan_skew_kernel<<<1, 1024, 0, s>>>(probe, ix.list_len, nq, nprobe, it_tiles, scanned, items, num_items, cursor,
                                         q_item_off, gthr, pool_cnt, item_cap);
     return check("plan_skew");
 }
@@ -578,9 +776,9 @@ int launch_lut_images(const DeviceIndex& ix, const float* queries, const uint32_
                       uint32_t nprobe, float* luts, cudaStream_t s) {
     const uint32_t npairs = nq * nprobe;
     dim3 grid((npairs + kLutPairs - 1) / kLutPairs, ix.nsq / 8);
-#define PG_LUT(MM, SS)                                                                             \
-    lut_kernel<MM, SS><<<grid, 256, 0, s>>>(queries, ix.centroids, ix.codewords, probe, ix.list_len, nq, \
-                                            nprobe, ix.d, ix.sub_dim, luts)
+#define PG_LUT(MM, SS)                                                                                     \
+    lut_image_kernel<MM, SS><<<grid, 256, 0, s>>>(queries, ix.centroids, ix.codewordsT, probe, ix.list_len, nq, \
+                                                  nprobe, ix.d, ix.sub_dim, luts)
     if (ix.nsq == 32 && ix.sub_dim == 12)
         PG_LUT(32, 12);
     else if (ix.nsq == 32)
@@ -594,22 +792,20 @@ int launch_lut_images(const DeviceIndex& ix, const float* queries, const uint32_
 }
 
 int launch_scan_skew(const DeviceIndex& ix, const uint4* items, const uint32_t* num_items, uint32_t* cursor,
-                     const uint32_t* probe, const float* images, uint32_t nprobe, uint32_t k, uint32_t* gthr,
+                     const uint32_t* probe, const float* luts, uint32_t nprobe, uint32_t k, uint32_t* gthr,
                      const uint32_t* q_item_off, uint32_t* pool_cnt, uint32_t* pool_key, uint64_t* pool_id,
                      int grid, cudaStream_t s) {
     if (ix.nsq == 32) {
         const size_t smem = skew_smem_bytes<32>();
         PG_CUDA(cudaFuncSetAttribute(scan_skew_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        PG_CUDA(cudaFuncSetAttribute(scan_skew_kernel<32>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-        scan_skew_kernel<32><<<grid, SkewCfg<32>::kWarps * 32, smem, s>>>(
-            items, num_items, cursor, probe, ix.list_len, ix.skew_off, ix.skew_codes, ix.list_off, ix.ids, images,
+        scan_skew_kernel<32><<<grid, SkewSmem<32>::threads, smem, s>>>(
+            items, num_items, cursor, probe, ix.list_len, ix.skew_off, ix.skew_codes, ix.list_off, ix.ids, luts,
             nprobe, k, gthr, q_item_off, pool_cnt, pool_key, pool_id);
     } else {
         const size_t smem = skew_smem_bytes<64>();
         PG_CUDA(cudaFuncSetAttribute(scan_skew_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        PG_CUDA(cudaFuncSetAttribute(scan_skew_kernel<64>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-        scan_skew_kernel<64><<<grid, SkewCfg<64>::kWarps * 32, smem, s>>>(
-            items, num_items, cursor, probe, ix.list_len, ix.skew_off, ix.skew_codes, ix.list_off, ix.ids, images,
+        scan_skew_kernel<64><<<grid, SkewSmem<64>::threads, smem, s>>>(
+            items, num_items, cursor, probe, ix.list_len, ix.skew_off, ix.skew_codes, ix.list_off, ix.ids, luts,
             nprobe, k, gthr, q_item_off, pool_cnt, pool_key, pool_id);
     }
     return check("scan_skew");

@@ -1,0 +1,136 @@
+"""List-sharded multi-GPU search.
+
+Inverted lists are independent and a candidate's distance depends only on
+(query, its list, its code), so the global top-k of a batch equals the exact
+top-k of the union of per-shard top-k lists, ordered by (distance, chunk_id)
+(annindex.hpp:54-60, :313). One process per GPU:
+
+  1. every rank holds the lists `prag_gpu_plan_shards` (greedy LPT on list
+     bytes) assigns it, plus replicated centroids and codebooks, so every rank
+     computes the identical probe set (annindex.hpp:277-281);
+  2. each rank searches its shard (K1-K4) -> per-shard top-k;
+  3. one all-gather of a packed [nq, 2k+2] int64 record per rank (ids,
+     distance bits, count, scanned_vectors) over NCCL / NVLink;
+  4. rank 0 runs the exact merge kernel (K5) and holds the batch result.
+
+The reference has no multi-GPU path (it is a single-process scalar library);
+this module is the B200 extension the north star asks for. The gather/merge
+logic is backend-agnostic so the CPU test suite exercises it over gloo.
+"""
+from __future__ import annotations
+
+import struct
+from typing import Callable, Optional
+
+import numpy as np
+
+from .ivfpq import BatchResult, GpuIndex, merge_topk, plan_shards
+
+try:
+    import torch
+    import torch.distributed as dist
+except Exception:  # pragma: no cover
+    torch = None
+    dist = None
+
+
+def pack_result(r: BatchResult, k: int) -> "torch.Tensor":
+    """[nq, 2k+2] int64: ids | distance bits | count | scanned."""
+    nq = r.ids.shape[0]
+    rec = torch.empty((nq, 2 * k + 2), dtype=torch.int64, device=r.ids.device)
+    rec[:, :k] = r.ids
+    rec[:, k:2 * k] = r.dist.view(torch.int32).to(torch.int64)
+    rec[:, 2 * k] = r.count.to(torch.int64)
+    rec[:, 2 * k + 1] = r.scanned
+    return rec
+
+
+def unpack_results(g: "torch.Tensor", k: int):
+    """[world, nq, 2k+2] -> ids [world, nq, k], dist, count [world, nq], scanned."""
+    ids = g[:, :, :k].contiguous()
+    dist_ = g[:, :, k:2 * k].to(torch.int32).view(torch.float32).contiguous()
+    cnt = g[:, :, 2 * k].to(torch.int32).contiguous()
+    sc = g[:, :, 2 * k + 1].contiguous()
+    return ids, dist_, cnt, sc
+
+
+def gather_merge(local: BatchResult, k: int, merge: Optional[Callable] = None, group=None, root: int = 0):
+    """All-gather the per-shard top-k of every rank and merge on `root`.
+
+    `merge(ids, dist, count, scanned, k)` defaults to the GPU merge kernel
+    (prag_gpu_merge_topk); returns the merged BatchResult on root, None
+    elsewhere."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    rec = pack_result(local, k)
+    g = torch.empty((world,) + tuple(rec.shape), dtype=rec.dtype, device=rec.device)
+    if rec.is_cuda:
+        dist.all_gather_into_tensor(g, rec, group=group)
+    else:  # gloo
+        dist.all_gather(list(g.unbind(0)), rec, group=group)
+    if rank != root:
+        return None
+    ids, dd, cnt, sc = unpack_results(g, k)
+    if merge is None:
+        return merge_topk(ids, dd, cnt, sc, k, device=ids.device.index or 0,
+                          stream=torch.cuda.current_stream(ids.device))
+    return merge(ids, dd, cnt, sc, k)
+
+
+class ShardedIndex:
+    """One rank's shard of a PRAGIX01 index on its own GPU."""
+
+    def __init__(self, path: str, device: Optional[int] = None, group=None):
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.device = torch.cuda.current_device() if device is None else device
+        self.index = GpuIndex.load_shard(path, self.rank, self.world, self.device)
+        self.nlist = self.index.nlist
+
+    def search_batch(self, queries, k: int, nprobe: int, stream=None):
+        """queries: CUDA tensor [nq, d] (identical on every rank). Returns the
+        merged result on rank 0 and None on the other ranks."""
+        local = self.index.search_batch(queries, k, nprobe, stream=stream)
+        return gather_merge(local, k, group=self.group)
+
+
+# ------------------------------------------------------------ shard files
+def _read_pragix(path: str):
+    """PRAGIX01 (annindex.hpp:335-359) -> (header, centroids, codewords, lists)."""
+    with open(path, "rb") as f:
+        buf = f.read()
+    if buf[:8] != b"PRAGIX01":
+        raise ValueError("bad index magic")
+    ver, nlist, d, nsq = struct.unpack_from("<IIII", buf, 8)
+    off = 24
+    cent = np.frombuffer(buf, dtype=np.float32, count=nlist * d, offset=off).reshape(nlist, d)
+    off += 4 * nlist * d
+    words = np.frombuffer(buf, dtype=np.float32, count=256 * d, offset=off)
+    off += 4 * 256 * d
+    rec = np.dtype([("id", "<u8"), ("code", "u1", (nsq,))])
+    lists = []
+    for _ in range(nlist):
+        (n,) = struct.unpack_from("<Q", buf, off)
+        off += 8
+        lists.append(np.frombuffer(buf, dtype=rec, count=n, offset=off))
+        off += n * rec.itemsize
+    return (ver, nlist, d, nsq), cent, words, lists
+
+
+def write_shard_pragix(src: str, dst: str, rank: int, world: int) -> np.ndarray:
+    """Writes the PRAGIX01 file of one shard: the lists plan_shards assigns to
+    `rank` (others empty), centroids and codebooks replicated. Returns the
+    owner array. Host-only (no GPU)."""
+    (ver, nlist, d, nsq), cent, words, lists = _read_pragix(src)
+    owner = plan_shards([len(l) for l in lists], world)
+    with open(dst, "wb") as f:
+        f.write(b"PRAGIX01")
+        f.write(struct.pack("<IIII", ver, nlist, d, nsq))
+        f.write(cent.tobytes())
+        f.write(words.tobytes())
+        for l, o in zip(lists, owner):
+            keep = l if int(o) == rank else l[:0]
+            f.write(struct.pack("<Q", len(keep)))
+            f.write(keep.tobytes())
+    return owner

@@ -194,6 +194,10 @@ class GpuIndex:
         """0 = automatic (fast lane-skewed path when eligible), 1 = generic."""
         check(lib().prag_gpu_set_scan_path(self._h, path))
 
+    def set_coarse_path(self, path: int) -> None:
+        """0 = automatic (tensor-core pre-filter + exact window), 1 = exact SIMT."""
+        check(lib().prag_gpu_set_coarse_path(self._h, path))
+
     # profiling -------------------------------------------------------------
     def set_profiling(self, on: bool) -> None:
         check(lib().prag_gpu_set_profiling(self._h, 1 if on else 0))

@@ -137,7 +137,9 @@ def test_no_fma_contraction_in_sass():
     """Exactness guard: the reference folds are
     separately rounded mul/add; no kernel may contract them into FFMA. The
     only fused op allowed is the scan's explicit FFMA2 with 0/1 masks
-    (x*1 + acc == acc + x exactly)."""
+    (x*1 + acc == acc + x exactly). coarse_tc_kernel is exempt: it computes
+    the approximate GEMM-form pre-filter and its error bound; the exact
+    distances that decide the probe order come from select_window_kernel."""
     import shutil
     import subprocess
     exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
@@ -150,7 +152,7 @@ def test_no_fma_contraction_in_sass():
         if "Function :" in line:
             func = line.split("Function :")[1].strip()
         toks = line.split()
-        if any(t == "FFMA" or t.startswith("FFMA.") for t in toks):
+        if any(t == "FFMA" or t.startswith("FFMA.") for t in toks) and "coarse_tc_kernel" not in (func or ""):
             raise AssertionError(f"FFMA in {func}: {line.strip()}")
         if any(t.startswith("FFMA2") for t in toks):
             ffma2_funcs.add(func)

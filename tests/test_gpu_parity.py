@@ -222,3 +222,79 @@ def test_batch_edges(synth):
     r = ix.search_batch(q[:3], 5000, 1)
     o = oi.search(q[:3], 1, 5000)
     assert_same("bigk", r.ids, r.dist, r.count, r.scanned, *o)
+
+
+# ----------------------------------------------------- tensor-core coarse K1
+def _probe_both(ix, q, nprobe):
+    ix.set_coarse_path(0)
+    a = ix.probe(q, nprobe)
+    ix.set_coarse_path(1)
+    b = ix.probe(q, nprobe)
+    ix.set_coarse_path(0)
+    return a, b
+
+
+@pytest.mark.parametrize("nsq", [32, 64])
+def test_tc_coarse_probe_lists_exact(synth, nsq):
+    """K1 tcgen05 pre-filter + exact window rescoring == exact SIMT coarse ==
+    the oracle's sequential squared_l2 order (annindex.hpp:277-281)."""
+    p, q = synth[nsq]
+    ix = pg.GpuIndex.load(p, 0)
+    oi = O.OracleIndex(p)
+    for nprobe in (1, 2, 16, 64, 200, 256):
+        (tl, td), (el, ed) = _probe_both(ix, q, nprobe)
+        assert (tl == el).all(), f"nprobe={nprobe}: TC probe lists differ from exact"
+        assert (td.view(np.uint32) == ed.view(np.uint32)).all()
+        for i in range(0, q.shape[0], 7):
+            ol, od = oi.probe_lists(q[i], nprobe)
+            assert (tl[i] == ol).all() and (td[i].view(np.uint32) == od.view(np.uint32)).all()
+
+
+def _adversarial_index(tmp_path, nlist=256, d=64, nsq=16, dup=8, seed=3):
+    """Duplicated centroids (exact distance ties across lists), a far-away
+    cluster of centroids (large norms), and queries sitting exactly on
+    centroids (distance 0: A - E < 0)."""
+    rng = np.random.default_rng(seed)
+    cent = rng.standard_normal((nlist, d)).astype(np.float32)
+    for i in range(0, nlist, dup):  # blocks of identical centroids
+        cent[i:i + dup // 2] = cent[i]
+    cent[-32:] += np.float32(40.0)
+    words = rng.standard_normal((nsq, 256, d // nsq)).astype(np.float32) * np.float32(0.1)
+    lists = []
+    nid = 0
+    for l in range(nlist):
+        n = int(rng.integers(0, 40))
+        lists.append((np.arange(nid, nid + n, dtype=np.uint64), rng.integers(0, 256, (n, nsq), dtype=np.uint8)))
+        nid += n
+    p = str(tmp_path / "adv.pragix")
+    O.write_pragix(p, cent, words, lists)
+    q = np.concatenate([cent[:40], cent[:20] + np.float32(1e-3), rng.standard_normal((40, d)).astype(np.float32),
+                        cent[-8:] * np.float32(1.0001)]).astype(np.float32)
+    return p, q
+
+
+def test_tc_coarse_adversarial_ties(gpu, tmp_path):
+    p, q = _adversarial_index(tmp_path)
+    ix = pg.GpuIndex.load(p, gpu)
+    oi = O.OracleIndex(p)
+    for nprobe in (1, 3, 4, 5, 17, 128, 256):
+        (tl, td), (el, ed) = _probe_both(ix, q, nprobe)
+        assert (tl == el).all() and (td.view(np.uint32) == ed.view(np.uint32)).all(), f"nprobe={nprobe}"
+        for i in range(q.shape[0]):
+            ol, _ = oi.probe_lists(q[i], nprobe)
+            assert (tl[i] == ol).all(), (nprobe, i)
+    # full search through the TC path against the oracle
+    for nprobe, k in [(4, 10), (64, 5)]:
+        r = ix.search_batch(q, k, nprobe)
+        assert_same(f"adv/p{nprobe}", r.ids, r.dist, r.count, r.scanned, *oi.search(q, nprobe, k))
+
+
+def test_tc_coarse_large_batch(synth):
+    """nq > 256 spans several N tiles of the tcgen05 GEMM."""
+    p, q = synth[32]
+    ix = pg.GpuIndex.load(p, 0)
+    rng = np.random.default_rng(1)
+    qq = (q[rng.integers(0, q.shape[0], 600)] + rng.standard_normal((600, q.shape[1])).astype(np.float32) *
+          np.float32(0.3)).astype(np.float32)
+    (tl, td), (el, ed) = _probe_both(ix, qq, 16)
+    assert (tl == el).all() and (td.view(np.uint32) == ed.view(np.uint32)).all()

@@ -67,8 +67,9 @@ for nq in (1, 16, 64):
         med = {k: round(statistics.median([p[k] for p in ph]), 4) for k in
                ("coarse_ms", "select_ms", "plan_ms", "scan_ms", "final_ms", "total_ms")}
         sb = statistics.median([p["scanned_bytes"] for p in ph])
+        win = statistics.median([p["coarse_window"] for p in ph]) / nq
         r = {"nq": nq, "nprobe": nprobe, "host_issue_ms": round(statistics.median(host), 4),
-             "event_ms": round(statistics.median(ev), 4), "phases": med, "scanned_MB": round(sb / 1e6, 2),
+             "event_ms": round(statistics.median(ev), 4), "phases": med, "scanned_MB": round(sb / 1e6, 2), "coarse_window_per_q": win,
              "scan_GBps": round(sb / (med["scan_ms"] / 1e3) / 1e9, 1) if med["scan_ms"] else None}
         rows.append(r)
         print(json.dumps(r), flush=True)
