@@ -189,6 +189,16 @@ int prag_gpu_set_coarse_path(prag_gpu_index* index, int path);
 int prag_gpu_set_profiling(prag_gpu_index* index, int enabled);
 int prag_gpu_last_timings(const prag_gpu_index* index, prag_gpu_timings* out);
 
+/* ------------------------------------------------- config-E harness */
+/* One synthetic decode step on `stream` (device pointers): y[r] = W[r] . x
+ * for a rows x cols fp32 weight matrix, plus a streaming read of kv_floats
+ * of KV cache. The memory-bound stand-in for a RETRO decode step that the
+ * PipeRAG pipeline overlaps retrieval with; it replaces the reference's
+ * SyntheticGenerator (generator.hpp:220-252), whose per-token cost is affine
+ * in position. Not part of the retrieval path. y must hold rows + 1 floats. */
+int prag_gpu_synthetic_decode(const float* weights, uint64_t rows, uint32_t cols, const float* x, float* y,
+                              const float* kv, uint64_t kv_floats, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -94,6 +94,7 @@ SYMBOLS = [
     ("prag_gpu_set_coarse_path", C.c_int, [P, C.c_int]),
     ("prag_gpu_set_profiling", C.c_int, [P, C.c_int]),
     ("prag_gpu_last_timings", C.c_int, [P, C.POINTER(Timings)]),
+    ("prag_gpu_synthetic_decode", C.c_int, [P, C.c_uint64, C.c_uint32, P, P, P, C.c_uint64, P]),
 ]
 
 _lib = None

@@ -42,6 +42,7 @@ constexpr uint32_t kTcRows = 128;   // centroids per CTA (MMA M)
 constexpr uint32_t kTcKBlock = 32;  // K elements per pipeline stage
 constexpr uint32_t kTcMaxN = 64;    // queries per CTA (MMA N)
 constexpr uint32_t kTcSliceBlocks = 3;  // K blocks per CTA (K slice of 96)
+constexpr uint32_t kTcMaxSlices = 8;    // d <= 8 * 96 on the tensor-core path
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -149,8 +150,12 @@ __global__ void __launch_bounds__(128, 1) coarse_tc_kernel(const float* __restri
         bar_init(bars + 1, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         bar_expect_tx(bars, nkb * kA + nvalid * row_bytes);
+        // index data first: it does not depend on the previous kernel
         for (uint32_t i = 0; i < nkb; ++i)
             bulk_load(sA + i * kA, cent_tc + (size_t(tile) * nkb_all + kb0 + i) * (2 * kTcRows * kTcKBlock), kA, bars);
+    }
+    pdl_wait();
+    if (tid == 0) {
         for (uint32_t n = 0; n < nvalid; ++n)
             bulk_load(raw + size_t(n) * nkb * kTcKBlock, queries + size_t(q0 + n) * d + kb0 * kTcKBlock, row_bytes,
                       bars);
@@ -202,6 +207,7 @@ __global__ void __launch_bounds__(128, 1) coarse_tc_kernel(const float* __restri
     }
     bar_wait(bars + 1, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    pdl_trigger();
     // epilogue: TMEM lane = centroid row (warp w owns lanes 32w..32w+31)
     const uint32_t c = tile * kTcRows + warp * 32 + lane;
     float* out = partial + size_t(blockIdx.z) * nq * nlist;
@@ -314,17 +320,56 @@ __device__ uint32_t block_collect(uint32_t n, Pred pred, uint32_t* win, uint32_t
     return *counter;
 }
 
+// Exact fallback of K1b (window larger than kWinCap): the exact distance of
+// every list into the query's scratch row, then selection on the unique
+// (distance, list id) keys. Kept out of line: it never runs on well-posed
+// inputs and would otherwise bloat the hot kernel's instruction footprint.
+template <uint32_t VPT>
+__device__ __noinline__ uint32_t exact_fallback(float* upq, const float* __restrict__ centroids, const float* sq,
+                                                uint32_t nlist, uint32_t d, uint32_t nprobe, uint32_t* hist,
+                                                uint32_t* misc, uint32_t* win, float* wd) {
+    const uint32_t tid = threadIdx.x;
+    uint32_t W;
+        // fallback: exact distance of every list into this query's scratch row
+    __syncthreads();
+    for (uint32_t c = tid; c < nlist; c += kWinThreads) {
+        const float* row = centroids + size_t(c) * d;
+        float acc = 0.0f;
+#pragma unroll 8
+        for (uint32_t j = 0; j < d; ++j) {
+            const float diff = __fsub_rn(sq[j], __ldg(row + j));
+            acc = __fadd_rn(acc, __fmul_rn(diff, diff));
+        }
+        upq[c] = acc;
+    }
+    __syncthreads();
+    // (distance, list id) composite keys are unique: the nprobe-th one
+    // bounds a set of exactly nprobe lists
+    uint64_t key64[VPT];
+#pragma unroll
+    for (uint32_t i = 0; i < VPT; ++i) {
+        const uint32_t c = i * kWinThreads + tid;
+        key64[i] = c < nlist ? (uint64_t(fkey(upq[c])) << 32 | c) : ~0ull;
+    }
+    const uint64_t tkey = block_select_kth<VPT>(key64, nlist, nprobe, hist, misc);
+    W = block_collect(nlist, [&](uint32_t c) { return (uint64_t(fkey(upq[c])) << 32 | c) <= tkey; }, win,
+                      misc + 4);
+    for (uint32_t i = tid; i < W; i += kWinThreads) wd[i] = upq[win[i]];
+        return W;
+}
+
 // K1b. One CTA per query. Keys of A + E stay in registers (nlist <= 16384);
 // U = the nprobe-th smallest by a 4-pass radix select; the window is rescored
 // exactly and ranked. If the window exceeds kWinCap (not seen in practice:
 // windows are nprobe + a few) the CTA falls back to the
 // exact distance of every list and selects on the unique (distance, id) keys.
+template <uint32_t VPT>  // lists per thread: nlist <= VPT * 512
 __global__ void __launch_bounds__(kWinThreads) select_window_kernel(
     float* __restrict__ partial, uint32_t nslices, const float* __restrict__ cent_norm, float bound_c,
     const float* __restrict__ centroids, const float* __restrict__ queries, uint32_t nq, uint32_t nlist, uint32_t d,
     uint32_t nprobe, uint32_t* __restrict__ probe, float* __restrict__ probe_dist,
     unsigned long long* __restrict__ win_stat) {
-    extern __shared__ __align__(16) unsigned char sm[];
+    extern __shared__ __align__(1024) unsigned char sm[];
     uint32_t* hist = reinterpret_cast<uint32_t*>(sm);          // [256]
     uint32_t* misc = hist + 256;                               // [8]: [1] rank, [2..3] selected key, [4] count
     uint32_t* win = misc + 8;                                  // [kWinCap] list ids
@@ -334,7 +379,7 @@ __global__ void __launch_bounds__(kWinThreads) select_window_kernel(
     float* red = rows + kStageRows * (d + 1);                  // [kWinThreads / 32] reduction scratch
 
     const uint32_t q = blockIdx.x, tid = threadIdx.x;
-    constexpr uint32_t VPT = 32;  // nlist <= 32 * 512
+    pdl_wait();
     // ||q||^2 (any order: it only enters the approximate A and the bound E)
     float part = 0.0f;
     for (uint32_t j = tid; j < d; j += kWinThreads) {
@@ -357,8 +402,14 @@ __global__ void __launch_bounds__(kWinThreads) select_window_kernel(
         key[i] = 0xffffffffu;
         lov[i] = 0.0f;
         if (c < nlist) {
+            // all slices' loads issued together (compile-time bound), then summed
+            float pv[kTcMaxSlices];
+#pragma unroll
+            for (uint32_t z = 0; z < kTcMaxSlices; ++z)
+                pv[z] = z < nslices ? partial[(size_t(z) * nq + q) * nlist + c] : 0.0f;
             float dot = 0.0f;
-            for (uint32_t z = 0; z < nslices; ++z) dot += partial[(size_t(z) * nq + q) * nlist + c];
+#pragma unroll
+            for (uint32_t z = 0; z < kTcMaxSlices; ++z) dot += pv[z];
             const float nrm = __fadd_rn(qn, cent_norm[c]);
             const float a = __fsub_rn(nrm, __fmul_rn(2.0f, dot));
             const float e = __fmul_rn(bound_c, nrm);
@@ -421,33 +472,10 @@ __global__ void __launch_bounds__(kWinThreads) select_window_kernel(
             }
         }
     } else {
-        // fallback: exact distance of every list into this query's scratch row
-        __syncthreads();
-        for (uint32_t c = tid; c < nlist; c += kWinThreads) {
-            const float* row = centroids + size_t(c) * d;
-            float acc = 0.0f;
-#pragma unroll 8
-            for (uint32_t j = 0; j < d; ++j) {
-                const float diff = __fsub_rn(sq[j], __ldg(row + j));
-                acc = __fadd_rn(acc, __fmul_rn(diff, diff));
-            }
-            upq[c] = acc;
-        }
-        __syncthreads();
-        // (distance, list id) composite keys are unique: the nprobe-th one
-        // bounds a set of exactly nprobe lists
-        uint64_t key64[VPT];
-#pragma unroll
-        for (uint32_t i = 0; i < VPT; ++i) {
-            const uint32_t c = i * kWinThreads + tid;
-            key64[i] = c < nlist ? (uint64_t(fkey(upq[c])) << 32 | c) : ~0ull;
-        }
-        const uint64_t tkey = block_select_kth<VPT>(key64, nlist, nprobe, hist, misc);
-        W = block_collect(nlist, [&](uint32_t c) { return (uint64_t(fkey(upq[c])) << 32 | c) <= tkey; }, win,
-                          misc + 4);
-        for (uint32_t i = tid; i < W; i += kWinThreads) wd[i] = upq[win[i]];
+        W = exact_fallback<VPT>(upq, centroids, sq, nlist, d, nprobe, hist, misc, win, wd);
     }
     __syncthreads();
+    pdl_trigger();
     // rank by (distance, list id) (annindex.hpp:281 std::sort of pairs)
     for (uint32_t i = tid; i < W; i += kWinThreads) {
         const float di = wd[i];
@@ -472,7 +500,8 @@ size_t tc_window_smem(uint32_t d) {
 }
 
 bool tc_coarse_supported(uint32_t nlist, uint32_t d) {
-    return nlist % kTcRows == 0 && nlist <= 32 * kWinThreads && d % kTcKBlock == 0 && d <= 4096 &&
+    return nlist % kTcRows == 0 && nlist <= 32 * kWinThreads && d % kTcKBlock == 0 &&
+           d <= kTcMaxSlices * kTcSliceBlocks * kTcKBlock &&
            tc_window_smem(d) <= 227 * 1024;
 }
 
@@ -518,8 +547,9 @@ int launch_coarse_tc(const DeviceIndex& ix, const float* queries, uint32_t nq, f
                         size_t(n_tile) * kTcSliceBlocks * kTcKBlock * 4 + 2 * 8 + 16;
     PG_CUDA(cudaFuncSetAttribute(coarse_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     dim3 grid(ix.nlist / kTcRows, (nq + n_tile - 1) / n_tile, tc_slices(ix.d));
-    coarse_tc_kernel<<<grid, 128, smem, s>>>(ix.cent_tc, queries, nq, ix.nlist, ix.d, n_tile, partial);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = launch_pdl(coarse_tc_kernel, grid, dim3(128), smem, s, ix.cent_tc, queries, nq, ix.nlist, ix.d,
+                               n_tile, partial);
+    if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) {
         set_error(std::string("CUDA launch failed (coarse_tc): ") + cudaGetErrorString(e));
         return PRAG_GPU_CUDA;
@@ -530,10 +560,26 @@ int launch_coarse_tc(const DeviceIndex& ix, const float* queries, uint32_t nq, f
 int launch_select_window(const DeviceIndex& ix, float* partial, const float* queries, uint32_t nq, uint32_t nprobe,
                          uint32_t* probe, float* probe_dist, unsigned long long* win_stat, cudaStream_t s) {
     const size_t smem = tc_window_smem(ix.d);
-    PG_CUDA(cudaFuncSetAttribute(select_window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    select_window_kernel<<<nq, kWinThreads, smem, s>>>(partial, tc_slices(ix.d), ix.cent_norm, tc_bound_c(ix.d),
-                                                       ix.centroids, queries, nq, ix.nlist, ix.d, nprobe, probe,
-                                                       probe_dist, win_stat);
+#define PG_WIN(V)                                                                                              \
+    do {                                                                                                       \
+        PG_CUDA(cudaFuncSetAttribute(select_window_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+                                     int(smem)));                                                              \
+        PG_CUDA(launch_pdl(select_window_kernel<V>, dim3(nq), dim3(kWinThreads), smem, s, partial,           \
+                           tc_slices(ix.d), ix.cent_norm, tc_bound_c(ix.d), ix.centroids, queries, nq, ix.nlist, \
+                           ix.d, nprobe, probe, probe_dist, win_stat));                                         \
+    } while (0)
+    const uint32_t vpt = (ix.nlist + kWinThreads - 1) / kWinThreads;
+    if (vpt <= 2)
+        PG_WIN(2);
+    else if (vpt <= 4)
+        PG_WIN(4);
+    else if (vpt <= 8)
+        PG_WIN(8);
+    else if (vpt <= 16)
+        PG_WIN(16);
+    else
+        PG_WIN(32);
+#undef PG_WIN
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         set_error(std::string("CUDA launch failed (select_window): ") + cudaGetErrorString(e));

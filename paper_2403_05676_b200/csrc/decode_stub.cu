@@ -1,0 +1,72 @@
+// decode_stub.cu -- the generator side of the config-E harness (BASELINE.json
+// configs[4]): a memory-bound stand-in for one RETRO
+// decode step, so retrieval on a side stream can be overlapped with -- and
+// contend for HBM with -- real GPU work. It plays the role of the
+// reference's SyntheticGenerator (generator.hpp:220-252), whose per-token
+// cost is affine in position: here a GEMV over the model's fp32 weights
+// (constant term; PAPER.md:347/703 RETRO 582M -> ~2.3 GB per token) plus a
+// read of the KV cache of every earlier position (the linear term).
+#include <cstdint>
+
+#include "internal.h"
+
+namespace pg {
+namespace {
+
+constexpr int kDecThreads = 256;
+
+// y[r] = sum_j W[r][j] * x[j]  (cols % 4 == 0), one warp per row, grid-stride;
+// then the first CTA-wide pass over kv folds it into y[0] so it is not dead.
+__global__ void __launch_bounds__(kDecThreads) decode_step_kernel(const float4* __restrict__ w, uint64_t rows,
+                                                                  uint32_t cols4, const float4* __restrict__ x,
+                                                                  float* __restrict__ y,
+                                                                  const float4* __restrict__ kv, uint64_t kv4) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warp = (uint64_t(blockIdx.x) * kDecThreads + threadIdx.x) >> 5;
+    const uint64_t nwarps = (uint64_t(gridDim.x) * kDecThreads) >> 5;
+    for (uint64_t r = warp; r < rows; r += nwarps) {
+        const float4* row = w + r * cols4;
+        float acc = 0.0f;
+        for (uint32_t j = lane; j < cols4; j += 32) {
+            const float4 a = __ldcs(row + j);
+            const float4 b = __ldg(x + j);
+            acc += a.x * b.x + a.y * b.y + a.z * b.z + a.w * b.w;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) y[r] = acc;
+    }
+    // attention stand-in: stream the KV cache of positions < current
+    float s = 0.0f;
+    for (uint64_t i = uint64_t(blockIdx.x) * kDecThreads + threadIdx.x; i < kv4; i += uint64_t(gridDim.x) * kDecThreads) {
+        const float4 v = __ldcs(kv + i);
+        s += v.x + v.y + v.z + v.w;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0 && s == 1234.5678f) y[rows] = s;  // data-dependent sink: keeps the reads
+}
+
+}  // namespace
+}  // namespace pg
+
+extern "C" int prag_gpu_synthetic_decode(const float* weights, uint64_t rows, uint32_t cols, const float* x, float* y,
+                                         const float* kv, uint64_t kv_floats, void* stream) {
+    using namespace pg;
+    if (!weights || !x || !y || cols % 4 != 0 || (kv_floats && !kv) || kv_floats % 4 != 0) {
+        set_error("synthetic_decode: bad arguments (cols and kv_floats must be multiples of 4)");
+        return PRAG_GPU_CONFIG;
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    decode_step_kernel<<<sms * 4, kDecThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+        reinterpret_cast<const float4*>(weights), rows, cols / 4, reinterpret_cast<const float4*>(x), y,
+        reinterpret_cast<const float4*>(kv), kv_floats / 4);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error(std::string("CUDA launch failed (synthetic_decode): ") + cudaGetErrorString(e));
+        return PRAG_GPU_CUDA;
+    }
+    return PRAG_GPU_OK;
+}

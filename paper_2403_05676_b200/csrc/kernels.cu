@@ -616,6 +616,7 @@ __global__ void __launch_bounds__(kSelThreads) select_pool_kernel(
     extern __shared__ __align__(16) unsigned char smraw[];
     SelShared& sm = *reinterpret_cast<SelShared*>(smraw);
     const uint32_t q = blockIdx.x, tid = threadIdx.x;
+    pdl_wait();  // the pool comes from the scan kernel
     const size_t off = size_t(q_item_off[q]) * warps * k;
     const uint32_t n = pool_cnt[q];
     constexpr int VPT = 8;
@@ -679,9 +680,9 @@ int launch_select_pool(const uint32_t* pool_key, const uint64_t* pool_id, const 
                        cudaStream_t s) {
     PG_CUDA(cudaFuncSetAttribute(select_pool_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(sizeof(SelShared))));
-    select_pool_kernel<<<nq, kSelThreads, sizeof(SelShared), s>>>(pool_key, pool_id, pool_cnt, q_item_off, warps, k,
-                                                                   out_ids, out_dist, out_count, gkey, gtie, pw);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = launch_pdl(select_pool_kernel, dim3(nq), dim3(kSelThreads), sizeof(SelShared), s, pool_key,
+                               pool_id, pool_cnt, q_item_off, warps, k, out_ids, out_dist, out_count, gkey, gtie, pw);
+    if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) {
         set_error(std::string("CUDA launch failed (select_pool): ") + cudaGetErrorString(e));
         return PRAG_GPU_CUDA;

@@ -72,14 +72,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
-__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
-    uint4 r;
-    asm volatile("ld.global.cs.v4.u32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "l"(p));
-    return r;
-}
-
 // {c0, c1} = {a*b0 + c0, a*b1 + c1}: two independent IEEE fp32 FMAs (rn) in
 // one FFMA2 with a scalar-broadcast first operand.
 __device__ __forceinline__ void fma2_bcast(float& c0, float& c1, float a, float b0, float b1) {
@@ -138,8 +130,8 @@ constexpr uint32_t image_floats() {
 // (coalesced), the next subquantizer's prefetched while the current one is
 // folded. Residuals sit in SMEM as [sq][j][pair] so one LDS.128 broadcasts
 // four pairs' values.
-template <int M, int SUBC>  // SUBC: compile-time sub_dim (0 = runtime `sub`, <= 16)
-__global__ void __launch_bounds__(256, 1) lut_image_kernel(const float* __restrict__ queries,
+template <int M, int SUBC, int SQB>  // SUBC: compile-time sub_dim (0 = runtime `sub`, <= 16); SQB subquantizers per CTA
+__global__ void __launch_bounds__(256, 2) lut_image_kernel(const float* __restrict__ queries,
                                                            const float* __restrict__ centroids,
                                                            const float* __restrict__ codewordsT,
                                                            const uint32_t* __restrict__ probe,
@@ -153,16 +145,14 @@ __global__ void __launch_bounds__(256, 1) lut_image_kernel(const float* __restri
     __shared__ uint32_t s_q[P], s_list[P];
     const uint32_t npairs = nq * nprobe;
     const uint32_t p0 = blockIdx.x * P;
-    const uint32_t sq0 = blockIdx.y * 8;
+    const uint32_t sq0 = blockIdx.y * SQB;
     const uint32_t code = threadIdx.x;
-    // all 8 subquantizers' codewords requested before anything else (one
-    // memory round trip instead of one per subquantizer)
-    float wall[8][JMAX];
+    // prefetch the first subquantizer's codeword before anything else
+    float wn[JMAX];
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < JMAX; ++j)
-            if (j < int(sub)) wall[i][j] = __ldg(codewordsT + (size_t(sq0 + i) * sub + j) * 256 + code);
+    for (int j = 0; j < JMAX; ++j)
+        if (j < int(sub)) wn[j] = __ldg(codewordsT + (size_t(sq0) * sub + j) * 256 + code);
+    pdl_wait();  // probe[] comes from the previous kernel
     if (threadIdx.x < P) {
         const uint32_t pair = p0 + threadIdx.x;
         uint32_t list = 0xffffffffu;
@@ -179,7 +169,7 @@ __global__ void __launch_bounds__(256, 1) lut_image_kernel(const float* __restri
     for (int p = 0; p < P; ++p) live |= (s_list[p] != 0xffffffffu) << p;
     if (!live) return;
     // residual r = q - c_list (annindex.hpp:288) for this CTA's 8 subquantizers
-    const uint32_t span = 8 * sub;  // contiguous dims [sq0*sub, +span)
+    const uint32_t span = SQB * sub;  // contiguous dims [sq0*sub, +span)
     for (uint32_t t = threadIdx.x; t < span * P; t += blockDim.x) {
         const uint32_t p = t / span, k = t - p * span;
         const uint32_t sl = k / sub, j = k - sl * sub;
@@ -191,10 +181,17 @@ __global__ void __launch_bounds__(256, 1) lut_image_kernel(const float* __restri
         resid[(sl * 16 + j) * P + p] = v;
     }
     __syncthreads();
-    float tv[8][P];  // T[sq0 + i][code] for each pair
+    float tv[SQB][P];  // T[sq0 + i][code] for each pair
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const float* w = wall[i];
+    for (int i = 0; i < SQB; ++i) {
+        float w[JMAX];
+#pragma unroll
+        for (int j = 0; j < JMAX; ++j) w[j] = wn[j];
+        if (i + 1 < SQB) {
+#pragma unroll
+            for (int j = 0; j < JMAX; ++j)
+                if (j < int(sub)) wn[j] = __ldg(codewordsT + (size_t(sq0 + i + 1) * sub + j) * 256 + code);
+        }
         float acc[P];
 #pragma unroll
         for (int p = 0; p < P; ++p) acc[p] = 0.0f;
@@ -216,13 +213,14 @@ __global__ void __launch_bounds__(256, 1) lut_image_kernel(const float* __restri
 #pragma unroll
         for (int p = 0; p < P; ++p) tv[i][p] = acc[p];
     }
+    pdl_trigger();
     // compact table luts[pair][sq][256]: each store is 32 consecutive codes
 #pragma unroll
     for (int p = 0; p < P; ++p) {
         if (!(live >> p & 1u)) continue;
         float* dst = luts + (size_t(p0 + p) * M + sq0) * 256 + code;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) dst[i * 256] = tv[i][p];
+        for (int i = 0; i < SQB; ++i) dst[i * 256] = tv[i][p];
     }
 }
 
@@ -232,13 +230,15 @@ struct SkewCfg;
 template <>
 struct SkewCfg<32> {
     static constexpr int kWarps = 13;  // consumer warps; + 1 producer + 2 expander warps, 1 CTA per SM
-    static constexpr int kDepth = 4;   // code tiles in flight per consumer warp (TMA ring)
+    static constexpr int kDepth = 4;   // TMA ring slots per consumer warp
+    static constexpr int kGroup = 1;   // code tiles per ring slot
     static constexpr int kBufs = 2;    // SMEM images: item i+1's is built while item i is scanned
 };
 template <>
 struct SkewCfg<64> {
     static constexpr int kWarps = 8;
     static constexpr int kDepth = 2;
+    static constexpr int kGroup = 1;
     static constexpr int kBufs = 1;    // 128 KiB image: single-buffered
 };
 constexpr int kExpWarps = 2;
@@ -265,7 +265,7 @@ struct SkewSmem {
     static constexpr uint32_t kImg = image_floats<M>() * 4;  // R x 64 KiB
     static constexpr uint32_t kStage = 32768;                // 32 subquantizers of T[sq][256] fp32
     static constexpr uint32_t kTile = 32u * M;
-    static constexpr uint32_t kRing = uint32_t(D) * kTile;   // per consumer warp
+    static constexpr uint32_t kRing = uint32_t(D) * SkewCfg<M>::kGroup * kTile;  // per consumer warp
     // img_full[NB], img_empty[NB], stg_full, stg_empty, ring[W*D]
     static constexpr uint32_t nbars = 2 * NB + 2 + W * D;
     static constexpr uint32_t kTail = 8 * nbars + (NB + 1) * uint32_t(sizeof(ItemSlot));
@@ -347,7 +347,7 @@ struct ScanCtx {
 template <int M>
 __device__ __forceinline__ void scan_range(const ScanCtx& cx, const ItemSlot& sl, uint32_t a, uint32_t e_end,
                                            uint32_t& consumed, const float* mk, const float* nk) {
-    constexpr int W = SkewCfg<M>::kWarps, D = SkewCfg<M>::kDepth;
+    constexpr int W = SkewCfg<M>::kWarps, D = SkewCfg<M>::kDepth, G = SkewCfg<M>::kGroup;
     constexpr int kChunks = M / 16;
     constexpr uint32_t kTileBytes = 32u * M;
     const uint32_t lane = cx.lane, bt = cx.bt, k = cx.k, ring_s = cx.ring_s;
@@ -364,41 +364,50 @@ __device__ __forceinline__ void scan_range(const ScanCtx& cx, const ItemSlot& sl
     const unsigned char* tiles = skew_codes + sl.tile_byte_off;
     // this warp streams tiles a..e_end inclusive: tile e_end holds the
     // tails of the range's last entries
+    // the ring holds D slots of G tiles; slot i of this range covers tiles
+    // a + G*i .. a + G*i + G - 1 (clipped to e_end)
     if (lane == 0) {
-        for (uint32_t t = 0; t < uint32_t(D) && a + t <= e_end; ++t) {
+        for (uint32_t t = 0; t < uint32_t(D) && a + G * t <= e_end; ++t) {
             const uint32_t slot = (consumed + t) % D;
-            mbar_expect_tx(wbar + slot, kTileBytes);
-            bulk_g2s(wring + slot * kTileBytes, tiles + size_t(a + t) * kTileBytes, kTileBytes, wbar + slot);
+            const uint32_t bytes = min(uint32_t(G), e_end - (a + G * t) + 1) * kTileBytes;
+            mbar_expect_tx(wbar + slot, bytes);
+            bulk_g2s(wring + slot * G * kTileBytes, tiles + size_t(a + G * t) * kTileBytes, bytes, wbar + slot);
         }
     }
     uint32_t tk_key = 0xffffffffu;  // warp top-k: lane i holds the i-th (distance bits, entry slot)
     uint32_t tk_pos = 0xffffffffu;
     uint32_t thr_key = 0xffffffffu;
-    uint32_t g_thr = ld_relaxed(gthr + q), g_next = 0xffffffffu;
+    // the query's shared threshold (other warps' k-th distances) is read once
+    // per range: an in-loop refresh would put a global load on every tile
+    uint32_t g_thr = ld_relaxed(gthr + q);
     float cur = 0.0f, prev = 0.0f;
-    for (uint32_t j = a; j <= e_end; ++j, ++consumed) {
+    for (uint32_t j0 = a; j0 <= e_end; j0 += G, ++consumed) {
         const uint32_t slot = consumed % D;
         mbar_wait(wbar + slot, (consumed / D) & 1u);
+#pragma unroll
+        for (uint32_t g = 0; g < uint32_t(G); ++g) {
+        const uint32_t j = j0 + g;
+        if (G > 1 && j > e_end) break;
         uint32_t wd[M / 4];
 #pragma unroll
         for (int c = 0; c < kChunks; ++c) {
-            const uint4 v = lds_u4(ring_s + slot * kTileBytes + c * 512 + lane * 16);
+            const uint4 v = lds_u4(ring_s + (slot * G + g) * kTileBytes + c * 512 + lane * 16);
             wd[4 * c] = v.x;
             wd[4 * c + 1] = v.y;
             wd[4 * c + 2] = v.z;
             wd[4 * c + 3] = v.w;
         }
-        // refresh the query's shared threshold (a pruning hint only): the load
-        // issued every 8th tile is consumed a tile later
-        g_thr = min(g_thr, g_next);
-        if (((j - a) & 7u) == 0u) g_next = __ldcg(gthr + q);
         skew_round<M>(wd, bt, cur, prev, mk, nk, std::make_integer_sequence<int, M>{});
-        // the codes of this slot are consumed (every lane's LDS.128 result
-        // was used by the steps above): refill it with tile j + D
-        __syncwarp();
-        if (lane == 0 && j + D <= e_end) {
-            mbar_expect_tx(wbar + slot, kTileBytes);
-            bulk_g2s(wring + slot * kTileBytes, tiles + size_t(j + D) * kTileBytes, kTileBytes, wbar + slot);
+        if (g + 1 == uint32_t(G) || j == e_end) {
+            // the codes of this slot are consumed (every lane's LDS.128 result
+            // was used by the steps above): refill it with the tiles D slots on
+            __syncwarp();
+            const uint32_t jr = j0 + uint32_t(D) * G;
+            if (lane == 0 && jr <= e_end) {
+                const uint32_t bytes = min(uint32_t(G), e_end - jr + 1) * kTileBytes;
+                mbar_expect_tx(wbar + slot, bytes);
+                bulk_g2s(wring + slot * G * kTileBytes, tiles + size_t(jr) * kTileBytes, bytes, wbar + slot);
+            }
         }
         // entry 32(j-1)+lane is complete in `prev`
         const uint32_t e = (j - 1) * kTileEntries + lane;
@@ -445,9 +454,13 @@ __device__ __forceinline__ void scan_range(const ScanCtx& cx, const ItemSlot& sl
                 g_thr = thr_key;
             }
         }
+        }  // g
     }
-    // publish this warp's list into the query's candidate pool
-    const unsigned have = __ballot_sync(0xffffffffu, lane < k && tk_key != 0xffffffffu);
+    // publish this warp's list into the query's candidate pool, minus entries
+    // above the query's shared threshold: some warp holds k candidates at or
+    // below it, so those entries cannot make the final top-k
+    const uint32_t g_pub = min(g_thr, ld_relaxed(gthr + q));
+    const unsigned have = __ballot_sync(0xffffffffu, lane < k && tk_key != 0xffffffffu && tk_key <= g_pub);
     const uint32_t cnt = __popc(have);
     if (cnt) {
         uint32_t base = 0;
@@ -525,6 +538,7 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    pdl_wait();  // items, LUTs and thresholds come from the previous kernels
     const uint32_t total = *num_items;
 
     if (warp == uint32_t(W)) {
@@ -548,6 +562,7 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
                     nx = atomicAdd(cursor, 1u);  // next item's index, fetched ahead
                 }
                 if (sl.pair == kEndItem) {
+                    pdl_trigger();  // no more work items: let the pool selection launch
                     mbar_wait(stg_empty, (round & 1u) ^ 1u);
                     *stg_slot = sl;
                     mbar_arrive(stg_full);
@@ -669,6 +684,7 @@ __global__ void __launch_bounds__(1024) plan_skew_kernel(const uint32_t* __restr
     __shared__ uint32_t tmp[33];
     __shared__ uint32_t bucket_cnt[32], bucket_pos[32];
     const uint32_t P = nq * nprobe;
+    pdl_wait();  // probe[] comes from the previous kernel
     if (threadIdx.x < 32) bucket_cnt[threadIdx.x] = 0;
     for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x) scanned[q] = 0;
     __syncthreads();
@@ -720,6 +736,7 @@ __global__ void __launch_bounds__(1024) plan_skew_kernel(const uint32_t* __restr
         }
     }
     __syncthreads();
+    pdl_trigger();
     // pass 2: scatter items
     for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
         const uint32_t len = list_len[probe[i]];
@@ -767,18 +784,27 @@ static int check(const char* what) {
 int launch_plan_skew(const DeviceIndex& ix, const uint32_t* probe, uint32_t nq, uint32_t nprobe, uint32_t it_tiles,
                      uint64_t* scanned, uint4* items, uint32_t* num_items, uint32_t* cursor, uint32_t* q_item_off,
                      uint32_t* gthr, uint32_t* pool_cnt, uint64_t item_cap, cudaStream_t s) {
-    plan_skew_kernel<<<1, 1024, 0, s>>>(probe, ix.list_len, nq, nprobe, it_tiles, scanned, items, num_items, cursor,
-                                        q_item_off, gthr, pool_cnt, item_cap);
+    PG_CUDA(launch_pdl(plan_skew_kernel, dim3(1), dim3(1024), 0, s, probe, ix.list_len, nq, nprobe, it_tiles, scanned,
+                       items, num_items, cursor, q_item_off, gthr, pool_cnt, item_cap));
     return check("plan_skew");
 }
 
 int launch_lut_images(const DeviceIndex& ix, const float* queries, const uint32_t* probe, uint32_t nq,
                       uint32_t nprobe, float* luts, cudaStream_t s) {
     const uint32_t npairs = nq * nprobe;
-    dim3 grid((npairs + kLutPairs - 1) / kLutPairs, ix.nsq / 8);
-#define PG_LUT(MM, SS)                                                                                     \
-    lut_image_kernel<MM, SS><<<grid, 256, 0, s>>>(queries, ix.centroids, ix.codewordsT, probe, ix.list_len, nq, \
-                                                  nprobe, ix.d, ix.sub_dim, luts)
+    // small batches: 2 subquantizers per CTA (4x the CTAs, 1/4 of the serial
+    // codeword round trips each); large ones: 8 (residuals shared by more work)
+    const bool small = uint64_t((npairs + kLutPairs - 1) / kLutPairs) * (ix.nsq / 8) < 2 * 148;
+    dim3 grid((npairs + kLutPairs - 1) / kLutPairs, ix.nsq / (small ? 2 : 8));
+#define PG_LUT(MM, SS)                                                                                          \
+    do {                                                                                                        \
+        if (small)                                                                                              \
+            PG_CUDA(launch_pdl(lut_image_kernel<MM, SS, 2>, grid, dim3(256), 0, s, queries, ix.centroids,       \
+                               ix.codewordsT, probe, ix.list_len, nq, nprobe, ix.d, ix.sub_dim, luts));           \
+        else                                                                                                    \
+            PG_CUDA(launch_pdl(lut_image_kernel<MM, SS, 8>, grid, dim3(256), 0, s, queries, ix.centroids,       \
+                               ix.codewordsT, probe, ix.list_len, nq, nprobe, ix.d, ix.sub_dim, luts));           \
+    } while (0)
     if (ix.nsq == 32 && ix.sub_dim == 12)
         PG_LUT(32, 12);
     else if (ix.nsq == 32)
@@ -798,15 +824,15 @@ int launch_scan_skew(const DeviceIndex& ix, const uint4* items, const uint32_t* 
     if (ix.nsq == 32) {
         const size_t smem = skew_smem_bytes<32>();
         PG_CUDA(cudaFuncSetAttribute(scan_skew_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        scan_skew_kernel<32><<<grid, SkewSmem<32>::threads, smem, s>>>(
-            items, num_items, cursor, probe, ix.list_len, ix.skew_off, ix.skew_codes, ix.list_off, ix.ids, luts,
-            nprobe, k, gthr, q_item_off, pool_cnt, pool_key, pool_id);
+        PG_CUDA(launch_pdl(scan_skew_kernel<32>, dim3(grid), dim3(SkewSmem<32>::threads), smem, s, items, num_items,
+                           cursor, probe, ix.list_len, ix.skew_off, ix.skew_codes, ix.list_off, ix.ids, luts, nprobe, k,
+                           gthr, q_item_off, pool_cnt, pool_key, pool_id));
     } else {
         const size_t smem = skew_smem_bytes<64>();
         PG_CUDA(cudaFuncSetAttribute(scan_skew_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        scan_skew_kernel<64><<<grid, SkewSmem<64>::threads, smem, s>>>(
-            items, num_items, cursor, probe, ix.list_len, ix.skew_off, ix.skew_codes, ix.list_off, ix.ids, luts,
-            nprobe, k, gthr, q_item_off, pool_cnt, pool_key, pool_id);
+        PG_CUDA(launch_pdl(scan_skew_kernel<64>, dim3(grid), dim3(SkewSmem<64>::threads), smem, s, items, num_items,
+                           cursor, probe, ix.list_len, ix.skew_off, ix.skew_codes, ix.list_off, ix.ids, luts, nprobe, k,
+                           gthr, q_item_off, pool_cnt, pool_key, pool_id));
     }
     return check("scan_skew");
 }

@@ -104,7 +104,7 @@ def build_ivfpq(n: int, d: int, nlist: int, nsq: int, seed: int = 1, device=None
     t0 = time.time()
     nchunks = (n + chunk - 1) // chunk
     # training sample: the first rows of the first chunks (data are i.i.d.)
-    S = min(n, train_sample)
+    S = min(n, max(train_sample, 16 * nlist))
     parts, got, ci = [], 0, 0
     while got < S:
         rows = min(chunk, n - ci * chunk)
@@ -128,16 +128,21 @@ def build_ivfpq(n: int, d: int, nlist: int, nsq: int, seed: int = 1, device=None
     qrng = np.random.default_rng(seed + 13)
     qrows = np.sort(qrng.choice(n, size=min(nq, n), replace=False)) if nq else np.zeros(0, np.int64)
     queries = np.zeros((len(qrows), d), dtype=np.float32)
+    blk = max(1024, min(chunk, (1 << 31) // max(nlist, 256 * nsq)))  # bound the distance matrices
     for ci in range(nchunks):
         r0 = ci * chunk
         rows = min(chunk, n - r0)
-        x = _chunk_rows(seed, ci, rows, d, dev)
-        aa = ((x * x).sum(1, keepdim=True) - 2.0 * x @ cents.T + c2[None, :]).argmin(1)
-        r = (x - cents[aa]).reshape(rows, nsq, sub).transpose(0, 1)  # [nsq, rows, sub]
-        dd = w2[:, None, :] - 2.0 * torch.bmm(r, words.transpose(1, 2))
-        cc = dd.argmin(2).T.contiguous()  # [rows, nsq]
-        assign[r0:r0 + rows] = aa.cpu().numpy()
-        codes[r0:r0 + rows] = cc.to(torch.uint8).cpu().numpy()
+        xc = _chunk_rows(seed, ci, rows, d, dev)
+        for b0 in range(0, rows, blk):
+            x = xc[b0:b0 + blk]
+            br = x.shape[0]
+            aa = ((x * x).sum(1, keepdim=True) - 2.0 * x @ cents.T + c2[None, :]).argmin(1)
+            r = (x - cents[aa]).reshape(br, nsq, sub).transpose(0, 1)  # [nsq, rows, sub]
+            dd = w2[:, None, :] - 2.0 * torch.bmm(r, words.transpose(1, 2))
+            cc = dd.argmin(2).T.contiguous()  # [rows, nsq]
+            assign[r0 + b0:r0 + b0 + br] = aa.cpu().numpy()
+            codes[r0 + b0:r0 + b0 + br] = cc.to(torch.uint8).cpu().numpy()
+        x = xc
         sel = qrows[(qrows >= r0) & (qrows < r0 + rows)]
         if len(sel):
             idx = np.searchsorted(qrows, sel)
