@@ -300,7 +300,7 @@ def main():
     # ---------------- roofline of the dominant kernel (fused LUT+scan+select)
     ix.set_profiling(True)
     tm_acc = {"scan_ms": 0.0, "total_ms": 0.0, "scanned_bytes": 0, "coarse_ms": 0.0, "select_ms": 0.0,
-              "plan_ms": 0.0, "final_ms": 0.0, "work_items": 0}
+              "plan_ms": 0.0, "final_ms": 0.0, "work_items": 0, "coarse_window": 0}
     prof_steps = max(5, min(args.steps, 20))
     for i in range(prof_steps):
         with torch.cuda.stream(stream):
@@ -325,7 +325,26 @@ def main():
                 traffic = tj.get("dram_bytes_per_launch")
         except Exception:
             pass
-    roofline = {"bound": "hbm", "kernel": "scan_kernel (fused ADC LUT + list scan)", "achieved": round(achieved, 1),
+    # K1 (tcgen05 3xTF32 GEMM pre-filter): flops actually issued to the tensor
+    # pipe (3 MMAs per product) over K1's CUDA-event time, against the TF32
+    # dense peak (half the measured bf16 figure: kind::tf32 runs at 1/2 rate)
+    k1_ms = tm_acc["coarse_ms"] / prof_steps
+    k1_flops = 3 * 2 * nq * cfg["nlist"] * cfg["d"]
+    bf16 = None
+    try:
+        bf16 = float(json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))["bf16_tflops"])
+    except Exception:
+        bf16 = 2250.0
+    roofline_coarse = {"bound": "tensor", "kernel": "coarse_tc_kernel (tcgen05 kind::tf32, 3xTF32)",
+                       "achieved": round(k1_flops / (k1_ms / 1e3) / 1e12, 2) if k1_ms > 0 else None,
+                       "peak": round(bf16 / 2, 1), "unit": "TFLOP/s",
+                       "peak_source": "MEASURED_PEAKS.json bf16_tflops / 2 (TF32 rate)",
+                       "kernel_ms": round(k1_ms, 4), "flops_per_launch": k1_flops,
+                       "window_lists_per_query": round(tm_acc["coarse_window"] / prof_steps / nq, 2),
+                       "note": "latency-bound at this GEMM size (nq x nlist x d = 64 x 4096 x 384)"}
+    if roofline_coarse["achieved"] is not None:
+        roofline_coarse["frac"] = round(roofline_coarse["achieved"] / roofline_coarse["peak"], 4)
+    roofline = {"bound": "hbm", "kernel": "scan_skew_kernel (ADC list scan + warp top-k)", "achieved": round(achieved, 1),
                 "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4), "traffic": traffic,
                 "peak_source": peak_src, "alg_bytes_per_launch": int(bytes_launch),
                 "kernel_ms": round(scan_ms, 4), "kernel_share_of_step": round(scan_ms / (tm_acc["total_ms"] /
@@ -379,8 +398,8 @@ def main():
                 "e2e": {"value": round(e2e_val, 1), "unit": "queries/s", "ms_per_step": round(e2e_ms, 4),
                         "p50_batch_ms": round(statistics.median(t_e2e), 4), "h2d_bytes_per_step": h2d,
                         "d2h_bytes_per_step": d2h},
-                "gpu_launches": 5 * (args.steps) + (args.steps if world > 1 else 0),
-                "roofline": roofline, "cpu_baseline": cpu_baseline, "clocks": clocks, "sweep": sweep,
+                "gpu_launches": 6 * (args.steps) + (args.steps if world > 1 else 0),
+                "roofline": roofline, "roofline_coarse": roofline_coarse, "cpu_baseline": cpu_baseline, "clocks": clocks, "sweep": sweep,
                 "perf_model": perf_models}
         print(json.dumps(line))
     if world > 1:

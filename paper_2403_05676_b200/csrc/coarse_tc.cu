@@ -375,10 +375,17 @@ __global__ void __launch_bounds__(kWinThreads) select_window_kernel(
     uint32_t* win = misc + 8;                                  // [kWinCap] list ids
     float* wd = reinterpret_cast<float*>(win + kWinCap);       // [kWinCap] exact distances
     float* sq = wd + kWinCap;                                  // [d] the query
-    float* rows = sq + ((d + 3) & ~3u);                        // [kStageRows][d + 1]
-    float* red = rows + kStageRows * (d + 1);                  // [kWinThreads / 32] reduction scratch
+    float* rows = sq + ((d + 3) & ~3u);                        // [2][kStageRows][d + 1]
+    float* red = rows + 2 * kStageRows * (d + 1);              // [kWinThreads / 32] reduction scratch
 
     const uint32_t q = blockIdx.x, tid = threadIdx.x;
+    // ||c||^2 is index data: load it before waiting on the previous kernel
+    float cnv[VPT];
+#pragma unroll
+    for (uint32_t i = 0; i < VPT; ++i) {
+        const uint32_t c = i * kWinThreads + tid;
+        cnv[i] = c < nlist ? __ldg(cent_norm + c) : 0.0f;
+    }
     pdl_wait();
     // ||q||^2 (any order: it only enters the approximate A and the bound E)
     float part = 0.0f;
@@ -390,10 +397,25 @@ __global__ void __launch_bounds__(kWinThreads) select_window_kernel(
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
     if ((tid & 31) == 0) red[tid >> 5] = part;
+    // q.c: sum of K1's slices; each slice's VPT loads are issued together
+    float dot[VPT];
+#pragma unroll
+    for (uint32_t i = 0; i < VPT; ++i) dot[i] = 0.0f;
+    for (uint32_t z = 0; z < nslices; ++z) {
+        float pv[VPT];
+        const float* pz = partial + (size_t(z) * nq + q) * nlist;
+#pragma unroll
+        for (uint32_t i = 0; i < VPT; ++i) {
+            const uint32_t c = i * kWinThreads + tid;
+            pv[i] = c < nlist ? pz[c] : 0.0f;
+        }
+#pragma unroll
+        for (uint32_t i = 0; i < VPT; ++i) dot[i] += pv[i];
+    }
     __syncthreads();
     float qn = 0.0f;
     for (uint32_t w = 0; w < kWinThreads / 32; ++w) qn += red[w];
-    // A = ||q||^2 + ||c||^2 - 2 q.c from K1's slices; keys of A + E, and A - E
+    // A = ||q||^2 + ||c||^2 - 2 q.c; keys of A + E, and A - E
     uint32_t key[VPT];
     float lov[VPT];
 #pragma unroll
@@ -402,16 +424,8 @@ __global__ void __launch_bounds__(kWinThreads) select_window_kernel(
         key[i] = 0xffffffffu;
         lov[i] = 0.0f;
         if (c < nlist) {
-            // all slices' loads issued together (compile-time bound), then summed
-            float pv[kTcMaxSlices];
-#pragma unroll
-            for (uint32_t z = 0; z < kTcMaxSlices; ++z)
-                pv[z] = z < nslices ? partial[(size_t(z) * nq + q) * nlist + c] : 0.0f;
-            float dot = 0.0f;
-#pragma unroll
-            for (uint32_t z = 0; z < kTcMaxSlices; ++z) dot += pv[z];
-            const float nrm = __fadd_rn(qn, cent_norm[c]);
-            const float a = __fsub_rn(nrm, __fmul_rn(2.0f, dot));
+            const float nrm = __fadd_rn(qn, cnv[i]);
+            const float a = __fsub_rn(nrm, __fmul_rn(2.0f, dot[i]));
             const float e = __fmul_rn(bound_c, nrm);
             key[i] = fkey(__fadd_rn(a, e));
             lov[i] = __fsub_rn(a, e);
@@ -446,22 +460,32 @@ __global__ void __launch_bounds__(kWinThreads) select_window_kernel(
     const uint32_t rs = d + 1;
     if (W <= kWinCap) {
         // exact rescoring (common.hpp:73-80 via annindex.hpp:279): rows staged
-        // in SMEM (stride d + 1: conflict-free), one thread folds one list
-        for (uint32_t b0 = 0; b0 < W; b0 += kStageRows) {
+        // in SMEM (stride d + 1: conflict-free) by cp.async, two batches of
+        // kStageRows in flight (batch b+1 loads while batch b is folded); one
+        // thread folds one list
+        auto stage_batch = [&](uint32_t b0, uint32_t buf) {
             const uint32_t nb = min(kStageRows, W - b0);
-            __syncthreads();
-            // LDGSTS: every element of the batch in flight at once (one memory
-            // round trip), no register staging
+            float* dst = rows + buf * kStageRows * rs;
             for (uint32_t idx = tid; idx < nb * d; idx += kWinThreads) {
                 const uint32_t r = idx / d, j = idx - r * d;
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(rows + r * rs + j)),
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst + r * rs + j)),
                              "l"(centroids + size_t(win[b0 + r]) * d + j)
                              : "memory");
             }
-            asm volatile("cp.async.wait_all;" ::: "memory");
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        };
+        if (W) stage_batch(0, 0);
+        for (uint32_t b0 = 0, buf = 0; b0 < W; b0 += kStageRows, buf ^= 1u) {
+            const uint32_t nb = min(kStageRows, W - b0);
+            if (b0 + kStageRows < W) {
+                stage_batch(b0 + kStageRows, buf ^ 1u);
+                asm volatile("cp.async.wait_group 1;" ::: "memory");
+            } else {
+                asm volatile("cp.async.wait_group 0;" ::: "memory");
+            }
             __syncthreads();
             if (tid < nb) {
-                const float* row = rows + tid * rs;
+                const float* row = rows + (buf * kStageRows + tid) * rs;
                 float acc = 0.0f;
 #pragma unroll 16
                 for (uint32_t j = 0; j < d; ++j) {
@@ -470,6 +494,7 @@ __global__ void __launch_bounds__(kWinThreads) select_window_kernel(
                 }
                 wd[b0 + tid] = acc;
             }
+            __syncthreads();  // batch buffer free for the prefetch two batches on
         }
     } else {
         W = exact_fallback<VPT>(upq, centroids, sq, nlist, d, nprobe, hist, misc, win, wd);
@@ -495,7 +520,7 @@ __global__ void __launch_bounds__(kWinThreads) select_window_kernel(
 }  // namespace
 
 size_t tc_window_smem(uint32_t d) {
-    return (256 + 8 + 2 * kWinCap) * 4 + ((d + 3) & ~3u) * 4 + size_t(kStageRows) * (d + 1) * 4 +
+    return (256 + 8 + 2 * kWinCap) * 4 + ((d + 3) & ~3u) * 4 + 2 * size_t(kStageRows) * (d + 1) * 4 +
            (kWinThreads / 32) * 4;
 }
 

@@ -231,14 +231,12 @@ template <>
 struct SkewCfg<32> {
     static constexpr int kWarps = 13;  // consumer warps; + 1 producer + 2 expander warps, 1 CTA per SM
     static constexpr int kDepth = 4;   // TMA ring slots per consumer warp
-    static constexpr int kGroup = 1;   // code tiles per ring slot
     static constexpr int kBufs = 2;    // SMEM images: item i+1's is built while item i is scanned
 };
 template <>
 struct SkewCfg<64> {
     static constexpr int kWarps = 8;
     static constexpr int kDepth = 2;
-    static constexpr int kGroup = 1;
     static constexpr int kBufs = 1;    // 128 KiB image: single-buffered
 };
 constexpr int kExpWarps = 2;
@@ -265,9 +263,9 @@ struct SkewSmem {
     static constexpr uint32_t kImg = image_floats<M>() * 4;  // R x 64 KiB
     static constexpr uint32_t kStage = 32768;                // 32 subquantizers of T[sq][256] fp32
     static constexpr uint32_t kTile = 32u * M;
-    static constexpr uint32_t kRing = uint32_t(D) * SkewCfg<M>::kGroup * kTile;  // per consumer warp
-    // img_full[NB], img_empty[NB], stg_full, stg_empty, ring[W*D]
-    static constexpr uint32_t nbars = 2 * NB + 2 + W * D;
+    static constexpr uint32_t kRing = uint32_t(D) * kTile;  // per consumer warp
+    // img_full[NB], img_empty[NB], stg_full, stg_empty
+    static constexpr uint32_t nbars = 2 * NB + 2;
     static constexpr uint32_t kTail = 8 * nbars + (NB + 1) * uint32_t(sizeof(ItemSlot));
     static constexpr uint32_t bytes = 232448;                // 227 KiB: the opt-in maximum
     // worst case: a pad just below one ring (nothing fits in it)
@@ -280,6 +278,15 @@ constexpr size_t skew_smem_bytes() {
     return SkewSmem<M>::bytes;
 }
 static_assert(SkewSmem<32>::worst <= 232448 && SkewSmem<64>::worst <= 232448, "K3 SMEM exceeds 227 KiB");
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 
 // LUT gather: 32-bit shared::cta address (uniform base folded by ptxas into
 // LDS [R + UR + imm]) plus a compile-time offset.
@@ -332,8 +339,6 @@ __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
 // (compile-time, so the gather is LDS [R + UR + imm]), keep the warp top-k and
 // publish it to the query's candidate pool.
 struct ScanCtx {
-    unsigned char* wring;
-    uint64_t* wbar;
     uint32_t ring_s, lane, bt, k;  // bt: column offset | image page (see SkewSmem)
     const uint8_t* skew_codes;
     const uint64_t* ids;
@@ -347,12 +352,10 @@ struct ScanCtx {
 template <int M>
 __device__ __forceinline__ void scan_range(const ScanCtx& cx, const ItemSlot& sl, uint32_t a, uint32_t e_end,
                                            uint32_t& consumed, const float* mk, const float* nk) {
-    constexpr int W = SkewCfg<M>::kWarps, D = SkewCfg<M>::kDepth, G = SkewCfg<M>::kGroup;
+    constexpr int W = SkewCfg<M>::kWarps, D = SkewCfg<M>::kDepth;
     constexpr int kChunks = M / 16;
     constexpr uint32_t kTileBytes = 32u * M;
     const uint32_t lane = cx.lane, bt = cx.bt, k = cx.k, ring_s = cx.ring_s;
-    unsigned char* wring = cx.wring;
-    uint64_t* wbar = cx.wbar;
     const uint64_t* __restrict__ ids = cx.ids;
     uint32_t* gthr = cx.gthr;
     const uint8_t* skew_codes = cx.skew_codes;
@@ -362,17 +365,22 @@ __device__ __forceinline__ void scan_range(const ScanCtx& cx, const ItemSlot& sl
     uint64_t* pool_id = cx.pool_id;
     const uint32_t q = sl.q;
     const unsigned char* tiles = skew_codes + sl.tile_byte_off;
-    // this warp streams tiles a..e_end inclusive: tile e_end holds the
-    // tails of the range's last entries
-    // the ring holds D slots of G tiles; slot i of this range covers tiles
-    // a + G*i .. a + G*i + G - 1 (clipped to e_end)
-    if (lane == 0) {
-        for (uint32_t t = 0; t < uint32_t(D) && a + G * t <= e_end; ++t) {
+    // this warp streams tiles a..e_end inclusive (tile e_end holds the tails
+    // of the range's last entries) through a D-deep ring. Each lane copies
+    // exactly the 16-byte chunks it will read itself (cp.async, one commit
+    // group per tile), so a lane only ever waits on its own copies: no
+    // barrier, no cross-lane synchronisation.
+    const unsigned char* src_lane = tiles + lane * 16;
+    const uint32_t dst_lane = ring_s + lane * 16;
+#pragma unroll
+    for (uint32_t t = 0; t < uint32_t(D); ++t) {
+        if (a + t <= e_end) {
             const uint32_t slot = (consumed + t) % D;
-            const uint32_t bytes = min(uint32_t(G), e_end - (a + G * t) + 1) * kTileBytes;
-            mbar_expect_tx(wbar + slot, bytes);
-            bulk_g2s(wring + slot * G * kTileBytes, tiles + size_t(a + G * t) * kTileBytes, bytes, wbar + slot);
+#pragma unroll
+            for (int c = 0; c < kChunks; ++c)
+                cp_async16(dst_lane + slot * kTileBytes + c * 512, src_lane + size_t(a + t) * kTileBytes + c * 512);
         }
+        cp_async_commit();
     }
     uint32_t tk_key = 0xffffffffu;  // warp top-k: lane i holds the i-th (distance bits, entry slot)
     uint32_t tk_pos = 0xffffffffu;
@@ -381,34 +389,26 @@ __device__ __forceinline__ void scan_range(const ScanCtx& cx, const ItemSlot& sl
     // per range: an in-loop refresh would put a global load on every tile
     uint32_t g_thr = ld_relaxed(gthr + q);
     float cur = 0.0f, prev = 0.0f;
-    for (uint32_t j0 = a; j0 <= e_end; j0 += G, ++consumed) {
+    for (uint32_t j = a; j <= e_end; ++j, ++consumed) {
         const uint32_t slot = consumed % D;
-        mbar_wait(wbar + slot, (consumed / D) & 1u);
-#pragma unroll
-        for (uint32_t g = 0; g < uint32_t(G); ++g) {
-        const uint32_t j = j0 + g;
-        if (G > 1 && j > e_end) break;
+        cp_async_wait<D - 1>();  // this lane's chunks of tile j have landed
         uint32_t wd[M / 4];
 #pragma unroll
         for (int c = 0; c < kChunks; ++c) {
-            const uint4 v = lds_u4(ring_s + (slot * G + g) * kTileBytes + c * 512 + lane * 16);
+            const uint4 v = lds_u4(dst_lane + slot * kTileBytes + c * 512);
             wd[4 * c] = v.x;
             wd[4 * c + 1] = v.y;
             wd[4 * c + 2] = v.z;
             wd[4 * c + 3] = v.w;
         }
         skew_round<M>(wd, bt, cur, prev, mk, nk, std::make_integer_sequence<int, M>{});
-        if (g + 1 == uint32_t(G) || j == e_end) {
-            // the codes of this slot are consumed (every lane's LDS.128 result
-            // was used by the steps above): refill it with the tiles D slots on
-            __syncwarp();
-            const uint32_t jr = j0 + uint32_t(D) * G;
-            if (lane == 0 && jr <= e_end) {
-                const uint32_t bytes = min(uint32_t(G), e_end - jr + 1) * kTileBytes;
-                mbar_expect_tx(wbar + slot, bytes);
-                bulk_g2s(wring + slot * G * kTileBytes, tiles + size_t(jr) * kTileBytes, bytes, wbar + slot);
-            }
+        // the fold consumed every byte of the slot: refill it with tile j + D
+        if (j + D <= e_end) {
+#pragma unroll
+            for (int c = 0; c < kChunks; ++c)
+                cp_async16(dst_lane + slot * kTileBytes + c * 512, src_lane + size_t(j + D) * kTileBytes + c * 512);
         }
+        cp_async_commit();
         // entry 32(j-1)+lane is complete in `prev`
         const uint32_t e = (j - 1) * kTileEntries + lane;
         const bool valid = j > a && e < sl.len;
@@ -454,8 +454,8 @@ __device__ __forceinline__ void scan_range(const ScanCtx& cx, const ItemSlot& sl
                 g_thr = thr_key;
             }
         }
-        }  // g
     }
+    cp_async_wait<0>();  // no copies left in flight into the ring
     // publish this warp's list into the query's candidate pool, minus entries
     // above the query's shared threshold: some warp holds k candidates at or
     // below it, so those entries cannot make the final top-k
@@ -479,10 +479,9 @@ __device__ __forceinline__ void scan_range(const ScanCtx& cx, const ItemSlot& sl
 //    tile_end} (largest first), resolves the list's metadata and TMA-copies
 //    the pair's compact table T[m][256] into a staging buffer;
 //  * kExpWarps expander warps: transpose the staged table into the
-//    conflict-free image (diagonal walk: lane L moves T[(s0+L) mod m][c0+L],
-//    so both the LDS and the STS of every step hit 32 distinct banks) in one
-//    of kBufs image buffers -- item i+1's image is built while item i is
-//    scanned;
+//    conflict-free image (4x4 register transposes walked diagonally, so every
+//    LDS.128 / STS.128 is conflict-free) in one of kBufs image buffers --
+//    item i+1's image is built while item i is scanned;
 //  * kWarps consumer warps: each scans a contiguous tile range of the item,
 //    its code tiles streamed through a per-warp ring of kDepth TMA bulk
 //    copies (one elected lane, one mbarrier per slot), keeps an exact top-k
@@ -522,7 +521,6 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
     uint64_t* img_empty = bars + NB;
     uint64_t* stg_full = bars + 2 * NB;
     uint64_t* stg_empty = bars + 2 * NB + 1;
-    uint64_t* rbar = bars + 2 * NB + 2;
     ItemSlot* slots = reinterpret_cast<ItemSlot*>(smem + tail_off + 8 * L::nbars);  // [NB] image slots
     ItemSlot* stg_slot = slots + NB;                                                 // staging slot
 
@@ -534,7 +532,6 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
         }
         mbar_init(stg_full, 1);
         mbar_init(stg_empty, kExpWarps);
-        for (int i = 0; i < W * D; ++i) mbar_init(rbar + i, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -600,23 +597,35 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
             float* img = reinterpret_cast<float*>(smem + img_off + b * kImgBytes);
             for (uint32_t h = 0; h < kHalves; ++h, ++round) {
                 if (h > 0) mbar_wait(stg_full, round & 1u);
-                // diagonal walk: lane L moves T[32h + (s0+L) mod 32][c0+L]; the LDS
-                // (bank = code) and both STS (bank = column mod 32) are conflict-free
+                // 4x4 register transposes: lane L owns codes cb + 4L .. +3 and
+                // walks the 8 groups of 4 subquantizers diagonally (group
+                // (g + L) mod 8), so every LDS.128 (4 codes of one staged row)
+                // and STS.128 (4 columns of one image row) is conflict-free
+#pragma unroll 1
+                for (uint32_t cb = ew * 128; cb < 256; cb += 128 * kExpWarps) {
+                    const uint32_t c4 = cb + 4 * lane;
 #pragma unroll 2
-                for (uint32_t c0 = ew * 32; c0 < 256; c0 += 32 * kExpWarps) {
-                    const uint32_t code = c0 + lane;
-                    float* row = img + code * 64;
-#pragma unroll 8
-                    for (uint32_t s0 = 0; s0 < 32; ++s0) {
-                        const uint32_t sl_ = (s0 + lane) & 31u;
-                        const float v = stage[sl_ * 256 + code];
-                        const uint32_t sq = 32 * h + sl_;
-                        if (M == 32) {  // image 0, column c = T[c mod 32]: columns sq and sq + 32
-                            row[sq] = v;
-                            row[sq + 32] = v;
-                        } else {        // image 0 at (sq + 32) mod 64, image 1 at sq
-                            row[(sq + 32) & (M - 1)] = v;
-                            row[16384 + sq] = v;
+                    for (uint32_t g = 0; g < 8; ++g) {
+                        const uint32_t sq0 = 4 * ((g + lane) & 7u);  // local subquantizer group
+                        float4 v[4];
+#pragma unroll
+                        for (int r = 0; r < 4; ++r)
+                            v[r] = *reinterpret_cast<const float4*>(stage + (sq0 + r) * 256 + c4);
+                        const float4 col[4] = {make_float4(v[0].x, v[1].x, v[2].x, v[3].x),
+                                               make_float4(v[0].y, v[1].y, v[2].y, v[3].y),
+                                               make_float4(v[0].z, v[1].z, v[2].z, v[3].z),
+                                               make_float4(v[0].w, v[1].w, v[2].w, v[3].w)};
+                        const uint32_t sq = 32 * h + sq0;
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            float* row = img + (c4 + i) * 64;
+                            if (M == 32) {  // image 0, column c = T[c mod 32]: columns sq and sq + 32
+                                *reinterpret_cast<float4*>(row + sq) = col[i];
+                                *reinterpret_cast<float4*>(row + sq + 32) = col[i];
+                            } else {        // image 0 at (sq + 32) mod 64, image 1 at sq
+                                *reinterpret_cast<float4*>(row + ((sq + 32) & (M - 1))) = col[i];
+                                *reinterpret_cast<float4*>(row + 16384 + sq) = col[i];
+                            }
                         }
                     }
                 }
@@ -635,7 +644,6 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
     // lane's column offset (bytes) in byte 0, the image's 64 KiB page in bytes 2-3
     const uint32_t bt0 = (32u - lane) * 4u | ((base + img_off) & 0xffff0000u);
     unsigned char* wring = smem + (warp < rings_in_pad ? warp * L::kRing : after_off + (warp - rings_in_pad) * L::kRing);
-    uint64_t* wbar = rbar + warp * D;
     const uint32_t ring_s = smem_u32(wring);
     uint32_t consumed = 0;  // tiles this warp has taken from its ring (slot/parity bookkeeping)
     // step masks: {1, 0} where step s >= lane (the starting entry), {0, 1}
@@ -658,7 +666,7 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
         const uint32_t a = sl.tb + warp * per;
         const uint32_t e_end = min(sl.te, a + per);
         if (warp < nw && a < e_end) {
-            const ScanCtx cx{wring, wbar, ring_s, lane, bt0 + b * (kImgBytes & 0xffff0000u), k, skew_codes, ids, gthr,
+            const ScanCtx cx{ring_s, lane, bt0 + b * (kImgBytes & 0xffff0000u), k, skew_codes, ids, gthr,
                              q_item_off, pool_cnt, pool_key, pool_id};
             scan_range<M>(cx, sl, a, e_end, consumed, mk, nk);
         }
