@@ -25,6 +25,7 @@
 //    memory (atomicMin on the k-th distance) prunes candidates; ids are
 //    loaded only for candidates that pass.
 #include <cstdint>
+#include <cstdlib>
 #include <utility>
 
 #include "internal.h"
@@ -62,6 +63,26 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
         "}\n" ::"r"(smem_u32(bar)),
         "r"(phase), "r"(0x989680u)
         : "memory");
+}
+
+// Support roles (producer, expanders) poll with a fixed back-off instead of
+// a suspend-hinted try_wait: the hinted wait is woken by every barrier and
+// async-copy event in the CTA, and those wake-ups cost consumer issue slots.
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t phase) {
+    for (;;) {
+        uint32_t done;
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, p;\n"
+            "}\n"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(phase)
+            : "memory");
+        if (done) return;
+        __nanosleep(200);
+    }
 }
 
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -235,7 +256,7 @@ struct SkewCfg<32> {
 };
 template <>
 struct SkewCfg<64> {
-    static constexpr int kWarps = 8;
+    static constexpr int kWarps = 12;
     static constexpr int kDepth = 2;
     static constexpr int kBufs = 1;    // 128 KiB image: single-buffered
 };
@@ -349,9 +370,44 @@ struct ScanCtx {
     uint64_t* pool_id;
 };
 
+// The next item a warp will scan (buffer b^1), known once its image is
+// published; lets the tail of one range prefetch the head of the next.
+struct NextRange {
+    const ItemSlot* slot;  // slots[b^1]
+    uint64_t* full;        // img_full[b^1]
+    uint32_t phase;        // parity of that item's img_full phase
+    uint32_t warp;
+    bool enabled;          // double-buffered images only
+};
+
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t phase) {
+    uint32_t done;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+    return done != 0;
+}
+
+// This warp's tile range [a, e_end) of an item (empty when a >= e_end).
+template <int W>
+__device__ __forceinline__ void warp_range(const ItemSlot& sl, uint32_t warp, uint32_t& a, uint32_t& e_end) {
+    const uint32_t ntile = sl.te - sl.tb;
+    const uint32_t nw = min(uint32_t(W), (ntile + kMinWarpTiles - 1) / kMinWarpTiles);
+    const uint32_t per = (ntile + nw - 1) / nw;
+    a = sl.tb + warp * per;
+    e_end = warp < nw ? min(sl.te, a + per) : a;
+}
+
 template <int M>
-__device__ __forceinline__ void scan_range(const ScanCtx& cx, const ItemSlot& sl, uint32_t a, uint32_t e_end,
-                                           uint32_t& consumed, const float* mk, const float* nk) {
+__device__ __forceinline__ bool scan_range(const ScanCtx& cx, const ItemSlot& sl, uint32_t a, uint32_t e_end,
+                                           uint32_t& consumed, const float* mk, const float* nk,
+                                           bool prefetched, const NextRange& nx) {
     constexpr int W = SkewCfg<M>::kWarps, D = SkewCfg<M>::kDepth;
     constexpr int kChunks = M / 16;
     constexpr uint32_t kTileBytes = 32u * M;
@@ -370,24 +426,36 @@ __device__ __forceinline__ void scan_range(const ScanCtx& cx, const ItemSlot& sl
     // exactly the 16-byte chunks it will read itself (cp.async, one commit
     // group per tile), so a lane only ever waits on its own copies: no
     // barrier, no cross-lane synchronisation.
+    // the query's shared threshold (other warps' k-th distances) is read once
+    // per range (an in-loop refresh would put a global load on every tile),
+    // issued before the ring prologue so its latency overlaps the copies
+    uint32_t g_thr = ld_relaxed(gthr + q);
     const unsigned char* src_lane = tiles + lane * 16;
     const uint32_t dst_lane = ring_s + lane * 16;
+    if (!prefetched) {
 #pragma unroll
-    for (uint32_t t = 0; t < uint32_t(D); ++t) {
-        if (a + t <= e_end) {
-            const uint32_t slot = (consumed + t) % D;
+        for (uint32_t t = 0; t < uint32_t(D); ++t) {
+            if (a + t <= e_end) {
+                const uint32_t slot = (consumed + t) % D;
 #pragma unroll
-            for (int c = 0; c < kChunks; ++c)
-                cp_async16(dst_lane + slot * kTileBytes + c * 512, src_lane + size_t(a + t) * kTileBytes + c * 512);
+                for (int c = 0; c < kChunks; ++c)
+                    cp_async16(dst_lane + slot * kTileBytes + c * 512, src_lane + size_t(a + t) * kTileBytes + c * 512);
+            }
+            cp_async_commit();
         }
-        cp_async_commit();
     }
+    // cross-range prefetch: once the last D tiles of this range are in
+    // flight, the freed ring slots take the first tiles of this warp's range
+    // in the next item (if that item is already published), so the next range
+    // starts without a memory round trip. Only for ranges of >= D tiles, so
+    // the prefetch covers exactly the next range's first D ring slots.
+    bool nx_tried = !nx.enabled || e_end - a + 1 < uint32_t(D);
+    bool nx_ok = false;
+    uint32_t nx_a = 0, nx_e = 0;
+    const unsigned char* nx_src = nullptr;
     uint32_t tk_key = 0xffffffffu;  // warp top-k: lane i holds the i-th (distance bits, entry slot)
     uint32_t tk_pos = 0xffffffffu;
     uint32_t thr_key = 0xffffffffu;
-    // the query's shared threshold (other warps' k-th distances) is read once
-    // per range: an in-loop refresh would put a global load on every tile
-    uint32_t g_thr = ld_relaxed(gthr + q);
     float cur = 0.0f, prev = 0.0f;
     for (uint32_t j = a; j <= e_end; ++j, ++consumed) {
         const uint32_t slot = consumed % D;
@@ -403,10 +471,29 @@ __device__ __forceinline__ void scan_range(const ScanCtx& cx, const ItemSlot& sl
         }
         skew_round<M>(wd, bt, cur, prev, mk, nk, std::make_integer_sequence<int, M>{});
         // the fold consumed every byte of the slot: refill it with tile j + D
+        // of this range, or with the next range's head
         if (j + D <= e_end) {
 #pragma unroll
             for (int c = 0; c < kChunks; ++c)
                 cp_async16(dst_lane + slot * kTileBytes + c * 512, src_lane + size_t(j + D) * kTileBytes + c * 512);
+        } else {
+            if (!nx_tried) {
+                nx_tried = true;
+                if (mbar_test(nx.full, nx.phase)) {
+                    const ItemSlot ns = *nx.slot;
+                    if (ns.pair != kEndItem) {
+                        warp_range<W>(ns, nx.warp, nx_a, nx_e);
+                        nx_ok = nx_a < nx_e;
+                        nx_src = skew_codes + ns.tile_byte_off + lane * 16;
+                    }
+                }
+            }
+            const uint32_t t = j + D - e_end - 1;  // next range's tile index this slot will hold
+            if (nx_ok && nx_a + t <= nx_e) {
+#pragma unroll
+                for (int c = 0; c < kChunks; ++c)
+                    cp_async16(dst_lane + slot * kTileBytes + c * 512, nx_src + size_t(nx_a + t) * kTileBytes + c * 512);
+            }
         }
         cp_async_commit();
         // entry 32(j-1)+lane is complete in `prev`
@@ -455,11 +542,12 @@ __device__ __forceinline__ void scan_range(const ScanCtx& cx, const ItemSlot& sl
             }
         }
     }
-    cp_async_wait<0>();  // no copies left in flight into the ring
     // publish this warp's list into the query's candidate pool, minus entries
     // above the query's shared threshold: some warp holds k candidates at or
     // below it, so those entries cannot make the final top-k
-    const uint32_t g_pub = min(g_thr, ld_relaxed(gthr + q));
+    // g_thr = min(the shared threshold at range start, this warp's own k-th
+    // distance): never below the final shared threshold, so a valid filter
+    const uint32_t g_pub = g_thr;
     const unsigned have = __ballot_sync(0xffffffffu, lane < k && tk_key != 0xffffffffu && tk_key <= g_pub);
     const uint32_t cnt = __popc(have);
     if (cnt) {
@@ -472,6 +560,7 @@ __device__ __forceinline__ void scan_range(const ScanCtx& cx, const ItemSlot& sl
             pool_id[poff + base + lane] = ids[tk_pos];
         }
     }
+    return nx_ok;
 }
 
 // Persistent, one CTA per SM, warp-specialised:
@@ -560,14 +649,14 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
                 }
                 if (sl.pair == kEndItem) {
                     pdl_trigger();  // no more work items: let the pool selection launch
-                    mbar_wait(stg_empty, (round & 1u) ^ 1u);
+                    mbar_wait_backoff(stg_empty, (round & 1u) ^ 1u);
                     *stg_slot = sl;
                     mbar_arrive(stg_full);
                     break;
                 }
                 const unsigned char* src = reinterpret_cast<const unsigned char*>(luts) + size_t(sl.pair) * M * 1024;
                 for (uint32_t h = 0; h < kHalves; ++h, ++round) {
-                    mbar_wait(stg_empty, (round & 1u) ^ 1u);
+                    mbar_wait_backoff(stg_empty, (round & 1u) ^ 1u);
                     if (h == 0) *stg_slot = sl;
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     mbar_expect_tx(stg_full, kStageBytes);
@@ -583,9 +672,9 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
         uint32_t round = 0;
         for (uint32_t i = 0;; ++i) {
             const uint32_t b = NB == 1 ? 0u : i % NB;
-            mbar_wait(stg_full, round & 1u);
+            mbar_wait_backoff(stg_full, round & 1u);
             const ItemSlot sl = *stg_slot;
-            mbar_wait(img_empty + b, ((NB == 1 ? i : i / NB) & 1u) ^ 1u);
+            mbar_wait_backoff(img_empty + b, ((NB == 1 ? i : i / NB) & 1u) ^ 1u);
             if (sl.pair == kEndItem) {
                 __syncwarp();
                 if (lane == 0) {
@@ -596,7 +685,7 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
             }
             float* img = reinterpret_cast<float*>(smem + img_off + b * kImgBytes);
             for (uint32_t h = 0; h < kHalves; ++h, ++round) {
-                if (h > 0) mbar_wait(stg_full, round & 1u);
+                if (h > 0) mbar_wait_backoff(stg_full, round & 1u);
                 // 4x4 register transposes: lane L owns codes cb + 4L .. +3 and
                 // walks the 8 groups of 4 subquantizers diagonally (group
                 // (g + L) mod 8), so every LDS.128 (4 codes of one staged row)
@@ -655,20 +744,22 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
         nk[s] = (uint32_t(s) >= lane) ? 0.0f : 1.0f;
     }
 
+    bool pref = false;  // the first ring slots of this item's range are already in flight
     for (uint32_t i = 0;; ++i) {
         const uint32_t b = NB == 1 ? 0u : i % NB;
         mbar_wait(img_full + b, (NB == 1 ? i : i / NB) & 1u);
         const ItemSlot sl = slots[b];
         if (sl.pair == kEndItem) break;
-        const uint32_t ntile = sl.te - sl.tb;
-        const uint32_t nw = min(uint32_t(W), (ntile + kMinWarpTiles - 1) / kMinWarpTiles);
-        const uint32_t per = (ntile + nw - 1) / nw;
-        const uint32_t a = sl.tb + warp * per;
-        const uint32_t e_end = min(sl.te, a + per);
-        if (warp < nw && a < e_end) {
+        uint32_t a, e_end;
+        warp_range<W>(sl, warp, a, e_end);
+        if (a < e_end) {
             const ScanCtx cx{ring_s, lane, bt0 + b * (kImgBytes & 0xffff0000u), k, skew_codes, ids, gthr,
                              q_item_off, pool_cnt, pool_key, pool_id};
-            scan_range<M>(cx, sl, a, e_end, consumed, mk, nk);
+            const uint32_t bn = NB == 1 ? 0u : (i + 1) % NB;
+            const NextRange nx{slots + bn, img_full + bn, (NB == 1 ? i + 1 : (i + 1) / NB) & 1u, warp, NB > 1};
+            pref = scan_range<M>(cx, sl, a, e_end, consumed, mk, nk, pref, nx);
+        } else {
+            pref = false;
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(img_empty + b);
@@ -770,8 +861,14 @@ __global__ void __launch_bounds__(1024) plan_skew_kernel(const uint32_t* __restr
 }  // namespace
 
 uint32_t skew_item_tiles(uint64_t est_tiles, uint32_t grid) {
-    // enough items for ~3 per CTA, within [kMinItemTiles, kMaxItemTiles]
-    uint64_t want = est_tiles / (uint64_t(grid) * 3 + 1);
+    // enough items for ~per_cta per CTA, within [kMinItemTiles, kMaxItemTiles]
+    // (PRAG_GPU_ITEMS_PER_CTA overrides the default of 3; tuning knob)
+    static const uint64_t per_cta = [] {
+        const char* e = getenv("PRAG_GPU_ITEMS_PER_CTA");
+        const long v = e ? atol(e) : 0;
+        return uint64_t(v > 0 ? v : 3);
+    }();
+    uint64_t want = est_tiles / (uint64_t(grid) * per_cta + 1);
     uint32_t it = kMinItemTiles;
     while (it < kMaxItemTiles && uint64_t(it) * 2 <= want) it *= 2;
     return it;
