@@ -395,9 +395,8 @@ int search_pass_skew(prag_gpu_index* ix, Workspace* w, const float* dq, uint32_t
     if (prof) cudaEventRecord(w->ev[0], s);
     PG_TRY(run_coarse(ix, dq, nq, nprobe, coarse, probe, probe_dist, pkey, ptie, s, prof ? w : nullptr));
     if (prof) cudaEventRecord(w->ev[2], s);
-    PG_TRY(launch_plan_skew(d, probe, nq, nprobe, IT, o_scanned, items, ctr, ctr + 1, q_item_off, gthr, pool_cnt,
-                            item_cap, s));
-    PG_TRY(launch_lut_images(d, dq, probe, nq, nprobe, images, s));
+    PG_TRY(launch_lut_images(d, dq, probe, nq, nprobe, images, IT, o_scanned, items, ctr, ctr + 1, q_item_off, gthr,
+                             pool_cnt, item_cap, s));
     if (prof) cudaEventRecord(w->ev[3], s);
     PG_TRY(launch_scan_skew(d, items, ctr, ctr + 1, probe, images, nprobe, k, gthr, q_item_off, pool_cnt, pool_key,
                             pool_id, grid, s));

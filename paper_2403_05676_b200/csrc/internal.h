@@ -188,11 +188,12 @@ int launch_merge(const uint64_t* ids, const float* dist, const uint32_t* count, 
                  uint64_t* gtie, uint32_t pw, cudaStream_t s);
 uint32_t scan_chunk();
 // fast path (scan_skew.cu)
-int launch_plan_skew(const DeviceIndex& ix, const uint32_t* probe, uint32_t nq, uint32_t nprobe, uint32_t it_tiles,
-                     uint64_t* scanned, uint4* items, uint32_t* num_items, uint32_t* cursor, uint32_t* q_item_off,
-                     uint32_t* gthr, uint32_t* pool_cnt, uint64_t item_cap, cudaStream_t s);
+// K2 + planner: LUTs of every (query, probed list) pair, and (one extra CTA)
+// the scan's work items, scanned_vectors and per-query threshold/pool reset
 int launch_lut_images(const DeviceIndex& ix, const float* queries, const uint32_t* probe, uint32_t nq,
-                      uint32_t nprobe, float* images, cudaStream_t s);
+                      uint32_t nprobe, float* luts, uint32_t it_tiles, uint64_t* scanned, uint4* items,
+                      uint32_t* num_items, uint32_t* cursor, uint32_t* q_item_off, uint32_t* gthr,
+                      uint32_t* pool_cnt, uint64_t item_cap, cudaStream_t s);
 int launch_scan_skew(const DeviceIndex& ix, const uint4* items, const uint32_t* num_items, uint32_t* cursor,
                      const uint32_t* probe, const float* images, uint32_t nprobe, uint32_t k, uint32_t* gthr,
                      const uint32_t* q_item_off, uint32_t* pool_cnt, uint32_t* pool_key, uint64_t* pool_id,

@@ -143,7 +143,116 @@ constexpr uint32_t image_floats() {
     return uint32_t(M / 32) * 256u * 64u;
 }
 
-// Grid: (ceil(npairs / kLutPairs), m / 8). CTA: 256 threads = 256 codes; it
+// Work items for the fast path: per (q, p) pair, ceil(len/32) tiles cut into
+// items of <= it_tiles tiles, emitted largest-first (log2 size buckets) so
+// the big lists set each query's threshold early and the small ones fill the
+// tail. q_item_off[q] = prefix of per-query item counts (candidate-pool
+// offsets). Also resets the per-query threshold and pool counters, and
+// writes scanned_vectors (annindex.hpp:305: the sum of probed list sizes).
+struct PlanArgs {
+    uint32_t it_tiles;
+    uint64_t* scanned;
+    uint4* items;
+    uint32_t* num_items;
+    uint32_t* cursor;
+    uint32_t* q_item_off;
+    uint32_t* gthr;
+    uint32_t* pool_cnt;
+    uint64_t item_cap;
+};
+
+// Runs on one CTA (any block size that is a multiple of 32, <= 1024): the
+// extra CTA of the LUT kernel's grid, so planning overlaps the LUT work.
+__device__ __noinline__ void plan_items(const uint32_t* __restrict__ probe, const uint32_t* __restrict__ list_len,
+                                        uint32_t nq, uint32_t nprobe, const PlanArgs pa) {
+    const uint32_t it_tiles = pa.it_tiles;
+    uint64_t* __restrict__ scanned = pa.scanned;
+    uint4* __restrict__ items = pa.items;
+    uint32_t* __restrict__ num_items = pa.num_items;
+    uint32_t* __restrict__ cursor = pa.cursor;
+    uint32_t* __restrict__ q_item_off = pa.q_item_off;
+    uint32_t* __restrict__ gthr = pa.gthr;
+    uint32_t* __restrict__ pool_cnt = pa.pool_cnt;
+    const uint64_t item_cap = pa.item_cap;
+    __shared__ uint32_t tmp[33];
+    __shared__ uint32_t bucket_cnt[32], bucket_pos[32];
+    const uint32_t P = nq * nprobe;
+    if (threadIdx.x < 32) bucket_cnt[threadIdx.x] = 0;
+    for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x) scanned[q] = 0;
+    __syncthreads();
+    // pass 1: per-query item counts (prefix) and bucket histogram
+    uint32_t carry = 0;
+    for (uint32_t base = 0; base < P; base += blockDim.x) {
+        const uint32_t i = base + threadIdx.x;
+        const bool valid = i < P;
+        const uint32_t len = valid ? list_len[probe[i]] : 0;
+        if (len) atomicAdd(reinterpret_cast<unsigned long long*>(scanned + i / nprobe), (unsigned long long)len);
+        const uint32_t tiles = (len + kTileEntries - 1) / kTileEntries;
+        const uint32_t nit = (tiles + it_tiles - 1) / it_tiles;
+        for (uint32_t j = 0; j < nit; ++j) {
+            const uint32_t t = min(tiles, (j + 1) * it_tiles) - j * it_tiles;
+            atomicAdd(&bucket_cnt[31 - __clz(t)], 1u);
+        }
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+        uint32_t incl = nit;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (lane == 31) tmp[w] = incl;
+        __syncthreads();
+        if (w == 0) {
+            const int nw = blockDim.x >> 5;
+            uint32_t x = lane < nw ? tmp[lane] : 0u, xi = x;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                uint32_t t = __shfl_up_sync(0xffffffffu, xi, o);
+                if (lane >= o) xi += t;
+            }
+            if (lane < nw) tmp[lane] = xi - x;
+            if (lane == nw - 1) tmp[32] = xi;
+        }
+        __syncthreads();
+        const uint32_t excl = carry + tmp[w] + incl - nit;
+        if (valid && i % nprobe == 0) q_item_off[i / nprobe] = excl;
+        carry += tmp[32];
+        __syncthreads();
+    }
+    // bucket start positions, largest bucket first
+    if (threadIdx.x == 0) {
+        uint32_t pos = 0;
+        for (int bkt = 31; bkt >= 0; --bkt) {
+            bucket_pos[bkt] = pos;
+            pos += bucket_cnt[bkt];
+        }
+    }
+    __syncthreads();
+    // pass 2: scatter items
+    for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
+        const uint32_t len = list_len[probe[i]];
+        const uint32_t tiles = (len + kTileEntries - 1) / kTileEntries;
+        const uint32_t nit = (tiles + it_tiles - 1) / it_tiles;
+        for (uint32_t j = 0; j < nit; ++j) {
+            const uint32_t te = min(tiles, (j + 1) * it_tiles);
+            const uint32_t slot = atomicAdd(&bucket_pos[31 - __clz(te - j * it_tiles)], 1u);
+            if (slot < item_cap) items[slot] = make_uint4(i, j * it_tiles, te, 0u);
+        }
+    }
+    if (threadIdx.x == 0) {
+        *num_items = carry;
+        *cursor = 0;
+        q_item_off[nq] = carry;
+    }
+    for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x) {
+        gthr[q] = 0xffffffffu;
+        pool_cnt[q] = 0;
+    }
+}
+
+
+// Grid: (ceil(npairs / kLutPairs) + 1, m / SQB); the last column of CTAs is
+// the work-item planner (plan_items), which overlaps the table computation. CTA: 256 threads = 256 codes; it
 // computes subquantizers [8*blockIdx.y, +8) of T[sq][code] =
 // squared_l2(r_sq, w[sq][code], sub_dim) (annindex.hpp:292-297, residual
 // r = q - c_list, annindex.hpp:287-289) for kLutPairs pairs and writes them
@@ -158,8 +267,15 @@ __global__ void __launch_bounds__(256, 2) lut_image_kernel(const float* __restri
                                                            const uint32_t* __restrict__ probe,
                                                            const uint32_t* __restrict__ list_len, uint32_t nq,
                                                            uint32_t nprobe, uint32_t d, uint32_t sub,
-                                                           float* __restrict__ luts) {
+                                                           float* __restrict__ luts, const PlanArgs pa) {
     constexpr int P = kLutPairs;  // 8
+    if (blockIdx.x == gridDim.x - 1) {  // the planning CTA
+        if (blockIdx.y == 0) {
+            pdl_wait();  // probe[] comes from the previous kernel
+            plan_items(probe, list_len, nq, nprobe, pa);
+        }
+        return;
+    }
     constexpr int JMAX = SUBC ? SUBC : 16;
     if (SUBC) sub = SUBC;
     __shared__ __align__(16) float resid[8 * 16 * P];  // [sq_local][j][pair]
@@ -287,7 +403,7 @@ struct SkewSmem {
     static constexpr uint32_t kRing = uint32_t(D) * kTile;  // per consumer warp
     // img_full[NB], img_empty[NB], stg_full, stg_empty
     static constexpr uint32_t nbars = 2 * NB + 2;
-    static constexpr uint32_t kTail = 8 * nbars + (NB + 1) * uint32_t(sizeof(ItemSlot));
+    static constexpr uint32_t kTail = 8 * nbars + (NB + 1) * uint32_t(sizeof(ItemSlot)) + 4 * NB;  // + cta_thr[NB]
     static constexpr uint32_t bytes = 232448;                // 227 KiB: the opt-in maximum
     // worst case: a pad just below one ring (nothing fits in it)
     static constexpr uint32_t worst = (kRing - 16) + NB * kImg + kStage + W * kRing + kTail;
@@ -360,6 +476,7 @@ __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
 // (compile-time, so the gather is LDS [R + UR + imm]), keep the warp top-k and
 // publish it to the query's candidate pool.
 struct ScanCtx {
+    uint32_t* cta_thr;  // this item's CTA-wide threshold (SMEM)
     uint32_t ring_s, lane, bt, k;  // bt: column offset | image page (see SkewSmem)
     const uint8_t* skew_codes;
     const uint64_t* ids;
@@ -496,6 +613,7 @@ __device__ __forceinline__ bool scan_range(const ScanCtx& cx, const ItemSlot& sl
             }
         }
         cp_async_commit();
+        g_thr = min(g_thr, *reinterpret_cast<volatile uint32_t*>(cx.cta_thr));  // other warps of this item
         // entry 32(j-1)+lane is complete in `prev`
         const uint32_t e = (j - 1) * kTileEntries + lane;
         const bool valid = j > a && e < sl.len;
@@ -537,7 +655,10 @@ __device__ __forceinline__ bool scan_range(const ScanCtx& cx, const ItemSlot& sl
                 }
             }
             if (thr_key < g_thr) {
-                if (lane == 0) atomicMin(gthr + q, thr_key);
+                if (lane == 0) {
+                    atomicMin(gthr + q, thr_key);
+                    atomicMin(cx.cta_thr, thr_key);
+                }
                 g_thr = thr_key;
             }
         }
@@ -545,9 +666,9 @@ __device__ __forceinline__ bool scan_range(const ScanCtx& cx, const ItemSlot& sl
     // publish this warp's list into the query's candidate pool, minus entries
     // above the query's shared threshold: some warp holds k candidates at or
     // below it, so those entries cannot make the final top-k
-    // g_thr = min(the shared threshold at range start, this warp's own k-th
-    // distance): never below the final shared threshold, so a valid filter
-    const uint32_t g_pub = g_thr;
+    // the warp's view (shared threshold at range start, its own and this CTA's
+    // k-th distances) is never below the final shared threshold: a valid filter
+    const uint32_t g_pub = min(g_thr, *reinterpret_cast<volatile uint32_t*>(cx.cta_thr));
     const unsigned have = __ballot_sync(0xffffffffu, lane < k && tk_key != 0xffffffffu && tk_key <= g_pub);
     const uint32_t cnt = __popc(have);
     if (cnt) {
@@ -591,7 +712,7 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
                      uint32_t* __restrict__ pool_cnt, uint32_t* __restrict__ pool_key,
                      uint64_t* __restrict__ pool_id) {
     using L = SkewSmem<M>;
-    constexpr int W = L::W, D = L::D, NB = L::NB;
+    constexpr int W = L::W, NB = L::NB;
     constexpr uint32_t kImgBytes = L::kImg;
     constexpr uint32_t kStageBytes = L::kStage;
     constexpr uint32_t kHalves = M / 32;  // staging rounds per item (32 subquantizers each)
@@ -612,6 +733,7 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
     uint64_t* stg_empty = bars + 2 * NB + 1;
     ItemSlot* slots = reinterpret_cast<ItemSlot*>(smem + tail_off + 8 * L::nbars);  // [NB] image slots
     ItemSlot* stg_slot = slots + NB;                                                 // staging slot
+    uint32_t* cta_thr = reinterpret_cast<uint32_t*>(stg_slot + 1);  // [NB]: the CTA's k-th distance per item
 
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) {
@@ -678,7 +800,10 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
             if (sl.pair == kEndItem) {
                 __syncwarp();
                 if (lane == 0) {
-                    if (ew == 0) slots[b] = sl;
+                    if (ew == 0) {
+                        slots[b] = sl;
+                        cta_thr[b] = 0xffffffffu;
+                    }
                     mbar_arrive(img_full + b);
                 }
                 break;
@@ -722,7 +847,10 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
                 if (lane == 0) mbar_arrive(stg_empty);
             }
             if (lane == 0) {
-                if (ew == 0) slots[b] = sl;
+                if (ew == 0) {
+                    slots[b] = sl;
+                    cta_thr[b] = 0xffffffffu;
+                }
                 mbar_arrive(img_full + b);
             }
         }
@@ -753,7 +881,7 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
         uint32_t a, e_end;
         warp_range<W>(sl, warp, a, e_end);
         if (a < e_end) {
-            const ScanCtx cx{ring_s, lane, bt0 + b * (kImgBytes & 0xffff0000u), k, skew_codes, ids, gthr,
+            const ScanCtx cx{cta_thr + b, ring_s, lane, bt0 + b * (kImgBytes & 0xffff0000u), k, skew_codes, ids, gthr,
                              q_item_off, pool_cnt, pool_key, pool_id};
             const uint32_t bn = NB == 1 ? 0u : (i + 1) % NB;
             const NextRange nx{slots + bn, img_full + bn, (NB == 1 ? i + 1 : (i + 1) / NB) & 1u, warp, NB > 1};
@@ -763,98 +891,6 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(img_empty + b);
-    }
-}
-
-// Work items for the fast path: per (q, p) pair, ceil(len/32) tiles cut into
-// items of <= it_tiles tiles, emitted largest-first (log2 size buckets) so
-// the big lists set each query's threshold early and the small ones fill the
-// tail. q_item_off[q] = prefix of per-query item counts (candidate-pool
-// offsets). Also resets the per-query threshold and pool counters, and
-// writes scanned_vectors (annindex.hpp:305: the sum of probed list sizes).
-__global__ void __launch_bounds__(1024) plan_skew_kernel(const uint32_t* __restrict__ probe,
-                                                         const uint32_t* __restrict__ list_len, uint32_t nq,
-                                                         uint32_t nprobe, uint32_t it_tiles,
-                                                         uint64_t* __restrict__ scanned,
-                                                         uint4* __restrict__ items, uint32_t* __restrict__ num_items,
-                                                         uint32_t* __restrict__ cursor, uint32_t* __restrict__ q_item_off,
-                                                         uint32_t* __restrict__ gthr, uint32_t* __restrict__ pool_cnt,
-                                                         uint64_t item_cap) {
-    __shared__ uint32_t tmp[33];
-    __shared__ uint32_t bucket_cnt[32], bucket_pos[32];
-    const uint32_t P = nq * nprobe;
-    pdl_wait();  // probe[] comes from the previous kernel
-    if (threadIdx.x < 32) bucket_cnt[threadIdx.x] = 0;
-    for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x) scanned[q] = 0;
-    __syncthreads();
-    // pass 1: per-query item counts (prefix) and bucket histogram
-    uint32_t carry = 0;
-    for (uint32_t base = 0; base < P; base += blockDim.x) {
-        const uint32_t i = base + threadIdx.x;
-        const bool valid = i < P;
-        const uint32_t len = valid ? list_len[probe[i]] : 0;
-        if (len) atomicAdd(reinterpret_cast<unsigned long long*>(scanned + i / nprobe), (unsigned long long)len);
-        const uint32_t tiles = (len + kTileEntries - 1) / kTileEntries;
-        const uint32_t nit = (tiles + it_tiles - 1) / it_tiles;
-        for (uint32_t j = 0; j < nit; ++j) {
-            const uint32_t t = min(tiles, (j + 1) * it_tiles) - j * it_tiles;
-            atomicAdd(&bucket_cnt[31 - __clz(t)], 1u);
-        }
-        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-        uint32_t incl = nit;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += t;
-        }
-        if (lane == 31) tmp[w] = incl;
-        __syncthreads();
-        if (w == 0) {
-            const int nw = blockDim.x >> 5;
-            uint32_t x = lane < nw ? tmp[lane] : 0u, xi = x;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                uint32_t t = __shfl_up_sync(0xffffffffu, xi, o);
-                if (lane >= o) xi += t;
-            }
-            if (lane < nw) tmp[lane] = xi - x;
-            if (lane == nw - 1) tmp[32] = xi;
-        }
-        __syncthreads();
-        const uint32_t excl = carry + tmp[w] + incl - nit;
-        if (valid && i % nprobe == 0) q_item_off[i / nprobe] = excl;
-        carry += tmp[32];
-        __syncthreads();
-    }
-    // bucket start positions, largest bucket first
-    if (threadIdx.x == 0) {
-        uint32_t pos = 0;
-        for (int bkt = 31; bkt >= 0; --bkt) {
-            bucket_pos[bkt] = pos;
-            pos += bucket_cnt[bkt];
-        }
-    }
-    __syncthreads();
-    pdl_trigger();
-    // pass 2: scatter items
-    for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
-        const uint32_t len = list_len[probe[i]];
-        const uint32_t tiles = (len + kTileEntries - 1) / kTileEntries;
-        const uint32_t nit = (tiles + it_tiles - 1) / it_tiles;
-        for (uint32_t j = 0; j < nit; ++j) {
-            const uint32_t te = min(tiles, (j + 1) * it_tiles);
-            const uint32_t slot = atomicAdd(&bucket_pos[31 - __clz(te - j * it_tiles)], 1u);
-            if (slot < item_cap) items[slot] = make_uint4(i, j * it_tiles, te, 0u);
-        }
-    }
-    if (threadIdx.x == 0) {
-        *num_items = carry;
-        *cursor = 0;
-        q_item_off[nq] = carry;
-    }
-    for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x) {
-        gthr[q] = 0xffffffffu;
-        pool_cnt[q] = 0;
     }
 }
 
@@ -886,29 +922,24 @@ static int check(const char* what) {
     return PRAG_GPU_OK;
 }
 
-int launch_plan_skew(const DeviceIndex& ix, const uint32_t* probe, uint32_t nq, uint32_t nprobe, uint32_t it_tiles,
-                     uint64_t* scanned, uint4* items, uint32_t* num_items, uint32_t* cursor, uint32_t* q_item_off,
-                     uint32_t* gthr, uint32_t* pool_cnt, uint64_t item_cap, cudaStream_t s) {
-    PG_CUDA(launch_pdl(plan_skew_kernel, dim3(1), dim3(1024), 0, s, probe, ix.list_len, nq, nprobe, it_tiles, scanned,
-                       items, num_items, cursor, q_item_off, gthr, pool_cnt, item_cap));
-    return check("plan_skew");
-}
-
 int launch_lut_images(const DeviceIndex& ix, const float* queries, const uint32_t* probe, uint32_t nq,
-                      uint32_t nprobe, float* luts, cudaStream_t s) {
+                      uint32_t nprobe, float* luts, uint32_t it_tiles, uint64_t* scanned, uint4* items,
+                      uint32_t* num_items, uint32_t* cursor, uint32_t* q_item_off, uint32_t* gthr,
+                      uint32_t* pool_cnt, uint64_t item_cap, cudaStream_t s) {
     const uint32_t npairs = nq * nprobe;
+    const PlanArgs pa{it_tiles, scanned, items, num_items, cursor, q_item_off, gthr, pool_cnt, item_cap};
     // small batches: 2 subquantizers per CTA (4x the CTAs, 1/4 of the serial
     // codeword round trips each); large ones: 8 (residuals shared by more work)
     const bool small = uint64_t((npairs + kLutPairs - 1) / kLutPairs) * (ix.nsq / 8) < 2 * 148;
-    dim3 grid((npairs + kLutPairs - 1) / kLutPairs, ix.nsq / (small ? 2 : 8));
+    dim3 grid((npairs + kLutPairs - 1) / kLutPairs + 1, ix.nsq / (small ? 2 : 8));
 #define PG_LUT(MM, SS)                                                                                          \
     do {                                                                                                        \
         if (small)                                                                                              \
             PG_CUDA(launch_pdl(lut_image_kernel<MM, SS, 2>, grid, dim3(256), 0, s, queries, ix.centroids,       \
-                               ix.codewordsT, probe, ix.list_len, nq, nprobe, ix.d, ix.sub_dim, luts));           \
+                               ix.codewordsT, probe, ix.list_len, nq, nprobe, ix.d, ix.sub_dim, luts, pa));       \
         else                                                                                                    \
             PG_CUDA(launch_pdl(lut_image_kernel<MM, SS, 8>, grid, dim3(256), 0, s, queries, ix.centroids,       \
-                               ix.codewordsT, probe, ix.list_len, nq, nprobe, ix.d, ix.sub_dim, luts));           \
+                               ix.codewordsT, probe, ix.list_len, nq, nprobe, ix.d, ix.sub_dim, luts, pa));       \
     } while (0)
     if (ix.nsq == 32 && ix.sub_dim == 12)
         PG_LUT(32, 12);
