@@ -604,7 +604,7 @@ __device__ uint32_t block_kth_reg(const uint32_t (&key)[VPT], uint32_t n, uint32
 
 // K4 (fast path): exact top-k over the per-query candidate pool the fused
 // scan filled (each warp's exact top-k of its share of the lists). Pools of
-// up to 8 * 1024 candidates are selected from registers in one read (radix
+// up to 16 * 1024 candidates are selected from registers in one read (radix
 // select of the k-th key, then the <= kSortCap survivors ranked by
 // (distance, chunk_id)); larger pools, or more than kSortCap survivors tied
 // at the k-th distance, take the general multi-pass block_topk.
@@ -619,7 +619,7 @@ __global__ void __launch_bounds__(kSelThreads) select_pool_kernel(
     pdl_wait();  // the pool comes from the scan kernel
     const size_t off = size_t(q_item_off[q]) * warps * k;
     const uint32_t n = pool_cnt[q];
-    constexpr int VPT = 8;
+    constexpr int VPT = 16;
     if (n <= VPT * kSelThreads) {
         uint32_t key[VPT];
 #pragma unroll

@@ -85,6 +85,13 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t phase)
     }
 }
 
+__device__ __forceinline__ void named_sync(uint32_t id, uint32_t count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_arrive(uint32_t id, uint32_t count) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -382,7 +389,8 @@ constexpr uint32_t kEndItem = 0xffffffffu;
 constexpr uint32_t kMinWarpTiles = 4;  // a warp re-reads one tail tile per range: keep ranges >= 4 tiles
 
 struct ItemSlot {
-    uint32_t pair, tb, te, len, q, pad;
+    uint32_t pair, tb, te, len, q;
+    uint32_t thr;            // the query's shared threshold when the producer fetched the item
     uint64_t tile_byte_off;  // skew_off[list] * tile bytes
     uint64_t lbase;          // list_off[list]: padded entry slot of the list's entry 0
 };
@@ -543,10 +551,11 @@ __device__ __forceinline__ bool scan_range(const ScanCtx& cx, const ItemSlot& sl
     // exactly the 16-byte chunks it will read itself (cp.async, one commit
     // group per tile), so a lane only ever waits on its own copies: no
     // barrier, no cross-lane synchronisation.
-    // the query's shared threshold (other warps' k-th distances) is read once
-    // per range (an in-loop refresh would put a global load on every tile),
-    // issued before the ring prologue so its latency overlaps the copies
-    uint32_t g_thr = ld_relaxed(gthr + q);
+    // the query's shared threshold (other CTAs' k-th distances), read once per
+    // range (an in-loop refresh would put a global load on every tile) and
+    // issued before the ring prologue so its latency overlaps the copies; the
+    // producer's snapshot from item fetch time bounds it meanwhile
+    uint32_t g_thr = min(sl.thr, ld_relaxed(gthr + q));
     const unsigned char* src_lane = tiles + lane * 16;
     const uint32_t dst_lane = ring_s + lane * 16;
     if (!prefetched) {
@@ -749,36 +758,50 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
     pdl_wait();  // items, LUTs and thresholds come from the previous kernels
     const uint32_t total = *num_items;
 
+    // hand-offs in the "slot is free" direction are named barriers: a waiting
+    // warp is descheduled until the last arrival (no polling), and arriving
+    // warps do not wait. Barrier 1 + b: consumers arrive when done with image
+    // buffer b, expanders sync before overwriting it; barrier 1 + NB:
+    // expanders arrive when done with the staging buffer, the producer syncs
+    // before refilling it. The "data is ready" direction stays on mbarriers.
+    constexpr uint32_t kImgEmptyCount = uint32_t(W + kExpWarps) * 32;
+    constexpr uint32_t kStgEmptyCount = uint32_t(kExpWarps + 1) * 32;
+    constexpr uint32_t kStgBar = 1 + NB;
     if (warp == uint32_t(W)) {
         // ------------------------------------------------------ producer
-        if (lane == 0) {
-            uint32_t nx = atomicAdd(cursor, 1u);
-            uint32_t round = 0;  // staging rounds issued (kHalves per item)
-            for (;;) {
-                ItemSlot sl{};
-                sl.pair = kEndItem;
-                if (nx < total) {
-                    const uint4 w4 = items[nx];
-                    const uint32_t list = probe[w4.x];
-                    sl.pair = w4.x;
-                    sl.tb = w4.y;
-                    sl.te = w4.z;
-                    sl.len = list_len[list];
-                    sl.q = w4.x / nprobe;
-                    sl.tile_byte_off = skew_off[list] * L::kTile;
-                    sl.lbase = list_off[list];
-                    nx = atomicAdd(cursor, 1u);  // next item's index, fetched ahead
-                }
-                if (sl.pair == kEndItem) {
-                    pdl_trigger();  // no more work items: let the pool selection launch
-                    mbar_wait_backoff(stg_empty, (round & 1u) ^ 1u);
+        uint32_t nx = 0;
+        if (lane == 0) nx = atomicAdd(cursor, 1u);
+        uint32_t round = 0;  // staging rounds issued (kHalves per item)
+        for (;;) {
+            ItemSlot sl{};
+            sl.pair = kEndItem;
+            if (lane == 0 && nx < total) {
+                const uint4 w4 = items[nx];
+                const uint32_t list = probe[w4.x];
+                sl.pair = w4.x;
+                sl.tb = w4.y;
+                sl.te = w4.z;
+                sl.len = list_len[list];
+                sl.q = w4.x / nprobe;
+                sl.tile_byte_off = skew_off[list] * L::kTile;
+                sl.lbase = list_off[list];
+                sl.thr = ld_relaxed(gthr + sl.q);
+                nx = atomicAdd(cursor, 1u);  // next item's index, fetched ahead
+            }
+            const uint32_t pair = __shfl_sync(0xffffffffu, sl.pair, 0);
+            if (pair == kEndItem) {
+                pdl_trigger();  // no more work items: let the pool selection launch
+                if (round > 0) named_sync(kStgBar, kStgEmptyCount);
+                if (lane == 0) {
                     *stg_slot = sl;
                     mbar_arrive(stg_full);
-                    break;
                 }
-                const unsigned char* src = reinterpret_cast<const unsigned char*>(luts) + size_t(sl.pair) * M * 1024;
-                for (uint32_t h = 0; h < kHalves; ++h, ++round) {
-                    mbar_wait_backoff(stg_empty, (round & 1u) ^ 1u);
+                break;
+            }
+            const unsigned char* src = reinterpret_cast<const unsigned char*>(luts) + size_t(pair) * M * 1024;
+            for (uint32_t h = 0; h < kHalves; ++h, ++round) {
+                if (round > 0) named_sync(kStgBar, kStgEmptyCount);
+                if (lane == 0) {
                     if (h == 0) *stg_slot = sl;
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     mbar_expect_tx(stg_full, kStageBytes);
@@ -794,9 +817,9 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
         uint32_t round = 0;
         for (uint32_t i = 0;; ++i) {
             const uint32_t b = NB == 1 ? 0u : i % NB;
-            mbar_wait_backoff(stg_full, round & 1u);
+            mbar_wait(stg_full, round & 1u);
             const ItemSlot sl = *stg_slot;
-            mbar_wait_backoff(img_empty + b, ((NB == 1 ? i : i / NB) & 1u) ^ 1u);
+            if (i >= uint32_t(NB)) named_sync(1 + b, kImgEmptyCount);  // consumers done with item i - NB
             if (sl.pair == kEndItem) {
                 __syncwarp();
                 if (lane == 0) {
@@ -810,7 +833,7 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
             }
             float* img = reinterpret_cast<float*>(smem + img_off + b * kImgBytes);
             for (uint32_t h = 0; h < kHalves; ++h, ++round) {
-                if (h > 0) mbar_wait_backoff(stg_full, round & 1u);
+                if (h > 0) mbar_wait(stg_full, round & 1u);
                 // 4x4 register transposes: lane L owns codes cb + 4L .. +3 and
                 // walks the 8 groups of 4 subquantizers diagonally (group
                 // (g + L) mod 8), so every LDS.128 (4 codes of one staged row)
@@ -843,9 +866,9 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
                         }
                     }
                 }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(stg_empty);
+                named_arrive(kStgBar, kStgEmptyCount);  // staging consumed
             }
+            __syncwarp();
             if (lane == 0) {
                 if (ew == 0) {
                     slots[b] = sl;
@@ -890,7 +913,7 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
             pref = false;
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(img_empty + b);
+        named_arrive(1 + b, kImgEmptyCount);  // image buffer b is free
     }
 }
 

@@ -64,10 +64,12 @@ def gather_merge(local: BatchResult, k: int, merge: Optional[Callable] = None, g
     rank = dist.get_rank(group)
     rec = pack_result(local, k)
     g = torch.empty((world,) + tuple(rec.shape), dtype=rec.dtype, device=rec.device)
-    if rec.is_cuda:
-        dist.all_gather_into_tensor(g, rec, group=group)
-    else:  # gloo
-        dist.all_gather(list(g.unbind(0)), rec, group=group)
+    if rec.is_cuda and dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(g, rec, group=group)  # NCCL over NVLink
+    else:  # gloo (CPU tests, or a single-GPU functional run of the N>1 path)
+        parts = [torch.empty_like(rec, device="cpu") for _ in range(world)]
+        dist.all_gather(parts, rec.cpu(), group=group)
+        g.copy_(torch.stack(parts))
     if rank != root:
         return None
     ids, dd, cnt, sc = unpack_results(g, k)
