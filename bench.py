@@ -254,10 +254,20 @@ def main():
     with ClockSampler(local) as clk:
         # pre-roll: back-to-back steps for ~1 s so the clock sampler sees this
         # load (the timed region itself is only tens of ms)
+        # (every rank must run the same number of steps: each one contains a
+        # collective, so with N > 1 the ranks agree on when to stop)
         t_end = time.time() + 1.0
-        while time.time() < t_end:
+        while True:
             step_dev(qdev, nprobe, k)
             torch.cuda.synchronize(dev)
+            stop = time.time() >= t_end
+            if world > 1:
+                flag = torch.tensor([1 if stop else 0], dtype=torch.int32,
+                                    device=dev if backend == "nccl" else "cpu")
+                dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+                stop = bool(flag.item())
+            if stop:
+                break
         t_dev = timed(lambda: step_dev(qdev, nprobe, k), args.steps, args.warmup)
         # e2e: pinned host queries -> host results through the C ABI
         qhost = torch.from_numpy(queries[:nq].copy()).pin_memory()

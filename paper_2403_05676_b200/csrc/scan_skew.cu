@@ -374,7 +374,7 @@ struct SkewCfg;
 template <>
 struct SkewCfg<32> {
     static constexpr int kWarps = 13;  // consumer warps; + 1 producer + 2 expander warps, 1 CTA per SM
-    static constexpr int kDepth = 4;   // TMA ring slots per consumer warp
+    static constexpr int kDepth = 4;   // cp.async ring slots per consumer warp
     static constexpr int kBufs = 2;    // SMEM images: item i+1's is built while item i is scanned
 };
 template <>
@@ -495,6 +495,56 @@ struct ScanCtx {
     uint64_t* pool_id;
 };
 
+// Exact warp top-k (k <= 32): lane i holds the i-th (distance bits, entry
+// slot) by (distance, chunk_id) (annindex.hpp:55-58); `thr` is the k-th key
+// (0xffffffff until the list is full) and `g` the warp's view of the query's
+// shared threshold. Chunk ids are read only on an exact distance tie.
+struct WarpTopK {
+    uint32_t key, pos, thr, g;
+};
+
+__device__ __forceinline__ void topk_offer(WarpTopK& t, uint32_t key, bool valid, uint32_t mypos, uint32_t lane,
+                                           uint32_t k, const uint64_t* __restrict__ ids, uint32_t* gthr_q,
+                                           uint32_t* cta_thr) {
+    const bool pass = valid && key <= min(t.thr, t.g);
+    unsigned bal = __ballot_sync(0xffffffffu, pass);
+    if (!bal) return;
+    while (bal) {
+        const int src = __ffs(bal) - 1;
+        bal &= bal - 1;
+        const uint32_t ck = __shfl_sync(0xffffffffu, key, src);
+        const uint32_t cp = __shfl_sync(0xffffffffu, mypos, src);
+        if (ck > t.thr) continue;  // threshold tightened by an earlier insertion
+        bool gt = t.key > ck;      // lanes whose element sorts after the candidate
+        if (__any_sync(0xffffffffu, t.key == ck)) {  // exact distance tie: compare ids
+            const uint64_t cid = ids[cp];
+            const uint64_t mid = t.key == ck ? ids[t.pos] : 0ull;
+            gt = gt || (t.key == ck && mid > cid);
+        }
+        const unsigned gm = __ballot_sync(0xffffffffu, gt);
+        const int pos = gm ? __ffs(gm) - 1 : 32;
+        if (pos < int(k)) {
+            const uint32_t uk = __shfl_up_sync(0xffffffffu, t.key, 1);
+            const uint32_t up = __shfl_up_sync(0xffffffffu, t.pos, 1);
+            if (int(lane) > pos) {
+                t.key = uk;
+                t.pos = up;
+            } else if (int(lane) == pos) {
+                t.key = ck;
+                t.pos = cp;
+            }
+            t.thr = __shfl_sync(0xffffffffu, t.key, k - 1);
+        }
+    }
+    if (t.thr < t.g) {
+        if (lane == 0) {
+            atomicMin(gthr_q, t.thr);
+            atomicMin(cta_thr, t.thr);
+        }
+        t.g = t.thr;
+    }
+}
+
 // The next item a warp will scan (buffer b^1), known once its image is
 // published; lets the tail of one range prefetch the head of the next.
 struct NextRange {
@@ -555,7 +605,7 @@ __device__ __forceinline__ bool scan_range(const ScanCtx& cx, const ItemSlot& sl
     // range (an in-loop refresh would put a global load on every tile) and
     // issued before the ring prologue so its latency overlaps the copies; the
     // producer's snapshot from item fetch time bounds it meanwhile
-    uint32_t g_thr = min(sl.thr, ld_relaxed(gthr + q));
+    WarpTopK t{0xffffffffu, 0xffffffffu, 0xffffffffu, min(sl.thr, ld_relaxed(gthr + q))};
     const unsigned char* src_lane = tiles + lane * 16;
     const uint32_t dst_lane = ring_s + lane * 16;
     if (!prefetched) {
@@ -579,9 +629,6 @@ __device__ __forceinline__ bool scan_range(const ScanCtx& cx, const ItemSlot& sl
     bool nx_ok = false;
     uint32_t nx_a = 0, nx_e = 0;
     const unsigned char* nx_src = nullptr;
-    uint32_t tk_key = 0xffffffffu;  // warp top-k: lane i holds the i-th (distance bits, entry slot)
-    uint32_t tk_pos = 0xffffffffu;
-    uint32_t thr_key = 0xffffffffu;
     float cur = 0.0f, prev = 0.0f;
     for (uint32_t j = a; j <= e_end; ++j, ++consumed) {
         const uint32_t slot = consumed % D;
@@ -622,63 +669,21 @@ __device__ __forceinline__ bool scan_range(const ScanCtx& cx, const ItemSlot& sl
             }
         }
         cp_async_commit();
-        g_thr = min(g_thr, *reinterpret_cast<volatile uint32_t*>(cx.cta_thr));  // other warps of this item
+        t.g = min(t.g, *reinterpret_cast<volatile uint32_t*>(cx.cta_thr));  // other warps of this item
         // entry 32(j-1)+lane is complete in `prev`
         const uint32_t e = (j - 1) * kTileEntries + lane;
-        const bool valid = j > a && e < sl.len;
         const uint32_t key = __float_as_uint(prev);
         prev = cur;
         cur = 0.0f;
-        const uint32_t lim = min(thr_key, g_thr);
-        const bool pass = valid && key <= lim;
-        unsigned bal = __ballot_sync(0xffffffffu, pass);
-        if (bal) {
-            const uint32_t mypos = uint32_t(sl.lbase) + e;
-            while (bal) {
-                const int src = __ffs(bal) - 1;
-                bal &= bal - 1;
-                const uint32_t ck = __shfl_sync(0xffffffffu, key, src);
-                const uint32_t cp = __shfl_sync(0xffffffffu, mypos, src);
-                if (ck > thr_key) continue;  // threshold tightened by an earlier insertion
-                // lanes whose element sorts after the candidate, by
-                // (distance, chunk_id) (annindex.hpp:55-58)
-                bool gt = tk_key > ck;
-                if (__any_sync(0xffffffffu, tk_key == ck)) {  // exact distance tie: compare ids
-                    const uint64_t cid = ids[cp];
-                    const uint64_t mid = tk_key == ck ? ids[tk_pos] : 0ull;
-                    gt = gt || (tk_key == ck && mid > cid);
-                }
-                const unsigned gm = __ballot_sync(0xffffffffu, gt);
-                const int pos = gm ? __ffs(gm) - 1 : 32;
-                if (pos < int(k)) {
-                    const uint32_t uk = __shfl_up_sync(0xffffffffu, tk_key, 1);
-                    const uint32_t up = __shfl_up_sync(0xffffffffu, tk_pos, 1);
-                    if (int(lane) > pos) {
-                        tk_key = uk;
-                        tk_pos = up;
-                    } else if (int(lane) == pos) {
-                        tk_key = ck;
-                        tk_pos = cp;
-                    }
-                    thr_key = __shfl_sync(0xffffffffu, tk_key, k - 1);
-                }
-            }
-            if (thr_key < g_thr) {
-                if (lane == 0) {
-                    atomicMin(gthr + q, thr_key);
-                    atomicMin(cx.cta_thr, thr_key);
-                }
-                g_thr = thr_key;
-            }
-        }
+        topk_offer(t, key, j > a && e < sl.len, uint32_t(sl.lbase) + e, lane, k, ids, gthr + q, cx.cta_thr);
     }
     // publish this warp's list into the query's candidate pool, minus entries
     // above the query's shared threshold: some warp holds k candidates at or
     // below it, so those entries cannot make the final top-k
     // the warp's view (shared threshold at range start, its own and this CTA's
     // k-th distances) is never below the final shared threshold: a valid filter
-    const uint32_t g_pub = min(g_thr, *reinterpret_cast<volatile uint32_t*>(cx.cta_thr));
-    const unsigned have = __ballot_sync(0xffffffffu, lane < k && tk_key != 0xffffffffu && tk_key <= g_pub);
+    const uint32_t g_pub = min(t.g, *reinterpret_cast<volatile uint32_t*>(cx.cta_thr));
+    const unsigned have = __ballot_sync(0xffffffffu, lane < k && t.key != 0xffffffffu && t.key <= g_pub);
     const uint32_t cnt = __popc(have);
     if (cnt) {
         uint32_t base = 0;
@@ -686,8 +691,8 @@ __device__ __forceinline__ bool scan_range(const ScanCtx& cx, const ItemSlot& sl
         base = __shfl_sync(0xffffffffu, base, 0);
         const size_t poff = size_t(q_item_off[q]) * W * k;
         if (lane < cnt) {
-            pool_key[poff + base + lane] = ord_key(__uint_as_float(tk_key));
-            pool_id[poff + base + lane] = ids[tk_pos];
+            pool_key[poff + base + lane] = ord_key(__uint_as_float(t.key));
+            pool_id[poff + base + lane] = ids[t.pos];
         }
     }
     return nx_ok;
