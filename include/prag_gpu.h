@@ -189,6 +189,22 @@ int prag_gpu_set_coarse_path(prag_gpu_index* index, int path);
 int prag_gpu_set_profiling(prag_gpu_index* index, int enabled);
 int prag_gpu_last_timings(const prag_gpu_index* index, prag_gpu_timings* out);
 
+/* ------------------------------------------------ query embedding */
+/* Device-resident prag::ChunkEmbedder (tokendb.hpp:84-124), the step before
+ * search in LocalRetriever::retrieve (pipeline.hpp:227). Token unit vectors
+ * for ids [0, vocab) are computed on the host exactly as token_unit_vector
+ * (tokendb.hpp:63-80) and kept in HBM; prag_gpu_embed reproduces embed()
+ * bit for bit (double accumulation in token order, sequential squared norm,
+ * IEEE sqrt/div, fp32 rounding; e_0 for an all-PAD chunk). */
+typedef struct prag_gpu_embedder prag_gpu_embedder;
+int prag_gpu_embedder_create(uint32_t d, uint64_t seed, uint32_t vocab, int device, prag_gpu_embedder** out);
+void prag_gpu_embedder_free(prag_gpu_embedder* embedder);
+/* tokens: nchunks x m token ids (PAD = 0 skipped), host or device; out:
+ * nchunks x d floats, host or device. A token id >= vocab is CONFIG (checked
+ * when any pointer is host memory). */
+int prag_gpu_embed(prag_gpu_embedder* embedder, const uint32_t* tokens, uint32_t nchunks, uint32_t m, float* out,
+                   void* stream);
+
 /* ------------------------------------------------- config-E harness */
 /* One synthetic decode step on `stream` (device pointers): y[r] = W[r] . x
  * for a rows x cols fp32 weight matrix, plus a streaming read of kv_floats

@@ -15,6 +15,7 @@
 //   bench   <index> <queries.f32> <nq> <nprobe> <k> <threads> <reps> <warmups> [max_seconds]
 //   calibrate <index> <queries.f32> <nq> <k> <grid_csv> <repeats>
 //   brute   <vectors.f32> <n> <d> <queries.f32> <nq> <k> <out.bin>
+//   embed   <tokens.u32> <nchunks> <m> <d> <seed> <out.f32>   (prag::ChunkEmbedder::embed)
 #include <atomic>
 #include <chrono>
 #include <cstdio>
@@ -28,6 +29,7 @@
 
 #include "prag/annindex.hpp"
 #include "prag/perfmodel.hpp"
+#include "prag/tokendb.hpp"
 
 namespace {
 
@@ -88,6 +90,25 @@ int main(int argc, char** argv) {
             auto vecs = rows(read_f32(argv[2], n * d), n, d);
             auto [index, codebook] = prag::train_index(vecs, params);
             prag::store_index(index, codebook, argv[8]);
+            return 0;
+        }
+        if (cmd == "embed" && argc == 8) {
+            const std::size_t nch = std::stoull(argv[3]), m = std::stoull(argv[4]);
+            const std::uint32_t d = std::stoul(argv[5]);
+            const std::uint64_t seed = std::stoull(argv[6]);
+            std::vector<std::uint32_t> tok(nch * m);
+            {
+                std::ifstream is(argv[2], std::ios::binary);
+                is.read(reinterpret_cast<char*>(tok.data()), tok.size() * 4);
+                if (!is) throw std::runtime_error("short read tokens");
+            }
+            prag::ChunkEmbedder emb(d, seed);
+            std::ofstream os(argv[7], std::ios::binary);
+            for (std::size_t c = 0; c < nch; ++c) {
+                prag::TokenChunk chunk(tok.begin() + c * m, tok.begin() + (c + 1) * m);
+                const auto v = emb.embed(chunk);
+                os.write(reinterpret_cast<const char*>(v.data()), v.size() * 4);
+            }
             return 0;
         }
         if (cmd == "search" && argc == 8) {

@@ -65,25 +65,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
         : "memory");
 }
 
-// Support roles (producer, expanders) poll with a fixed back-off instead of
-// a suspend-hinted try_wait: the hinted wait is woken by every barrier and
-// async-copy event in the CTA, and those wake-ups cost consumer issue slots.
-__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t phase) {
-    for (;;) {
-        uint32_t done;
-        asm volatile(
-            "{\n"
-            ".reg .pred p;\n"
-            "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-            "selp.u32 %0, 1, 0, p;\n"
-            "}\n"
-            : "=r"(done)
-            : "r"(smem_u32(bar)), "r"(phase)
-            : "memory");
-        if (done) return;
-        __nanosleep(200);
-    }
-}
 
 __device__ __forceinline__ void named_sync(uint32_t id, uint32_t count) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");

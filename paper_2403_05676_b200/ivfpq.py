@@ -208,6 +208,45 @@ class GpuIndex:
         return {f: getattr(t, f) for f, _ in Timings._fields_}
 
 
+class GpuChunkEmbedder:
+    """Device-resident prag::ChunkEmbedder (tokendb.hpp:84-124): bit-identical
+    bag-of-tokens embeddings, computed on the GPU."""
+
+    def __init__(self, d: int, seed: int, vocab: int = 257, device: int = 0):
+        h = C.c_void_p()
+        check(lib().prag_gpu_embedder_create(d, seed, vocab, device, C.byref(h)))
+        self._h, self.d, self.seed, self.vocab = h, d, seed, vocab
+
+    def embed(self, chunks, stream=None):
+        """chunks: [n, m] token ids (numpy / CUDA tensor) -> [n, d] float32."""
+        on_dev = torch is not None and isinstance(chunks, torch.Tensor) and chunks.is_cuda
+        if on_dev:
+            t = chunks.contiguous().to(torch.int32)
+            n, m = t.shape
+            out = torch.empty((n, self.d), dtype=torch.float32, device=t.device)
+            if stream is None:
+                stream = torch.cuda.current_stream(t.device)
+        else:
+            t = np.ascontiguousarray(chunks, dtype=np.uint32)
+            if t.ndim == 1:
+                t = t.reshape(1, -1)
+            n, m = t.shape
+            out = np.zeros((n, self.d), dtype=np.float32)
+        check(lib().prag_gpu_embed(self._h, _ptr(t), n, m, _ptr(out), _stream_ptr(stream)))
+        return out
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib().prag_gpu_embedder_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def load_index(path: str, device: int = 0) -> GpuIndex:
     return GpuIndex.load(path, device)
 
