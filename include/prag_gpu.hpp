@@ -212,22 +212,25 @@ inline std::uint32_t select_nprobe(const RetrievalPerfModel& model, double budge
 
 #ifdef PRAG_GPU_HAVE_REFERENCE
 // Drop-in for prag::LocalRetriever (pipeline.hpp:213-249): same constructor
-// arguments, same nprobe directive handling (:224-226), same embedding
-// (:227) and record resolution (:232-235); the search runs on the B200.
-// Re-entrant for concurrent callers (service.hpp:303, :338): each call uses
-// its own stream-ordered workspace inside the library; the embedder's
-// token cache (tokendb.hpp:115-119) is guarded by a mutex here.
+// arguments, same nprobe directive handling (:224-226), same record
+// resolution (:232-235). The query embedding (:227) and the search run on the
+// B200: prag_gpu_embed reproduces ChunkEmbedder::embed bit for bit from
+// token vectors computed on the host for the database's vocabulary.
+// Re-entrant for concurrent callers (service.hpp:303, :338): each search
+// uses its own stream-ordered workspace inside the library; the embedder's
+// staging buffers are guarded by a mutex here.
 class GpuRetriever : public ::prag::Retriever {
 public:
     GpuRetriever(const ::prag::Database& db, const ::prag::IvfIndex& index, const ::prag::PqCodebook& codebook,
                  std::uint64_t embed_seed, ::prag::RetrievalPerfModel perf = {}, double safety_margin = 0.10,
                  int device = 0)
         : db_(&db), gpu_(Index::from_reference(index, codebook, device)), nlist_(index.nlist),
-          embedder_(db.d, embed_seed), perf_(perf), safety_margin_(safety_margin) {}
+          embedder_(make_embedder(db, embed_seed, device)), perf_(perf), safety_margin_(safety_margin) {}
 
     GpuRetriever(const ::prag::Database& db, Index gpu_index, std::uint64_t embed_seed,
                  ::prag::RetrievalPerfModel perf = {}, double safety_margin = 0.10)
-        : db_(&db), gpu_(std::move(gpu_index)), nlist_(gpu_.nlist()), embedder_(db.d, embed_seed), perf_(perf),
+        : db_(&db), gpu_(std::move(gpu_index)), nlist_(gpu_.nlist()),
+          embedder_(make_embedder(db, embed_seed, gpu_.describe().device)), perf_(perf),
           safety_margin_(safety_margin) {}
 
     ::prag::RetrievalOutcome retrieve(const ::prag::TokenChunk& query_tokens, std::uint32_t k,
@@ -236,10 +239,11 @@ public:
         const std::uint32_t nprobe = directive.auto_mode
                                          ? ::prag::select_nprobe(perf_, directive.budget_s, nlist_, safety_margin_)
                                          : std::min(directive.nprobe, nlist_);
-        std::vector<float> query;
+        std::vector<float> query(db_->d);
         {
             std::lock_guard<std::mutex> lk(embed_mu_);
-            query = embedder_.embed(query_tokens);
+            check(prag_gpu_embed(embedder_.get(), query_tokens.data(), 1, std::uint32_t(query_tokens.size()),
+                                 query.data(), nullptr));
         }
         auto found = search_batch(gpu_, query.data(), 1, SearchParams{nprobe, k, false})[0];
         ::prag::RetrievalOutcome outcome;
@@ -268,10 +272,28 @@ public:
     }
 
 private:
+    struct FreeEmbedder {
+        void operator()(prag_gpu_embedder* e) const { prag_gpu_embedder_free(e); }
+    };
+    using EmbedderPtr = std::unique_ptr<prag_gpu_embedder, FreeEmbedder>;
+
+    // Token vectors for every id the database uses (at least the byte
+    // vocabulary, kByteVocabSize, common.hpp:21).
+    static EmbedderPtr make_embedder(const ::prag::Database& db, std::uint64_t seed, int device) {
+        std::uint32_t vocab = ::prag::kByteVocabSize;
+        for (const auto& rec : db.records) {
+            for (auto t : rec.tokens) vocab = std::max<std::uint32_t>(vocab, t + 1);
+            for (auto t : rec.continuation) vocab = std::max<std::uint32_t>(vocab, t + 1);
+        }
+        prag_gpu_embedder* e = nullptr;
+        check(prag_gpu_embedder_create(db.d, seed, vocab, device, &e));
+        return EmbedderPtr(e);
+    }
+
     const ::prag::Database* db_;
     Index gpu_;
     std::uint32_t nlist_;
-    ::prag::ChunkEmbedder embedder_;
+    EmbedderPtr embedder_;
     std::mutex embed_mu_;
     ::prag::RetrievalPerfModel perf_;
     double safety_margin_;
