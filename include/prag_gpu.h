@@ -113,6 +113,16 @@ int prag_gpu_index_from_host(uint32_t nlist, uint32_t d, uint32_t nsq, const flo
                              const float* codewords, const uint64_t* list_off, const uint64_t* ids,
                              const uint8_t* codes, int device, prag_gpu_index** out);
 
+/* Config-D fixture (BASELINE.json configs[3]): an index of `ntotal` entries
+ * built directly in HBM, for the m = 32 / 64 fast path (k <= 32). List sizes
+ * follow a log-normal skew (sigma) from SplitMix64(seed); entry g (global,
+ * list-major) has chunk id g and code byte b = (W_{b/8} >> 8(b%8)) & 0xff with
+ * W_i = splitmix64_finalize(seed + 8g + i + 0x9e3779b97f4a7c15). Centroids
+ * [nlist][d] and codewords [nsq][256][d/nsq] are the caller's. No host copy
+ * of the codes is ever made (1B entries = 64 GB at m = 64). */
+int prag_gpu_index_synthetic(uint32_t nlist, uint32_t d, uint32_t nsq, uint64_t ntotal, uint64_t seed, double sigma,
+                             const float* centroids, const float* codewords, int device, prag_gpu_index** out);
+
 void prag_gpu_index_free(prag_gpu_index* index);
 int prag_gpu_index_describe(const prag_gpu_index* index, prag_gpu_index_desc* out);
 /* IvfIndex::nlist, as prag::Retriever::nlist() (pipeline.hpp:207). */

@@ -76,6 +76,8 @@ SYMBOLS = [
     ("prag_gpu_index_load_shard", C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(P)]),
     ("prag_gpu_index_from_host", C.c_int,
      [C.c_uint32, C.c_uint32, C.c_uint32, P, P, P, P, P, C.c_int, C.POINTER(P)]),
+    ("prag_gpu_index_synthetic", C.c_int,
+     [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64, C.c_double, P, P, C.c_int, C.POINTER(P)]),
     ("prag_gpu_index_free", None, [P]),
     ("prag_gpu_index_describe", C.c_int, [P, C.POINTER(IndexDesc)]),
     ("prag_gpu_index_nlist", C.c_uint32, [P]),

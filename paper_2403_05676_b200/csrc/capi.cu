@@ -533,6 +533,10 @@ int search_pass(prag_gpu_index* ix, Workspace* w, const float* dq, uint32_t nq, 
 }
 
 int validate(const prag_gpu_index* ix, uint32_t nprobe, uint32_t k) {
+    if (!ix->dev.plain_codes && (k > 32 || ix->scan_path != 0)) {
+        set_error("search: this index keeps only the lane-skewed code layout (synthetic index): k must be <= 32");
+        return PRAG_GPU_CONFIG;
+    }
     if (k < 1) {  // annindex.hpp:265
         set_error("search: k must be >= 1");
         return PRAG_GPU_CONFIG;
@@ -695,6 +699,118 @@ int prag_gpu_index_load_shard(const char* path, int device, int rank, int world,
     ix->shard_rank = rank;
     ix->shard_world = world;
     return finish_load(ix, h, device, out);
+}
+
+int prag_gpu_index_synthetic(uint32_t nlist, uint32_t d, uint32_t nsq, uint64_t ntotal, uint64_t seed, double sigma,
+                             const float* centroids, const float* codewords, int device, prag_gpu_index** out) {
+    if (!out || !centroids || !codewords) {
+        set_error("null argument");
+        return PRAG_GPU_CONFIG;
+    }
+    *out = nullptr;
+    if ((nsq != 32 && nsq != 64) || d % nsq != 0 || d / nsq > 16 || d % 4 != 0 || nlist == 0) {
+        set_error("synthetic index: needs m in {32, 64}, d % m == 0, d / m <= 16, d % 4 == 0, nlist >= 1");
+        return PRAG_GPU_CONFIG;
+    }
+    PG_TRY(require_device(device));
+    DeviceGuard g(device);
+    auto ix = std::make_unique<prag_gpu_index>();
+    ix->device = device;
+    ix->ntotal_global = ntotal;
+    DeviceIndex& dv = ix->dev;
+    dv.nlist = nlist;
+    dv.d = d;
+    dv.nsq = nsq;
+    dv.sub_dim = d / nsq;
+    dv.plain_codes = false;
+    std::vector<uint64_t> sizes;
+    synth_list_sizes(nlist, ntotal, seed, sigma, sizes);
+    std::vector<uint64_t> loff(size_t(nlist) + 1, 0), poff(size_t(nlist) + 1, 0), soff(size_t(nlist) + 1, 0);
+    std::vector<uint32_t> len(nlist);
+    uint32_t maxlen = 0;
+    for (uint32_t l = 0; l < nlist; ++l) {
+        if (sizes[l] >= (1ull << 32)) {
+            set_error("synthetic index: list exceeds 2^32 entries");
+            return PRAG_GPU_CONFIG;
+        }
+        len[l] = uint32_t(sizes[l]);
+        maxlen = std::max(maxlen, len[l]);
+        loff[l + 1] = loff[l] + sizes[l];
+        poff[l + 1] = poff[l] + (sizes[l] + kListPad - 1) / kListPad * kListPad;
+        soff[l + 1] = soff[l] + (sizes[l] ? (sizes[l] + 31) / 32 + 1 : 0);
+    }
+    if (poff[nlist] >= (1ull << 32)) {
+        set_error("more than 2^32 resident entries on one device; shard the index");
+        return PRAG_GPU_CONFIG;
+    }
+    dv.ntotal = ntotal;
+    dv.npadded = poff[nlist];
+    dv.max_list_len = maxlen;
+    ix->host_list_len = sizes;
+    std::vector<uint64_t> sorted(sizes);
+    std::sort(sorted.begin(), sorted.end(), std::greater<uint64_t>());
+    ix->top_prefix.assign(size_t(nlist) + 1, 0);
+    for (uint32_t i = 0; i < nlist; ++i) ix->top_prefix[i + 1] = ix->top_prefix[i] + sorted[i];
+    uint64_t* acct = &ix->device_bytes;
+    auto fail = [&](int rc) {
+        free_device_index(dv);
+        return rc;
+    };
+    int rc = PRAG_GPU_OK;
+    uint64_t* dloff = nullptr;
+    const size_t cw = size_t(nsq) * 256 * (d / nsq);
+    std::vector<float> t(size_t(nlist) * d);
+    if ((rc = dmalloc(&dv.centroids, size_t(nlist) * d, acct)) ||
+        (rc = dmalloc(&dv.centroids4, size_t(nlist) * d, acct)) || (rc = dmalloc(&dv.codewordsT, cw, acct)) ||
+        (rc = dmalloc(&dv.codewords, cw, acct)) || (rc = dmalloc(&dv.list_off, size_t(nlist) + 1, acct)) ||
+        (rc = dmalloc(&dv.list_len, nlist, acct)) || (rc = dmalloc(&dv.skew_off, size_t(nlist) + 1, acct)) ||
+        (rc = dmalloc(&dv.ids, dv.npadded, acct)) || (rc = dmalloc(&dv.skew_codes, soff[nlist] * 32 * nsq, acct)) ||
+        (rc = dmalloc(&dloff, size_t(nlist) + 1, nullptr)))
+        return fail(rc);
+    for (uint32_t c = 0; c < nlist; ++c)
+        for (uint32_t j = 0; j < d; ++j) t[(size_t(j / 4) * nlist + c) * 4 + (j % 4)] = centroids[size_t(c) * d + j];
+    std::vector<float> wt(cw);
+    const uint32_t sub = d / nsq;
+    for (uint32_t sq = 0; sq < nsq; ++sq)
+        for (uint32_t c = 0; c < 256; ++c)
+            for (uint32_t j = 0; j < sub; ++j) wt[(size_t(sq) * sub + j) * 256 + c] = codewords[(size_t(sq) * 256 + c) * sub + j];
+    cudaError_t e = cudaSuccess;
+    auto cp = [&](void* dst, const void* src, size_t bytes) {
+        if (e == cudaSuccess) e = cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice);
+    };
+    cp(dv.centroids, centroids, size_t(nlist) * d * 4);
+    cp(dv.centroids4, t.data(), t.size() * 4);
+    cp(dv.codewordsT, wt.data(), cw * 4);
+    cp(dv.codewords, codewords, cw * 4);
+    cp(dv.list_off, poff.data(), poff.size() * 8);
+    cp(dv.list_len, len.data(), len.size() * 4);
+    cp(dv.skew_off, soff.data(), soff.size() * 8);
+    cp(dloff, loff.data(), loff.size() * 8);
+    if (e != cudaSuccess) {
+        cudaFree(dloff);
+        set_error(std::string("CUDA error (synthetic index upload): ") + cudaGetErrorString(e));
+        return fail(PRAG_GPU_CUDA);
+    }
+    rc = launch_synth_codes(nsq, dloff, dv.skew_off, nlist, seed, dv.skew_codes, soff[nlist], dv.ids, dv.list_off,
+                            dv.npadded);
+    cudaFree(dloff);
+    if (rc) return fail(rc);
+    dv.code_layout = 1;
+    if (tc_coarse_supported(nlist, d)) {
+        std::vector<float> tc, norms;
+        build_tc_centroids(centroids, nlist, d, tc, norms);
+        if ((rc = dmalloc(&dv.cent_tc, tc.size(), acct)) || (rc = dmalloc(&dv.cent_norm, norms.size(), acct)))
+            return fail(rc);
+        cp(dv.cent_tc, tc.data(), tc.size() * 4);
+        cp(dv.cent_norm, norms.data(), norms.size() * 4);
+        if (e != cudaSuccess) {
+            set_error(std::string("CUDA error (synthetic index upload): ") + cudaGetErrorString(e));
+            return fail(PRAG_GPU_CUDA);
+        }
+        dv.tc_ok = true;
+    }
+    *out = ix.release();
+    return PRAG_GPU_OK;
 }
 
 int prag_gpu_index_from_host(uint32_t nlist, uint32_t d, uint32_t nsq, const float* centroids,

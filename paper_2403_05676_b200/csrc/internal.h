@@ -104,6 +104,7 @@ struct DeviceIndex {
     float* cent_tc = nullptr;     // K1 A operand: centroids pre-split hi/lo in UMMA core-matrix order
     float* cent_norm = nullptr;   // [nlist] ||c||^2
     bool tc_ok = false;           // tensor-core coarse quantizer usable for this shape
+    bool plain_codes = true;      // codes[] present (generic path); false for device-built synthetic indexes
 };
 
 // ------------------------------------------------------------ workspace
@@ -219,6 +220,10 @@ int launch_coarse_tc(const DeviceIndex& ix, const float* queries, uint32_t nq, f
 int launch_select_window(const DeviceIndex& ix, float* partial, const float* queries, uint32_t nq, uint32_t nprobe,
                          uint32_t* probe, float* probe_dist, unsigned long long* win_stat, cudaStream_t s);
 constexpr uint32_t kTcMaxNprobe = 256;
+// device-built synthetic index (synth_index.cu)
+void synth_list_sizes(uint32_t nlist, uint64_t ntotal, uint64_t seed, double sigma, std::vector<uint64_t>& sizes);
+int launch_synth_codes(uint32_t m, const uint64_t* list_off, const uint64_t* skew_off, uint32_t nlist, uint64_t seed,
+                       uint8_t* out, uint64_t ntiles, uint64_t* ids, const uint64_t* pad_off, uint64_t npadded);
 size_t select_smem_bytes();
 
 }  // namespace pg

@@ -133,6 +133,19 @@ class GpuIndex:
                                              _ptr(ids), _ptr(codes), device, C.byref(h)))
         return cls(h)
 
+    @classmethod
+    def synthetic(cls, centroids, codewords, ntotal: int, seed: int = 1, sigma: float = 1.0,
+                  device: int = 0) -> "GpuIndex":
+        """Config-D fixture built in HBM (prag_gpu_index_synthetic; k <= 32)."""
+        centroids = np.ascontiguousarray(centroids, dtype=np.float32)
+        codewords = np.ascontiguousarray(codewords, dtype=np.float32)
+        nlist, d = centroids.shape
+        nsq = codewords.shape[0]
+        h = C.c_void_p()
+        check(lib().prag_gpu_index_synthetic(nlist, d, nsq, ntotal, seed, sigma, _ptr(centroids), _ptr(codewords),
+                                             device, C.byref(h)))
+        return cls(h)
+
     def close(self) -> None:
         if getattr(self, "_h", None):
             lib().prag_gpu_index_free(self._h)
