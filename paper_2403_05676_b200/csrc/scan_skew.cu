@@ -102,20 +102,21 @@ __device__ __forceinline__ uint32_t ord_key(float f) {
 }
 
 // ----------------------------------------------------------- LUT images
-// {r0 - w, r1 - w}: one FADD2 with a scalar-broadcast operand; a subtraction
-// is a single rounding, identical to two __fsub_rn. (Packed MUL/ADD pairs are
-// NOT used anywhere: ptxas contracts mul.rn.f32x2 + add.rn.f32x2 into FFMA2,
-// which would change the reference's rounding.)
-__device__ __forceinline__ void sub2_bcast(float r0, float r1, float w, float& d0, float& d1) {
+// {(r0 - w)^2, (r1 - w)^2}: one FADD2 then one FMUL2, each lane a single
+// rounding (= __fsub_rn then __fmul_rn). The fold's adds stay scalar FADD:
+// ptxas contracts a packed mul followed by a packed add into FFMA2, but never
+// a packed mul into a scalar add.
+__device__ __forceinline__ void subsq2_bcast(float r0, float r1, float w, float& s0, float& s1) {
     unsigned long long out;
-    asm("{.reg .b64 A, B;\n"
+    asm("{.reg .b64 A, B, D;\n"
         " mov.b64 A, {%1, %2};\n"
         " mov.b64 B, {%3, %3};\n"
-        " sub.rn.f32x2 %0, A, B;}"
+        " sub.rn.f32x2 D, A, B;\n"
+        " mul.rn.f32x2 %0, D, D;}"
         : "=l"(out)
         : "f"(r0), "f"(r1), "f"(w));
-    d0 = __uint_as_float(uint32_t(out));
-    d1 = __uint_as_float(uint32_t(out >> 32));
+    s0 = __uint_as_float(uint32_t(out));
+    s1 = __uint_as_float(uint32_t(out >> 32));
 }
 
 // SMEM image of one (query, list) ADC table, as K3 gathers it: R = m/32
@@ -326,13 +327,13 @@ __global__ void __launch_bounds__(256, 2) lut_image_kernel(const float* __restri
             if (j < int(sub)) {
                 const float4 ra = *reinterpret_cast<const float4*>(rr + j * P);
                 const float4 rb = *reinterpret_cast<const float4*>(rr + j * P + 4);
-                float dd[P];
-                sub2_bcast(ra.x, ra.y, w[j], dd[0], dd[1]);
-                sub2_bcast(ra.z, ra.w, w[j], dd[2], dd[3]);
-                sub2_bcast(rb.x, rb.y, w[j], dd[4], dd[5]);
-                sub2_bcast(rb.z, rb.w, w[j], dd[6], dd[7]);
+                float sq[P];  // fl(fl(r - w)^2), two pairs per FADD2 / FMUL2
+                subsq2_bcast(ra.x, ra.y, w[j], sq[0], sq[1]);
+                subsq2_bcast(ra.z, ra.w, w[j], sq[2], sq[3]);
+                subsq2_bcast(rb.x, rb.y, w[j], sq[4], sq[5]);
+                subsq2_bcast(rb.z, rb.w, w[j], sq[6], sq[7]);
 #pragma unroll
-                for (int p = 0; p < P; ++p) acc[p] = __fadd_rn(acc[p], __fmul_rn(dd[p], dd[p]));
+                for (int p = 0; p < P; ++p) acc[p] = __fadd_rn(acc[p], sq[p]);
             }
         }
 #pragma unroll
