@@ -123,6 +123,32 @@ int prag_gpu_index_from_host(uint32_t nlist, uint32_t d, uint32_t nsq, const flo
 int prag_gpu_index_synthetic(uint32_t nlist, uint32_t d, uint32_t nsq, uint64_t ntotal, uint64_t seed, double sigma,
                              const float* centroids, const float* codewords, int device, prag_gpu_index** out);
 
+/* ---------------------------------------------------------------- build */
+/* prag::TrainParams (annindex.hpp:152-160); reference defaults:
+ * {nlist 64, n_subquantizers 0 (-> d/4), seed 7, kmeans_iterations 25,
+ *  train_sample_cap 32768}. */
+typedef struct prag_gpu_train_params {
+    uint32_t nlist;
+    uint32_t n_subquantizers;
+    uint64_t seed;
+    int32_t kmeans_iterations;
+    int32_t reserved;
+    uint64_t train_sample_cap;
+} prag_gpu_train_params;
+
+/* Replaces prag::train_index (annindex.hpp:164-241) on the device, bit-exact:
+ * the same sample, k-means++ seeds, Lloyd iterations, IVF assignment, PQ
+ * codebooks and codes as the reference's scalar code. vectors: n x d fp32
+ * row-major (host or device). Outputs (host or device, each independently) in
+ * the flattened IvfIndex/PqCodebook layout prag_gpu_index_from_host takes:
+ * centroids[nlist][d], codewords[nsq][256][d/nsq] (unused tail codes zero),
+ * list_off[nlist+1], ids[n] and codes[n][nsq] list-major, each list in vector
+ * order (ids are vector indices). Errors: the reference's ConfigError texts;
+ * n must be < 2^32. */
+int prag_gpu_train_index(const float* vectors, uint64_t n, uint32_t d, const prag_gpu_train_params* params,
+                         int device, float* centroids, float* codewords, uint64_t* list_off, uint64_t* ids,
+                         uint8_t* codes);
+
 void prag_gpu_index_free(prag_gpu_index* index);
 int prag_gpu_index_describe(const prag_gpu_index* index, prag_gpu_index_desc* out);
 /* IvfIndex::nlist, as prag::Retriever::nlist() (pipeline.hpp:207). */

@@ -488,3 +488,194 @@ uint32_t ora_select_nprobe(double slope_s, double intercept_s, double budget_s, 
     double f = floor(max_n + 1e-9);
     return (uint32_t)(f > 1.0 ? f : 1.0);
 }
+
+/* ------------------------------------------------------------------ build
+ * prag::train_index (annindex.hpp:164-241) and its kmeans
+ * (annindex.hpp:62-130), restated over flat arrays. Outputs the flattened
+ * IvfIndex/PqCodebook (list-major, each list in vector order). */
+
+/* annindex.hpp:64-130: k-means++ seeding then Lloyd; pts[i] points at a row
+ * of `dim` floats; centroids out [k][dim]. */
+static int ora_kmeans(const float* const* pts, uint64_t n, uint32_t dim, uint32_t k, uint64_t seed, int iters,
+                      float* cent) {
+    if (n < k) {
+        set_err("kmeans: fewer points than clusters");
+        return ORA_CONFIG;
+    }
+    uint64_t st = seed;
+    float* md = malloc(n * sizeof(float));
+    for (uint64_t i = 0; i < n; ++i) md[i] = 3.402823466e+38f; /* FLT_MAX */
+    uint64_t first = ora_splitmix_next(&st) % n;
+    memcpy(cent, pts[first], dim * sizeof(float));
+    for (uint32_t t = 1; t < k; ++t) {
+        const float* last = cent + (size_t)(t - 1) * dim;
+        double total = 0.0;
+        for (uint64_t i = 0; i < n; ++i) {
+            float dsq = ora_squared_l2(pts[i], last, dim);
+            if (dsq < md[i]) md[i] = dsq;
+            total += md[i];
+        }
+        uint64_t pick = 0;
+        if (total > 0.0) {
+            double r = splitmix_double(&st) * total;
+            double acc = 0.0;
+            for (uint64_t i = 0; i < n; ++i) {
+                acc += md[i];
+                if (acc >= r) {
+                    pick = i;
+                    break;
+                }
+            }
+        } else {
+            pick = ora_splitmix_next(&st) % n;
+        }
+        memcpy(cent + (size_t)t * dim, pts[pick], dim * sizeof(float));
+    }
+    free(md);
+    uint32_t* asg = calloc(n, sizeof(uint32_t));
+    float* adist = calloc(n, sizeof(float));
+    double* sums = malloc((size_t)k * dim * sizeof(double));
+    uint64_t* cnt = malloc((size_t)k * sizeof(uint64_t));
+    for (int it = 0; it < iters; ++it) {
+        for (uint64_t i = 0; i < n; ++i) {
+            float best = 3.402823466e+38f;
+            uint32_t bc = 0;
+            for (uint32_t c = 0; c < k; ++c) {
+                float dsq = ora_squared_l2(pts[i], cent + (size_t)c * dim, dim);
+                if (dsq < best) {
+                    best = dsq;
+                    bc = c;
+                }
+            }
+            asg[i] = bc;
+            adist[i] = best;
+        }
+        memset(sums, 0, (size_t)k * dim * sizeof(double));
+        memset(cnt, 0, (size_t)k * sizeof(uint64_t));
+        for (uint64_t i = 0; i < n; ++i) {
+            ++cnt[asg[i]];
+            double* s = sums + (size_t)asg[i] * dim;
+            for (uint32_t j = 0; j < dim; ++j) s[j] += pts[i][j];
+        }
+        for (uint32_t c = 0; c < k; ++c) {
+            float* dst = cent + (size_t)c * dim;
+            if (cnt[c] == 0) {
+                uint64_t far = 0;
+                float far_d = -1.0f;
+                for (uint64_t i = 0; i < n; ++i)
+                    if (adist[i] > far_d) {
+                        far_d = adist[i];
+                        far = i;
+                    }
+                memcpy(dst, pts[far], dim * sizeof(float));
+                adist[far] = 0.0f;
+            } else {
+                for (uint32_t j = 0; j < dim; ++j) dst[j] = (float)(sums[(size_t)c * dim + j] / (double)cnt[c]);
+            }
+        }
+    }
+    free(asg);
+    free(adist);
+    free(sums);
+    free(cnt);
+    return ORA_OK;
+}
+
+int ora_train_index(const float* vecs, uint64_t n, uint32_t d, uint32_t nlist, uint32_t n_subquantizers,
+                    uint64_t seed, int iters, uint64_t sample_cap, float* centroids, float* codewords,
+                    uint64_t* list_off, uint64_t* ids, uint8_t* codes) {
+    if (n == 0) {
+        set_err("train_index: empty embedding set");
+        return ORA_CONFIG;
+    }
+    if (n < nlist) {
+        set_err("train_index: nlist exceeds number of vectors");
+        return ORA_CONFIG;
+    }
+    uint32_t nsq = n_subquantizers ? n_subquantizers : (d / 4 > 1 ? d / 4 : 1);
+    if (d % nsq != 0) {
+        set_err("train_index: d not divisible by n_subquantizers");
+        return ORA_CONFIG;
+    }
+    uint32_t sub = d / nsq;
+    /* training_sample (annindex.hpp:134-145) */
+    uint64_t* idx = malloc(n * sizeof(uint64_t));
+    for (uint64_t i = 0; i < n; ++i) idx[i] = i;
+    uint64_t ns = n;
+    if (n > sample_cap) {
+        uint64_t st = seed ^ 0x5a5a;
+        for (uint64_t i = 0; i < sample_cap; ++i) {
+            uint64_t j = i + ora_splitmix_next(&st) % (n - i);
+            uint64_t t = idx[i];
+            idx[i] = idx[j];
+            idx[j] = t;
+        }
+        ns = sample_cap;
+    }
+    const float** sp = malloc((ns ? ns : 1) * sizeof(float*));
+    for (uint64_t i = 0; i < ns; ++i) sp[i] = vecs + idx[i] * d;
+    int rc = ora_kmeans(sp, ns, d, nlist, seed, iters, centroids);
+    if (rc) {
+        free(idx);
+        free(sp);
+        return rc;
+    }
+    /* assignment + residuals (annindex.hpp:195-202) */
+    uint32_t* asg = malloc(n * sizeof(uint32_t));
+    float* res = malloc(n * d * sizeof(float));
+    for (uint64_t i = 0; i < n; ++i) {
+        const float* v = vecs + i * d;
+        float best = 3.402823466e+38f;
+        uint32_t bc = 0;
+        for (uint32_t c = 0; c < nlist; ++c) {
+            float dsq = ora_squared_l2(v, centroids + (size_t)c * d, d);
+            if (dsq < best) {
+                best = dsq;
+                bc = c;
+            }
+        }
+        asg[i] = bc;
+        for (uint32_t j = 0; j < d; ++j) res[i * d + j] = v[j] - centroids[(size_t)bc * d + j];
+    }
+    /* PQ codebooks (annindex.hpp:209-218) */
+    uint64_t pq = n < 256 ? n : 256;
+    uint64_t clusters = pq < ns ? pq : ns;
+    memset(codewords, 0, (size_t)nsq * 256 * sub * sizeof(float));
+    for (uint32_t q = 0; q < nsq; ++q) {
+        for (uint64_t i = 0; i < ns; ++i) sp[i] = res + idx[i] * d + (size_t)q * sub;
+        rc = ora_kmeans(sp, ns, sub, (uint32_t)clusters, ora_hash_combine(seed, q + 1), iters,
+                        codewords + (size_t)q * 256 * sub);
+        if (rc) break;
+    }
+    if (!rc) {
+        /* postings in vector order (annindex.hpp:222-238) */
+        memset(list_off, 0, (nlist + 1) * sizeof(uint64_t));
+        for (uint64_t i = 0; i < n; ++i) ++list_off[asg[i] + 1];
+        for (uint32_t l = 0; l < nlist; ++l) list_off[l + 1] += list_off[l];
+        uint64_t* fill = malloc((nlist + 1) * sizeof(uint64_t));
+        memcpy(fill, list_off, (nlist + 1) * sizeof(uint64_t));
+        for (uint64_t i = 0; i < n; ++i) {
+            uint64_t at = fill[asg[i]]++;
+            ids[at] = i;
+            for (uint32_t q = 0; q < nsq; ++q) {
+                const float* s = res + i * d + (size_t)q * sub;
+                float best = 3.402823466e+38f;
+                uint32_t bc = 0;
+                for (uint32_t c = 0; c < pq; ++c) {
+                    float dsq = ora_squared_l2(s, codewords + ((size_t)q * 256 + c) * sub, sub);
+                    if (dsq < best) {
+                        best = dsq;
+                        bc = c;
+                    }
+                }
+                codes[at * nsq + q] = (uint8_t)bc;
+            }
+        }
+        free(fill);
+    }
+    free(idx);
+    free(sp);
+    free(asg);
+    free(res);
+    return rc;
+}

@@ -10,7 +10,7 @@
 // tool does: perfmodel_main.cpp:49). No reference source is copied here.
 //
 // Commands:
-//   train   <vectors.f32> <n> <d> <nlist> <nsq> <seed> <out.pragix>
+//   train   <vectors.f32> <n> <d> <nlist> <nsq> <seed> <out.pragix> [iterations] [sample_cap]
 //   search  <index> <queries.f32> <nq> <nprobe> <k> <out.bin>
 //   bench   <index> <queries.f32> <nq> <nprobe> <k> <threads> <reps> <warmups> [max_seconds]
 //   calibrate <index> <queries.f32> <nq> <k> <grid_csv> <repeats>
@@ -80,13 +80,15 @@ int main(int argc, char** argv) {
     }
     std::string cmd = argv[1];
     try {
-        if (cmd == "train" && argc == 9) {
+        if (cmd == "train" && argc >= 9 && argc <= 11) {
             std::size_t n = std::stoull(argv[3]);
             std::uint32_t d = std::stoul(argv[4]);
             prag::TrainParams params;
             params.nlist = std::stoul(argv[5]);
             params.n_subquantizers = std::stoul(argv[6]);
             params.seed = std::stoull(argv[7]);
+            if (argc >= 10) params.kmeans_iterations = std::stoi(argv[9]);
+            if (argc >= 11) params.train_sample_cap = std::stoull(argv[10]);
             auto vecs = rows(read_f32(argv[2], n * d), n, d);
             auto [index, codebook] = prag::train_index(vecs, params);
             prag::store_index(index, codebook, argv[8]);

@@ -64,6 +64,11 @@ class Timings(C.Structure):
                 ("scanned_bytes", C.c_uint64), ("work_items", C.c_uint64), ("coarse_window", C.c_uint64)]
 
 
+class TrainParamsC(C.Structure):
+    _fields_ = [("nlist", C.c_uint32), ("n_subquantizers", C.c_uint32), ("seed", C.c_uint64),
+                ("kmeans_iterations", C.c_int32), ("reserved", C.c_int32), ("train_sample_cap", C.c_uint64)]
+
+
 MEASURE_FN = C.CFUNCTYPE(C.c_double, C.c_uint32, C.c_void_p)
 
 # (name, restype, argtypes) for every symbol include/prag_gpu.h declares.
@@ -78,6 +83,8 @@ SYMBOLS = [
      [C.c_uint32, C.c_uint32, C.c_uint32, P, P, P, P, P, C.c_int, C.POINTER(P)]),
     ("prag_gpu_index_synthetic", C.c_int,
      [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64, C.c_double, P, P, C.c_int, C.POINTER(P)]),
+    ("prag_gpu_train_index", C.c_int,
+     [P, C.c_uint64, C.c_uint32, C.POINTER(TrainParamsC), C.c_int, P, P, P, P, P]),
     ("prag_gpu_index_free", None, [P]),
     ("prag_gpu_index_describe", C.c_int, [P, C.POINTER(IndexDesc)]),
     ("prag_gpu_index_nlist", C.c_uint32, [P]),

@@ -48,6 +48,36 @@ def write_pragix(path, centroids, codewords, list_off, ids, codes) -> None:
     os.replace(tmp, path)
 
 
+def read_pragix(path):
+    """PRAGIX01 reader (annindex.hpp:361-411) into flat list-major arrays:
+    (centroids [nlist][d], codewords [nsq][256][d/nsq], list_off [nlist+1],
+    ids [n], codes [n][nsq])."""
+    buf = open(path, "rb").read()
+    if buf[:8] != b"PRAGIX01":
+        raise ValueError("bad magic")
+    _ver, nlist, d, nsq = struct.unpack_from("<IIII", buf, 8)
+    at = 24
+    cents = np.frombuffer(buf, np.float32, nlist * d, at).reshape(nlist, d)
+    at += 4 * nlist * d
+    sub = d // nsq
+    words = np.frombuffer(buf, np.float32, nsq * 256 * sub, at).reshape(nsq, 256, sub)
+    at += 4 * nsq * 256 * sub
+    rec = np.dtype([("id", "<u8"), ("code", "u1", (nsq,))])
+    off = [0]
+    ids, codes = [], []
+    for _ in range(nlist):
+        (ln,) = struct.unpack_from("<Q", buf, at)
+        at += 8
+        r = np.frombuffer(buf, rec, ln, at)
+        at += ln * rec.itemsize
+        ids.append(r["id"])
+        codes.append(r["code"])
+        off.append(off[-1] + ln)
+    return (cents.copy(), words.copy(), np.array(off, dtype=np.uint64),
+            np.concatenate(ids).astype(np.uint64) if ids else np.zeros(0, np.uint64),
+            np.concatenate(codes).reshape(-1, nsq) if codes else np.zeros((0, nsq), np.uint8))
+
+
 def _chunk_rows(seed: int, chunk: int, rows: int, d: int, device) -> torch.Tensor:
     g = torch.Generator(device=device)
     g.manual_seed((seed * 1000003 + chunk) & 0x7FFFFFFFFFFFFFFF)

@@ -15,7 +15,7 @@ from typing import Callable, Iterable, List, Optional, Sequence
 
 import numpy as np
 
-from ._lib import (ConfigError, FormatError, IndexDesc, MEASURE_FN, PerfModelC, Timings, check, lib)
+from ._lib import (ConfigError, FormatError, IndexDesc, MEASURE_FN, PerfModelC, Timings, TrainParamsC, check, lib)
 
 try:  # torch is plumbing only (device buffers / streams); optional here
     import torch
@@ -258,6 +258,66 @@ class GpuChunkEmbedder:
             self.close()
         except Exception:
             pass
+
+
+# ------------------------------------------------------------------ build
+@dataclass
+class TrainParams:
+    """annindex.hpp:152-160 (same defaults)."""
+    nlist: int = 64
+    n_subquantizers: int = 0          # 0 -> d / 4
+    seed: int = 7
+    kmeans_iterations: int = 25
+    train_sample_cap: int = 32768
+
+
+@dataclass
+class TrainedIndex:
+    """prag::train_index's {IvfIndex, PqCodebook} in flattened list-major form:
+    centroids [nlist][d], codewords [nsq][256][d/nsq], list_off [nlist+1],
+    ids [n] (vector indices, each list in vector order), codes [n][nsq]."""
+    centroids: np.ndarray
+    codewords: np.ndarray
+    list_off: np.ndarray
+    ids: np.ndarray
+    codes: np.ndarray
+
+    def to_gpu(self, device: int = 0) -> "GpuIndex":
+        return GpuIndex.from_host(self.centroids, self.codewords, self.list_off, self.ids, self.codes, device)
+
+    def write_pragix(self, path: str) -> None:
+        """prag::store_index (annindex.hpp:335-359)."""
+        from .fixtures import write_pragix
+        write_pragix(path, self.centroids, self.codewords, self.list_off, self.ids, self.codes)
+
+
+def train_index(vectors, params: Optional[TrainParams] = None, device: int = 0) -> TrainedIndex:
+    """prag::train_index (annindex.hpp:164-241) on the device, bit-exact
+    (prag_gpu_train_index). `vectors`: n x d fp32 (numpy or a CUDA tensor)."""
+    p = params or TrainParams()
+    if torch is not None and isinstance(vectors, torch.Tensor):
+        if vectors.dtype != torch.float32 or vectors.dim() != 2:
+            raise ConfigError("train_index: vectors must be a 2-D float32 tensor")
+        vectors = vectors.contiguous()
+        n, d = vectors.shape
+    else:
+        vectors = np.ascontiguousarray(vectors, dtype=np.float32)
+        if vectors.ndim != 2:
+            raise ConfigError("train_index: vectors must be n x d")
+        n, d = vectors.shape
+    nsq = p.n_subquantizers if p.n_subquantizers else max(1, d // 4)
+    nlist = p.nlist
+    ok = n > 0 and d > 0 and 0 < nlist <= n and d % nsq == 0
+    shp = (max(nlist, 1), max(d, 1))
+    cents = np.zeros(shp, dtype=np.float32)
+    words = np.zeros((nsq, 256, max(d // nsq, 1)) if ok else (1,), dtype=np.float32)
+    off = np.zeros(max(nlist, 0) + 1, dtype=np.uint64)
+    ids = np.zeros(max(n, 1), dtype=np.uint64)
+    codes = np.zeros((max(n, 1), nsq), dtype=np.uint8)
+    c = TrainParamsC(nlist, p.n_subquantizers, p.seed, p.kmeans_iterations, 0, p.train_sample_cap)
+    check(lib().prag_gpu_train_index(_ptr(vectors) if n else None, n, d, C.byref(c), device, _ptr(cents),
+                                     _ptr(words), _ptr(off), _ptr(ids), _ptr(codes)))
+    return TrainedIndex(cents, words, off, ids[:n], codes[:n])
 
 
 def load_index(path: str, device: int = 0) -> GpuIndex:

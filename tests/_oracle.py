@@ -54,6 +54,8 @@ def lib() -> C.CDLL:
         L.ora_hash_combine.argtypes = [C.c_uint64, C.c_uint64]
         L.ora_hash_combine.restype = C.c_uint64
         L.ora_random_vectors.argtypes = [C.c_uint64, C.c_uint64, C.c_uint32, P]
+        L.ora_train_index.argtypes = [P, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, C.c_int,
+                                      C.c_uint64, P, P, P, P, P]
         _lib = L
     return _lib
 
@@ -89,6 +91,24 @@ def random_vectors(n: int, d: int, seed: int) -> np.ndarray:
     out = np.empty((n, d), dtype=np.float32)
     lib().ora_random_vectors(seed, n, d, _p(out))
     return out
+
+
+def train_index(v: np.ndarray, nlist: int, nsq: int = 0, seed: int = 7, iters: int = 25, cap: int = 32768):
+    """annindex.hpp:164-241 via the C restatement: (centroids, codewords,
+    list_off, ids, codes), flattened list-major."""
+    v = np.ascontiguousarray(v, dtype=np.float32)
+    n, d = v.shape
+    m = nsq if nsq else max(1, d // 4)
+    cents = np.zeros((max(nlist, 1), d), np.float32)
+    words = np.zeros((m, 256, max(d // m, 1)), np.float32)
+    off = np.zeros(nlist + 1, np.uint64)
+    ids = np.zeros(max(n, 1), np.uint64)
+    codes = np.zeros((max(n, 1), m), np.uint8)
+    rc = lib().ora_train_index(_p(v), n, d, nlist, nsq, seed, iters, cap, _p(cents), _p(words), _p(off), _p(ids),
+                               _p(codes))
+    if rc:
+        raise OracleError(rc, lib().ora_last_error().decode())
+    return cents, words, off, ids[:n], codes[:n]
 
 
 def noisy_queries(base: np.ndarray, nq: int, seed: int, scale: float) -> np.ndarray:
