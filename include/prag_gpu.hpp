@@ -211,6 +211,55 @@ inline std::uint32_t select_nprobe(const RetrievalPerfModel& model, double budge
 }
 
 #ifdef PRAG_GPU_HAVE_REFERENCE
+// Drop-in for prag::train_index (annindex.hpp:164-241): the identical
+// {IvfIndex, PqCodebook} (same sample, seeds, Lloyd iterations, lists in
+// vector order, codebooks, codes), computed on `device`.
+inline std::pair<::prag::IvfIndex, ::prag::PqCodebook> train_index(
+    const std::vector<std::vector<float>>& embeddings, ::prag::TrainParams params, int device = 0) {
+    const std::uint64_t n = embeddings.size();
+    const std::uint32_t d = n ? static_cast<std::uint32_t>(embeddings[0].size()) : 0;
+    std::vector<float> flat(n * d);
+    for (std::uint64_t i = 0; i < n; ++i) {
+        if (embeddings[i].size() != d) throw ConfigError("train_index: ragged embedding set");
+        std::copy(embeddings[i].begin(), embeddings[i].end(), flat.begin() + i * d);
+    }
+    const std::uint32_t nsq = params.n_subquantizers ? params.n_subquantizers : std::max(1u, d / 4);
+    const std::uint32_t sub = nsq && d % nsq == 0 ? d / nsq : 1;
+    prag_gpu_train_params p{params.nlist, params.n_subquantizers, params.seed, params.kmeans_iterations, 0,
+                            static_cast<std::uint64_t>(params.train_sample_cap)};
+    std::vector<float> cent(std::size_t(params.nlist) * d + 1), words(std::size_t(nsq) * 256 * sub + 1);
+    std::vector<std::uint64_t> off(std::size_t(params.nlist) + 1), ids(n + 1);
+    std::vector<std::uint8_t> codes(n * nsq + 1);
+    check(prag_gpu_train_index(n ? flat.data() : nullptr, n, d, &p, device, cent.data(), words.data(), off.data(),
+                               ids.data(), codes.data()));
+    ::prag::IvfIndex index;
+    index.nlist = params.nlist;
+    index.d = d;
+    index.centroids.resize(params.nlist);
+    index.postings.resize(params.nlist);
+    for (std::uint32_t l = 0; l < params.nlist; ++l) {
+        index.centroids[l].assign(cent.begin() + std::size_t(l) * d, cent.begin() + std::size_t(l + 1) * d);
+        auto& list = index.postings[l];
+        list.resize(off[l + 1] - off[l]);
+        for (std::uint64_t e = off[l]; e < off[l + 1]; ++e) {
+            auto& pe = list[e - off[l]];
+            pe.chunk_id = ids[e];
+            pe.code.assign(codes.begin() + e * nsq, codes.begin() + (e + 1) * nsq);
+        }
+    }
+    ::prag::PqCodebook cb;
+    cb.n_subquantizers = nsq;
+    cb.sub_dim = sub;
+    cb.codewords.assign(nsq, std::vector<std::vector<float>>(256, std::vector<float>(sub)));
+    for (std::uint32_t s = 0; s < nsq; ++s)
+        for (std::uint32_t c = 0; c < 256; ++c)
+            std::copy(words.begin() + (std::size_t(s) * 256 + c) * sub,
+                      words.begin() + (std::size_t(s) * 256 + c + 1) * sub, cb.codewords[s][c].begin());
+    return {std::move(index), std::move(cb)};
+}
+#endif
+
+#ifdef PRAG_GPU_HAVE_REFERENCE
 // Drop-in for prag::LocalRetriever (pipeline.hpp:213-249): same constructor
 // arguments, same nprobe directive handling (:224-226), same record
 // resolution (:232-235). The query embedding (:227) and the search run on the

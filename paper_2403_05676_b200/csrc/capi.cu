@@ -348,8 +348,7 @@ int search_pass_skew(prag_gpu_index* ix, Workspace* w, const float* dq, uint32_t
     const uint64_t max_tiles_q = (ix->top_prefix[nprobe] + 31) / 32 + nprobe;
     const uint32_t IT = skew_item_tiles(uint64_t(nq) * max_tiles_q, uint32_t(grid));
     const uint64_t item_cap = uint64_t(nq) * (nprobe + max_tiles_q / IT + 1) + 1;
-    const uint32_t warps = skew_warps(d.nsq);
-    const uint64_t pool_cap = item_cap * warps * k;
+    const uint64_t pool_cap = item_cap * k;  // k entries per work item
     const uint32_t pw_p = pow2_at_least(nprobe);
     const uint32_t pw_f = pow2_at_least(std::max<uint64_t>(1, std::min<uint64_t>(k, pool_cap)));
     const uint64_t img_floats = uint64_t(nq) * nprobe * (skew_lut_bytes(d.nsq) / 4);  // K3 LUT images
@@ -365,7 +364,7 @@ int search_pass_skew(prag_gpu_index* ix, Workspace* w, const float* dq, uint32_t
         c.take<uint32_t>(2);
         c.take<uint32_t>(size_t(nq) + 1);
         c.take<uint32_t>(nq);
-        c.take<uint32_t>(nq);
+        c.take<uint32_t>(size_t(nq) * nprobe);
         c.take<uint32_t>(pool_cap);
         c.take<uint64_t>(pool_cap);
         c.take<uint32_t>(size_t(nq) * pw_f);
@@ -384,7 +383,7 @@ int search_pass_skew(prag_gpu_index* ix, Workspace* w, const float* dq, uint32_t
     uint32_t* ctr = c.take<uint32_t>(2);
     uint32_t* q_item_off = c.take<uint32_t>(size_t(nq) + 1);
     uint32_t* gthr = c.take<uint32_t>(nq);
-    uint32_t* pool_cnt = c.take<uint32_t>(nq);
+    uint32_t* pair_off = c.take<uint32_t>(size_t(nq) * nprobe);
     uint32_t* pool_key = c.take<uint32_t>(pool_cap);
     uint64_t* pool_id = c.take<uint64_t>(pool_cap);
     uint32_t* fkey = c.take<uint32_t>(size_t(nq) * pw_f);
@@ -396,12 +395,11 @@ int search_pass_skew(prag_gpu_index* ix, Workspace* w, const float* dq, uint32_t
     PG_TRY(run_coarse(ix, dq, nq, nprobe, coarse, probe, probe_dist, pkey, ptie, s, prof ? w : nullptr));
     if (prof) cudaEventRecord(w->ev[2], s);
     PG_TRY(launch_lut_images(d, dq, probe, nq, nprobe, images, IT, o_scanned, items, ctr, ctr + 1, q_item_off, gthr,
-                             pool_cnt, item_cap, s));
+                             pair_off, item_cap, s));
     if (prof) cudaEventRecord(w->ev[3], s);
-    PG_TRY(launch_scan_skew(d, items, ctr, ctr + 1, probe, images, nprobe, k, gthr, q_item_off, pool_cnt, pool_key,
-                            pool_id, grid, s));
+    PG_TRY(launch_scan_skew(d, items, ctr, ctr + 1, probe, images, nprobe, k, gthr, pool_key, pool_id, grid, s));
     if (prof) cudaEventRecord(w->ev[4], s);
-    PG_TRY(launch_select_pool(pool_key, pool_id, pool_cnt, q_item_off, warps, nq, k, o_ids, o_dist, o_count, fkey,
+    PG_TRY(launch_select_pool(pool_key, pool_id, o_scanned, q_item_off, gthr, nq, k, o_ids, o_dist, o_count, fkey,
                               ftie, pw_f, s));
     if (prof) {
         cudaEventRecord(w->ev[5], s);

@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(kWinThreads) select_window_kernel(
     unsigned long long* __restrict__ win_stat) {
     extern __shared__ __align__(1024) unsigned char sm[];
     uint32_t* hist = reinterpret_cast<uint32_t*>(sm);          // [256]
-    uint32_t* misc = hist + 256;                               // [8]: [1] rank, [2..3] selected key, [4] count
+    uint32_t* misc = hist + 256;                               // [8]: [1] rank, [2..3] selected key, [4] count, [5..6] two-level U
     uint32_t* win = misc + 8;                                  // [kWinCap] list ids
     float* wd = reinterpret_cast<float*>(win + kWinCap);       // [kWinCap] exact distances
     float* sq = wd + kWinCap;                                  // [d] the query
@@ -386,8 +386,9 @@ __global__ void __launch_bounds__(kWinThreads) select_window_kernel(
         const uint32_t c = i * kWinThreads + tid;
         cnv[i] = c < nlist ? __ldg(cent_norm + c) : 0.0f;
     }
-    pdl_wait();
-    // ||q||^2 (any order: it only enters the approximate A and the bound E)
+    // ||q||^2 (any order: it only enters the approximate A and the bound E).
+    // The queries were written before K1 started, so they are read before
+    // waiting on K1.
     float part = 0.0f;
     for (uint32_t j = tid; j < d; j += kWinThreads) {
         const float x = queries[size_t(q) * d + j];
@@ -397,20 +398,30 @@ __global__ void __launch_bounds__(kWinThreads) select_window_kernel(
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
     if ((tid & 31) == 0) red[tid >> 5] = part;
-    // q.c: sum of K1's slices; each slice's VPT loads are issued together
+    pdl_wait();
+    // q.c: sum of K1's slices in slice order; up to ZB slices' loads are
+    // issued together before the first add
     float dot[VPT];
 #pragma unroll
     for (uint32_t i = 0; i < VPT; ++i) dot[i] = 0.0f;
-    for (uint32_t z = 0; z < nslices; ++z) {
-        float pv[VPT];
-        const float* pz = partial + (size_t(z) * nq + q) * nlist;
+    constexpr uint32_t ZB = VPT <= 8 ? 4 : 1;  // slices in flight (register budget)
+    for (uint32_t z0 = 0; z0 < nslices; z0 += ZB) {
+        float pv[ZB][VPT];
 #pragma unroll
-        for (uint32_t i = 0; i < VPT; ++i) {
-            const uint32_t c = i * kWinThreads + tid;
-            pv[i] = c < nlist ? pz[c] : 0.0f;
+        for (uint32_t zz = 0; zz < ZB; ++zz) {
+            const float* pz = partial + (size_t(z0 + zz) * nq + q) * nlist;
+#pragma unroll
+            for (uint32_t i = 0; i < VPT; ++i) {
+                const uint32_t c = i * kWinThreads + tid;
+                pv[zz][i] = (z0 + zz < nslices && c < nlist) ? pz[c] : 0.0f;
+            }
         }
 #pragma unroll
-        for (uint32_t i = 0; i < VPT; ++i) dot[i] += pv[i];
+        for (uint32_t zz = 0; zz < ZB; ++zz)
+            if (z0 + zz < nslices) {
+#pragma unroll
+                for (uint32_t i = 0; i < VPT; ++i) dot[i] += pv[zz][i];
+            }
     }
     __syncthreads();
     float qn = 0.0f;
@@ -432,7 +443,54 @@ __global__ void __launch_bounds__(kWinThreads) select_window_kernel(
         }
     }
     float* upq = partial + size_t(q) * nlist;  // slice-0 row: scratch for the exact fallback
-    const uint32_t ukey = block_select_kth<VPT>(key, nlist, nprobe, hist, misc);  // U
+    // U = the nprobe-th smallest key. Two levels when every thread holds
+    // several keys: the nprobe-th smallest of the 512 per-thread minima is an
+    // upper bound U' >= U (a subset's order statistic), so the keys <= U'
+    // (about nprobe of them) contain the nprobe smallest; U is ranked among
+    // those by counting. Falls back to the 4-pass radix select over all keys
+    // when that candidate set is large.
+    uint32_t ukey;
+    if (VPT > 1) {
+        uint32_t kmin[1] = {key[0]};
+#pragma unroll
+        for (uint32_t i = 1; i < VPT; ++i) kmin[0] = min(kmin[0], key[i]);
+        const uint32_t ub = block_select_kth<1>(kmin, kWinThreads, nprobe, hist, misc);
+        uint32_t* cand = reinterpret_cast<uint32_t*>(wd);  // scratch until the window is rescored
+        if (tid == 0) misc[5] = 0;
+        __syncthreads();
+#pragma unroll
+        for (uint32_t i = 0; i < VPT; ++i) {
+            const bool in = key[i] <= ub;
+            const unsigned bal = __ballot_sync(0xffffffffu, in);
+            uint32_t base = 0;
+            if ((tid & 31) == 0 && bal) base = atomicAdd(misc + 5, __popc(bal));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (in) {
+                const uint32_t pos = base + __popc(bal & ((1u << (tid & 31)) - 1));
+                if (pos < kWinCap) cand[pos] = key[i];
+            }
+        }
+        __syncthreads();
+        const uint32_t nc = misc[5];
+        if (nc <= kWinCap) {
+            for (uint32_t i = tid; i < nc; i += kWinThreads) {
+                const uint32_t ki = cand[i];
+                uint32_t less = 0, eq = 0;
+                for (uint32_t j = 0; j < nc; ++j) {
+                    const uint32_t kj = cand[j];
+                    less += kj < ki;
+                    eq += kj == ki;
+                }
+                if (less < nprobe && nprobe <= less + eq) misc[6] = ki;
+            }
+            __syncthreads();
+            ukey = misc[6];
+        } else {
+            ukey = block_select_kth<VPT>(key, nlist, nprobe, hist, misc);
+        }
+    } else {
+        ukey = block_select_kth<VPT>(key, nlist, nprobe, hist, misc);
+    }
     // window: lists whose lower bound A - E does not exceed U
     // lov[] is in registers: collect through a per-thread test (c = i*512 + tid)
     uint32_t W;

@@ -194,13 +194,14 @@ uint32_t scan_chunk();
 int launch_lut_images(const DeviceIndex& ix, const float* queries, const uint32_t* probe, uint32_t nq,
                       uint32_t nprobe, float* luts, uint32_t it_tiles, uint64_t* scanned, uint4* items,
                       uint32_t* num_items, uint32_t* cursor, uint32_t* q_item_off, uint32_t* gthr,
-                      uint32_t* pool_cnt, uint64_t item_cap, cudaStream_t s);
+                      uint32_t* pair_off, uint64_t item_cap, cudaStream_t s);
 int launch_scan_skew(const DeviceIndex& ix, const uint4* items, const uint32_t* num_items, uint32_t* cursor,
                      const uint32_t* probe, const float* images, uint32_t nprobe, uint32_t k, uint32_t* gthr,
-                     const uint32_t* q_item_off, uint32_t* pool_cnt, uint32_t* pool_key, uint64_t* pool_id,
-                     int grid, cudaStream_t s);
-int launch_select_pool(const uint32_t* pool_key, const uint64_t* pool_id, const uint32_t* pool_cnt,
-                       const uint32_t* q_item_off, uint32_t warps, uint32_t nq, uint32_t k, uint64_t* out_ids,
+                     uint32_t* pool_key, uint64_t* pool_id, int grid, cudaStream_t s);
+// K4: per query, exact top-k of its items' pool slots (k entries per item,
+// [q_item_off[q] * k, q_item_off[q + 1] * k)); count = min(scanned[q], k)
+int launch_select_pool(const uint32_t* pool_key, const uint64_t* pool_id, const uint64_t* scanned,
+                       const uint32_t* q_item_off, const uint32_t* gthr, uint32_t nq, uint32_t k, uint64_t* out_ids,
                        float* out_dist, uint32_t* out_count, uint32_t* gkey, uint64_t* gtie, uint32_t pw,
                        cudaStream_t s);
 uint32_t skew_item_tiles(uint64_t est_tiles, uint32_t grid);

@@ -36,7 +36,6 @@ namespace {
 constexpr uint32_t kTileEntries = 32;
 constexpr uint32_t kMaxItemTiles = 512;  // tiles per scan work item (16384 entries) at most
 constexpr uint32_t kMinItemTiles = 32;   // and at least (small batches: more, smaller items)
-constexpr uint32_t kLutPairs = 8;     // (query, list) pairs per LUT-kernel CTA
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -146,9 +145,106 @@ struct PlanArgs {
     uint32_t* cursor;
     uint32_t* q_item_off;
     uint32_t* gthr;
-    uint32_t* pool_cnt;
+    uint32_t* pair_off;  // [nq * nprobe] pool item index of each pair's first item
     uint64_t item_cap;
 };
+
+// plan_items for up to R pairs per thread (P <= R * blockDim.x): thread t
+// owns pairs [t*R, t*R + R), so every probe[] / list_len[] load is issued up
+// front (two dependent rounds in all), the pair-order prefix is one serial
+// sum per thread plus one block scan, and the scatter reuses the registers.
+// Same outputs as plan_items.
+template <int R>
+__device__ __noinline__ void plan_items_regs(const uint32_t* __restrict__ probe, const uint32_t* __restrict__ list_len,
+                                             uint32_t nq, uint32_t nprobe, const PlanArgs pa) {
+    const uint32_t it_tiles = pa.it_tiles;
+    __shared__ uint32_t wsum[33];
+    __shared__ uint32_t bucket_cnt[32], bucket_pos[32];
+    const uint32_t P = nq * nprobe, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    if (tid < 32) bucket_cnt[tid] = 0;
+    for (uint32_t q = tid; q < nq; q += blockDim.x) {
+        pa.scanned[q] = 0;
+        pa.gthr[q] = 0xffffffffu;
+    }
+    uint32_t len[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const uint32_t i = tid * R + r;
+        len[r] = i < P ? probe[i] : 0u;  // list id for now
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const uint32_t i = tid * R + r;
+        len[r] = i < P ? list_len[len[r]] : 0u;
+    }
+    __syncthreads();  // scanned[] zeroed, bucket_cnt ready
+    uint32_t mine = 0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const uint32_t i = tid * R + r;
+        if (len[r]) atomicAdd(reinterpret_cast<unsigned long long*>(pa.scanned + i / nprobe), (unsigned long long)len[r]);
+        const uint32_t tiles = (len[r] + kTileEntries - 1) / kTileEntries;
+        const uint32_t nit = (tiles + it_tiles - 1) / it_tiles;
+        if (nit) {  // nit - 1 full items, then the remainder
+            if (nit > 1) atomicAdd(&bucket_cnt[31 - __clz(it_tiles)], nit - 1);
+            atomicAdd(&bucket_cnt[31 - __clz(tiles - (nit - 1) * it_tiles)], 1u);
+        }
+        mine += nit;
+    }
+    // exclusive block prefix of `mine` (pair order = thread order)
+    uint32_t incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= uint32_t(o)) incl += t;
+    }
+    if (lane == 31) wsum[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+        const uint32_t nw = blockDim.x >> 5;
+        const uint32_t x = lane < nw ? wsum[lane] : 0u;
+        uint32_t xi = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, xi, o);
+            if (lane >= uint32_t(o)) xi += t;
+        }
+        if (lane < nw) wsum[lane] = xi - x;
+        if (lane == nw - 1) wsum[32] = xi;
+    }
+    if (tid == 0) {
+        uint32_t pos = 0;
+        for (int bkt = 31; bkt >= 0; --bkt) {
+            bucket_pos[bkt] = pos;
+            pos += bucket_cnt[bkt];
+        }
+    }
+    __syncthreads();
+    uint32_t excl = wsum[w] + incl - mine;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const uint32_t i = tid * R + r;
+        if (i >= P) break;
+        pa.pair_off[i] = excl;
+        if (i % nprobe == 0) pa.q_item_off[i / nprobe] = excl;
+        const uint32_t tiles = (len[r] + kTileEntries - 1) / kTileEntries;
+        const uint32_t nit = (tiles + it_tiles - 1) / it_tiles;
+        if (nit) {
+            const uint32_t full = nit - 1;
+            const uint32_t b0 = full ? atomicAdd(&bucket_pos[31 - __clz(it_tiles)], full) : 0u;
+            for (uint32_t j = 0; j < full; ++j)
+                if (b0 + j < pa.item_cap) pa.items[b0 + j] = make_uint4(i, j * it_tiles, (j + 1) * it_tiles, excl + j);
+            const uint32_t slot = atomicAdd(&bucket_pos[31 - __clz(tiles - full * it_tiles)], 1u);
+            if (slot < pa.item_cap) pa.items[slot] = make_uint4(i, full * it_tiles, tiles, excl + full);
+        }
+        excl += nit;
+    }
+    if (tid == 0) {
+        *pa.num_items = wsum[32];
+        *pa.cursor = 0;
+        pa.q_item_off[nq] = wsum[32];
+    }
+}
 
 // Runs on one CTA (any block size that is a multiple of 32, <= 1024): the
 // extra CTA of the LUT kernel's grid, so planning overlaps the LUT work.
@@ -161,7 +257,7 @@ __device__ __noinline__ void plan_items(const uint32_t* __restrict__ probe, cons
     uint32_t* __restrict__ cursor = pa.cursor;
     uint32_t* __restrict__ q_item_off = pa.q_item_off;
     uint32_t* __restrict__ gthr = pa.gthr;
-    uint32_t* __restrict__ pool_cnt = pa.pool_cnt;
+    uint32_t* __restrict__ pair_off = pa.pair_off;
     const uint64_t item_cap = pa.item_cap;
     __shared__ uint32_t tmp[33];
     __shared__ uint32_t bucket_cnt[32], bucket_pos[32];
@@ -204,6 +300,7 @@ __device__ __noinline__ void plan_items(const uint32_t* __restrict__ probe, cons
         }
         __syncthreads();
         const uint32_t excl = carry + tmp[w] + incl - nit;
+        if (valid) pair_off[i] = excl;
         if (valid && i % nprobe == 0) q_item_off[i / nprobe] = excl;
         carry += tmp[32];
         __syncthreads();
@@ -225,7 +322,9 @@ __device__ __noinline__ void plan_items(const uint32_t* __restrict__ probe, cons
         for (uint32_t j = 0; j < nit; ++j) {
             const uint32_t te = min(tiles, (j + 1) * it_tiles);
             const uint32_t slot = atomicAdd(&bucket_pos[31 - __clz(te - j * it_tiles)], 1u);
-            if (slot < item_cap) items[slot] = make_uint4(i, j * it_tiles, te, 0u);
+            // .w: the item's slot in the candidate pool (pair order, so a query's
+            // items are contiguous: [q_item_off[q], q_item_off[q + 1]))
+            if (slot < item_cap) items[slot] = make_uint4(i, j * it_tiles, te, pair_off[i] + j);
         }
     }
     if (threadIdx.x == 0) {
@@ -233,23 +332,22 @@ __device__ __noinline__ void plan_items(const uint32_t* __restrict__ probe, cons
         *cursor = 0;
         q_item_off[nq] = carry;
     }
-    for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x) {
-        gthr[q] = 0xffffffffu;
-        pool_cnt[q] = 0;
-    }
+    for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x) gthr[q] = 0xffffffffu;
 }
 
 
-// Grid: (ceil(npairs / kLutPairs) + 1, m / SQB); the last column of CTAs is
-// the work-item planner (plan_items), which overlaps the table computation. CTA: 256 threads = 256 codes; it
-// computes subquantizers [8*blockIdx.y, +8) of T[sq][code] =
-// squared_l2(r_sq, w[sq][code], sub_dim) (annindex.hpp:292-297, residual
-// r = q - c_list, annindex.hpp:287-289) for kLutPairs pairs and writes them
-// as the compact table luts[pair][sq][256]. Codewords come from the transposed [sq][j][256] copy
-// (coalesced), the next subquantizer's prefetched while the current one is
-// folded. Residuals sit in SMEM as [sq][j][pair] so one LDS.128 broadcasts
-// four pairs' values.
-template <int M, int SUBC, int SQB>  // SUBC: compile-time sub_dim (0 = runtime `sub`, <= 16); SQB subquantizers per CTA
+// Grid: (ceil(npairs / (8 * PCH)) + 1, m / SQB); the last column of CTAs is
+// the work-item planner (plan_items), which overlaps the table computation.
+// CTA: 256 threads = 256 codes; it computes subquantizers [SQB*blockIdx.y,
+// +SQB) of T[sq][code] = squared_l2(r_sq, w[sq][code], sub_dim)
+// (annindex.hpp:292-297, residual r = q - c_list, annindex.hpp:287-289) for
+// 8 * PCH pairs and writes them as the compact table luts[pair][sq][256]
+// (each store: 256 consecutive codes of one (pair, sq)). A thread's codeword
+// w[sq][code] is loaded once per subquantizer (transposed [sq][j][256] copy:
+// coalesced; the next subquantizer's prefetched while the current one is
+// folded) and reused for all 8 * PCH pairs; residuals sit in SMEM as
+// [sq][j][pair] so one LDS.128 broadcasts four pairs' values.
+template <int M, int SUBC, int SQB, int PCH>  // SUBC: compile-time sub_dim (0 = runtime `sub`, <= 16)
 __global__ void __launch_bounds__(256, 2) lut_image_kernel(const float* __restrict__ queries,
                                                            const float* __restrict__ centroids,
                                                            const float* __restrict__ codewordsT,
@@ -257,17 +355,25 @@ __global__ void __launch_bounds__(256, 2) lut_image_kernel(const float* __restri
                                                            const uint32_t* __restrict__ list_len, uint32_t nq,
                                                            uint32_t nprobe, uint32_t d, uint32_t sub,
                                                            float* __restrict__ luts, const PlanArgs pa) {
-    constexpr int P = kLutPairs;  // 8
+    constexpr int P = 8 * PCH;
     if (blockIdx.x == gridDim.x - 1) {  // the planning CTA
         if (blockIdx.y == 0) {
             pdl_wait();  // probe[] comes from the previous kernel
-            plan_items(probe, list_len, nq, nprobe, pa);
+            const uint32_t P = nq * nprobe;
+            if (P <= blockDim.x)
+                plan_items_regs<1>(probe, list_len, nq, nprobe, pa);
+            else if (P <= 4 * blockDim.x)
+                plan_items_regs<4>(probe, list_len, nq, nprobe, pa);
+            else if (P <= 16 * blockDim.x)
+                plan_items_regs<16>(probe, list_len, nq, nprobe, pa);
+            else
+                plan_items(probe, list_len, nq, nprobe, pa);
         }
         return;
     }
     constexpr int JMAX = SUBC ? SUBC : 16;
     if (SUBC) sub = SUBC;
-    __shared__ __align__(16) float resid[8 * 16 * P];  // [sq_local][j][pair]
+    __shared__ __align__(16) float resid[SQB * 16 * P];  // [sq_local][j][pair]
     __shared__ uint32_t s_q[P], s_list[P];
     const uint32_t npairs = nq * nprobe;
     const uint32_t p0 = blockIdx.x * P;
@@ -281,20 +387,12 @@ __global__ void __launch_bounds__(256, 2) lut_image_kernel(const float* __restri
     pdl_wait();  // probe[] comes from the previous kernel
     if (threadIdx.x < P) {
         const uint32_t pair = p0 + threadIdx.x;
-        uint32_t list = 0xffffffffu;
-        if (pair < npairs) {
-            list = probe[pair];
-            if (list_len[list] == 0) list = 0xffffffffu;
-        }
         s_q[threadIdx.x] = pair / nprobe;
-        s_list[threadIdx.x] = list;
+        s_list[threadIdx.x] = pair < npairs ? probe[pair] : 0xffffffffu;
     }
     __syncthreads();
-    uint32_t live = 0;  // bitmask of pairs with a non-empty list
-#pragma unroll
-    for (int p = 0; p < P; ++p) live |= (s_list[p] != 0xffffffffu) << p;
-    if (!live) return;
-    // residual r = q - c_list (annindex.hpp:288) for this CTA's 8 subquantizers
+    // residual r = q - c_list (annindex.hpp:288) for this CTA's subquantizers
+    // (tables of empty lists are computed too: the scan never reads them)
     const uint32_t span = SQB * sub;  // contiguous dims [sq0*sub, +span)
     for (uint32_t t = threadIdx.x; t < span * P; t += blockDim.x) {
         const uint32_t p = t / span, k = t - p * span;
@@ -307,8 +405,8 @@ __global__ void __launch_bounds__(256, 2) lut_image_kernel(const float* __restri
         resid[(sl * 16 + j) * P + p] = v;
     }
     __syncthreads();
-    float tv[SQB][P];  // T[sq0 + i][code] for each pair
-#pragma unroll
+    const uint32_t nlive = npairs > p0 ? min(uint32_t(P), npairs - p0) : 0u;
+#pragma unroll 1
     for (int i = 0; i < SQB; ++i) {
         float w[JMAX];
 #pragma unroll
@@ -318,36 +416,34 @@ __global__ void __launch_bounds__(256, 2) lut_image_kernel(const float* __restri
             for (int j = 0; j < JMAX; ++j)
                 if (j < int(sub)) wn[j] = __ldg(codewordsT + (size_t(sq0 + i + 1) * sub + j) * 256 + code);
         }
-        float acc[P];
-#pragma unroll
-        for (int p = 0; p < P; ++p) acc[p] = 0.0f;
         const float* rr = resid + (i * 16) * P;
 #pragma unroll
-        for (int j = 0; j < JMAX; ++j) {
-            if (j < int(sub)) {
-                const float4 ra = *reinterpret_cast<const float4*>(rr + j * P);
-                const float4 rb = *reinterpret_cast<const float4*>(rr + j * P + 4);
-                float sq[P];  // fl(fl(r - w)^2), two pairs per FADD2 / FMUL2
-                subsq2_bcast(ra.x, ra.y, w[j], sq[0], sq[1]);
-                subsq2_bcast(ra.z, ra.w, w[j], sq[2], sq[3]);
-                subsq2_bcast(rb.x, rb.y, w[j], sq[4], sq[5]);
-                subsq2_bcast(rb.z, rb.w, w[j], sq[6], sq[7]);
+        for (int c = 0; c < PCH; ++c) {
+            if (uint32_t(c * 8) >= nlive) break;
+            float acc[8];
 #pragma unroll
-                for (int p = 0; p < P; ++p) acc[p] = __fadd_rn(acc[p], sq[p]);
+            for (int p = 0; p < 8; ++p) acc[p] = 0.0f;
+#pragma unroll
+            for (int j = 0; j < JMAX; ++j) {
+                if (j < int(sub)) {
+                    const float4 ra = *reinterpret_cast<const float4*>(rr + j * P + c * 8);
+                    const float4 rb = *reinterpret_cast<const float4*>(rr + j * P + c * 8 + 4);
+                    float sq[8];  // fl(fl(r - w)^2), two pairs per FADD2 / FMUL2
+                    subsq2_bcast(ra.x, ra.y, w[j], sq[0], sq[1]);
+                    subsq2_bcast(ra.z, ra.w, w[j], sq[2], sq[3]);
+                    subsq2_bcast(rb.x, rb.y, w[j], sq[4], sq[5]);
+                    subsq2_bcast(rb.z, rb.w, w[j], sq[6], sq[7]);
+#pragma unroll
+                    for (int p = 0; p < 8; ++p) acc[p] = __fadd_rn(acc[p], sq[p]);
+                }
             }
-        }
+            float* dst = luts + (size_t(p0 + c * 8) * M + sq0 + i) * 256 + code;
 #pragma unroll
-        for (int p = 0; p < P; ++p) tv[i][p] = acc[p];
+            for (int p = 0; p < 8; ++p)
+                if (uint32_t(c * 8 + p) < nlive) dst[size_t(p) * M * 256] = acc[p];
+        }
     }
     pdl_trigger();
-    // compact table luts[pair][sq][256]: each store is 32 consecutive codes
-#pragma unroll
-    for (int p = 0; p < P; ++p) {
-        if (!(live >> p & 1u)) continue;
-        float* dst = luts + (size_t(p0 + p) * M + sq0) * 256 + code;
-#pragma unroll
-        for (int i = 0; i < SQB; ++i) dst[i * 256] = tv[i][p];
-    }
 }
 
 // ------------------------------------------------------------------- scan
@@ -373,6 +469,7 @@ constexpr uint32_t kMinWarpTiles = 4;  // a warp re-reads one tail tile per rang
 struct ItemSlot {
     uint32_t pair, tb, te, len, q;
     uint32_t thr;            // the query's shared threshold when the producer fetched the item
+    uint32_t pslot;          // the item's slot in the query's candidate pool (k entries each)
     uint64_t tile_byte_off;  // skew_off[list] * tile bytes
     uint64_t lbase;          // list_off[list]: padded entry slot of the list's entry 0
 };
@@ -393,7 +490,9 @@ struct SkewSmem {
     static constexpr uint32_t kRing = uint32_t(D) * kTile;  // per consumer warp
     // img_full[NB], img_empty[NB], stg_full, stg_empty
     static constexpr uint32_t nbars = 2 * NB + 2;
-    static constexpr uint32_t kTail = 8 * nbars + (NB + 1) * uint32_t(sizeof(ItemSlot)) + 4 * NB;  // + cta_thr[NB]
+    // + cta_thr[NB] + merge counters[NB] + per-(buffer, warp) list stash {key[32], pos[32]}
+    static constexpr uint32_t kTail = 8 * nbars + (NB + 1) * uint32_t(sizeof(ItemSlot)) + 4 * NB + 4 * NB +
+                                      uint32_t(NB) * W * 64 * 4;
     static constexpr uint32_t bytes = 232448;                // 227 KiB: the opt-in maximum
     // worst case: a pad just below one ring (nothing fits in it)
     static constexpr uint32_t worst = (kRing - 16) + NB * kImg + kStage + W * kRing + kTail;
@@ -471,10 +570,12 @@ struct ScanCtx {
     const uint8_t* skew_codes;
     const uint64_t* ids;
     uint32_t* gthr;
-    const uint32_t* q_item_off;
-    uint32_t* pool_cnt;
     uint32_t* pool_key;
     uint64_t* pool_id;
+    uint32_t* mslot;   // this warp's stash for the item: key[32], pos[32] (SMEM)
+    uint32_t* mbase;   // the item's stashes, 64 words per warp
+    uint32_t* mcount;  // warps of the item done so far
+    uint32_t nact;     // warps with a non-empty range in the item
 };
 
 // Exact warp top-k (k <= 32): lane i holds the i-th (distance bits, entry
@@ -561,6 +662,15 @@ __device__ __forceinline__ void warp_range(const ItemSlot& sl, uint32_t warp, ui
     e_end = warp < nw ? min(sl.te, a + per) : a;
 }
 
+// Warps of an item that get a non-empty range (a < te) from warp_range.
+template <int W>
+__device__ __forceinline__ uint32_t warp_count(const ItemSlot& sl) {
+    const uint32_t ntile = sl.te - sl.tb;
+    const uint32_t nw = min(uint32_t(W), (ntile + kMinWarpTiles - 1) / kMinWarpTiles);
+    const uint32_t per = (ntile + nw - 1) / nw;
+    return min(nw, (ntile + per - 1) / per);
+}
+
 template <int M>
 __device__ __forceinline__ bool scan_range(const ScanCtx& cx, const ItemSlot& sl, uint32_t a, uint32_t e_end,
                                            uint32_t& consumed, const float* mk, const float* nk,
@@ -572,8 +682,6 @@ __device__ __forceinline__ bool scan_range(const ScanCtx& cx, const ItemSlot& sl
     const uint64_t* __restrict__ ids = cx.ids;
     uint32_t* gthr = cx.gthr;
     const uint8_t* skew_codes = cx.skew_codes;
-    const uint32_t* q_item_off = cx.q_item_off;
-    uint32_t* pool_cnt = cx.pool_cnt;
     uint32_t* pool_key = cx.pool_key;
     uint64_t* pool_id = cx.pool_id;
     const uint32_t q = sl.q;
@@ -659,23 +767,63 @@ __device__ __forceinline__ bool scan_range(const ScanCtx& cx, const ItemSlot& sl
         cur = 0.0f;
         topk_offer(t, key, j > a && e < sl.len, uint32_t(sl.lbase) + e, lane, k, ids, gthr + q, cx.cta_thr);
     }
-    // publish this warp's list into the query's candidate pool, minus entries
-    // above the query's shared threshold: some warp holds k candidates at or
-    // below it, so those entries cannot make the final top-k
-    // the warp's view (shared threshold at range start, its own and this CTA's
-    // k-th distances) is never below the final shared threshold: a valid filter
-    const uint32_t g_pub = min(t.g, *reinterpret_cast<volatile uint32_t*>(cx.cta_thr));
-    const unsigned have = __ballot_sync(0xffffffffu, lane < k && t.key != 0xffffffffu && t.key <= g_pub);
-    const uint32_t cnt = __popc(have);
-    if (cnt) {
-        uint32_t base = 0;
-        if (lane == 0) base = atomicAdd(pool_cnt + q, cnt);
-        base = __shfl_sync(0xffffffffu, base, 0);
-        const size_t poff = size_t(q_item_off[q]) * W * k;
-        if (lane < cnt) {
-            pool_key[poff + base + lane] = ord_key(__uint_as_float(t.key));
-            pool_id[poff + base + lane] = ids[t.pos];
+    // Stash this warp's list; the item's last warp merges the stashed lists
+    // into the CTA's exact top-k of the item and publishes only that (k
+    // entries per item reach the query's pool instead of k per warp).
+    cx.mslot[lane] = lane < k ? t.key : 0xffffffffu;
+    cx.mslot[32 + lane] = t.pos;
+    __syncwarp();
+    uint32_t arrived = 0;
+    if (lane == 0) {
+        __threadfence_block();
+        arrived = atomicAdd(cx.mcount, 1u);
+    }
+    arrived = __shfl_sync(0xffffffffu, arrived, 0);
+    if (arrived + 1 < cx.nact) return nx_ok;
+    __threadfence_block();
+    if (lane == 0) *cx.mcount = 0;  // the buffer's next item starts from zero
+    // k rounds of "smallest (key, id) among the list heads" (lane w < nact
+    // owns warp w's list, sorted by (distance, chunk id))
+    const uint32_t* ml = cx.mbase + lane * 64;
+    const bool own = lane < cx.nact;
+    uint32_t hi = 0;
+    uint32_t hk = own ? ml[0] : 0xffffffffu, hp = own ? ml[32] : 0u;
+    uint32_t rk = 0xffffffffu, rp = 0u, cnt = 0;
+    for (uint32_t r = 0; r < k; ++r) {
+        const uint32_t kmin = __reduce_min_sync(0xffffffffu, hk);
+        if (kmin == 0xffffffffu) break;
+        const unsigned tie = __ballot_sync(0xffffffffu, hk == kmin);
+        int win = __ffs(tie) - 1;
+        if (tie & (tie - 1)) {  // exact distance tie between lists: lowest chunk id first
+            uint64_t id = hk == kmin ? ids[hp] : ~0ull;
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                const uint64_t oid = __shfl_xor_sync(0xffffffffu, id, o);
+                id = oid < id ? oid : id;
+            }
+            win = __ffs(__ballot_sync(0xffffffffu, hk == kmin && ids[hp] == id)) - 1;
         }
+        const uint32_t wp = __shfl_sync(0xffffffffu, hp, win);
+        if (lane == r) {
+            rk = kmin;
+            rp = wp;
+        }
+        ++cnt;
+        if (int(lane) == win) {
+            ++hi;
+            hk = hi < k ? ml[hi] : 0xffffffffu;
+            hp = hi < k ? ml[32 + hi] : 0u;
+        }
+    }
+    if (cnt == k) {
+        const uint32_t kth = __shfl_sync(0xffffffffu, rk, k - 1);
+        if (lane == 0) atomicMin(gthr + q, kth);
+    }
+    // the item's fixed pool slot: k entries, unfilled ones as +inf sentinels
+    if (lane < k) {
+        const size_t o = size_t(sl.pslot) * k + lane;
+        pool_key[o] = lane < cnt ? ord_key(__uint_as_float(rk)) : 0xffffffffu;
+        pool_id[o] = lane < cnt ? ids[rp] : ~0ull;
     }
     return nx_ok;
 }
@@ -704,8 +852,7 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
                      const uint32_t* __restrict__ list_len, const uint64_t* __restrict__ skew_off,
                      const uint8_t* __restrict__ skew_codes, const uint64_t* __restrict__ list_off,
                      const uint64_t* __restrict__ ids, const float* __restrict__ luts, uint32_t nprobe,
-                     uint32_t k, uint32_t* __restrict__ gthr, const uint32_t* __restrict__ q_item_off,
-                     uint32_t* __restrict__ pool_cnt, uint32_t* __restrict__ pool_key,
+                     uint32_t k, uint32_t* __restrict__ gthr, uint32_t* __restrict__ pool_key,
                      uint64_t* __restrict__ pool_id) {
     using L = SkewSmem<M>;
     constexpr int W = L::W, NB = L::NB;
@@ -719,8 +866,10 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
     const uint32_t stage_off = img_off + NB * kImgBytes;
     const uint32_t rings_in_pad = min(uint32_t(W), pad / L::kRing);
     const uint32_t after_off = stage_off + kStageBytes;  // rings not in the pad, then the tail
-    const uint32_t tail_off = after_off + (W - rings_in_pad) * L::kRing;
-    if (tail_off + L::kTail > L::bytes) __trap();
+    // the tail goes into what the rings leave of the pad when it fits there
+    const uint32_t pad_tail = (rings_in_pad * L::kRing + 15u) & ~15u;
+    const uint32_t tail_off = pad_tail + L::kTail <= pad ? pad_tail : after_off + (W - rings_in_pad) * L::kRing;
+    if (tail_off + L::kTail > L::bytes || after_off + (W - rings_in_pad) * L::kRing > L::bytes) __trap();
     float* stage = reinterpret_cast<float*>(smem + stage_off);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + tail_off);
     uint64_t* img_full = bars;
@@ -730,6 +879,8 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
     ItemSlot* slots = reinterpret_cast<ItemSlot*>(smem + tail_off + 8 * L::nbars);  // [NB] image slots
     ItemSlot* stg_slot = slots + NB;                                                 // staging slot
     uint32_t* cta_thr = reinterpret_cast<uint32_t*>(stg_slot + 1);  // [NB]: the CTA's k-th distance per item
+    uint32_t* mcount = cta_thr + NB;                                  // [NB]: merge arrivals per item
+    uint32_t* mstash = mcount + NB;                                   // [NB][W][64]: warp lists of an item
 
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) {
@@ -739,6 +890,7 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
         }
         mbar_init(stg_full, 1);
         mbar_init(stg_empty, kExpWarps);
+        for (int i = 0; i < NB; ++i) mcount[i] = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -773,6 +925,7 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
                 sl.tile_byte_off = skew_off[list] * L::kTile;
                 sl.lbase = list_off[list];
                 sl.thr = ld_relaxed(gthr + sl.q);
+                sl.pslot = w4.w;
                 nx = atomicAdd(cursor, 1u);  // next item's index, fetched ahead
             }
             const uint32_t pair = __shfl_sync(0xffffffffu, sl.pair, 0);
@@ -891,8 +1044,9 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
         uint32_t a, e_end;
         warp_range<W>(sl, warp, a, e_end);
         if (a < e_end) {
+            uint32_t* mb = mstash + b * (W * 64);
             const ScanCtx cx{cta_thr + b, ring_s, lane, bt0 + b * (kImgBytes & 0xffff0000u), k, skew_codes, ids, gthr,
-                             q_item_off, pool_cnt, pool_key, pool_id};
+                             pool_key, pool_id, mb + warp * 64, mb, mcount + b, warp_count<W>(sl)};
             const uint32_t bn = NB == 1 ? 0u : (i + 1) % NB;
             const NextRange nx{slots + bn, img_full + bn, (NB == 1 ? i + 1 : (i + 1) / NB) & 1u, warp, NB > 1};
             pref = scan_range<M>(cx, sl, a, e_end, consumed, mk, nk, pref, nx);
@@ -935,20 +1089,21 @@ static int check(const char* what) {
 int launch_lut_images(const DeviceIndex& ix, const float* queries, const uint32_t* probe, uint32_t nq,
                       uint32_t nprobe, float* luts, uint32_t it_tiles, uint64_t* scanned, uint4* items,
                       uint32_t* num_items, uint32_t* cursor, uint32_t* q_item_off, uint32_t* gthr,
-                      uint32_t* pool_cnt, uint64_t item_cap, cudaStream_t s) {
+                      uint32_t* pair_off, uint64_t item_cap, cudaStream_t s) {
     const uint32_t npairs = nq * nprobe;
-    const PlanArgs pa{it_tiles, scanned, items, num_items, cursor, q_item_off, gthr, pool_cnt, item_cap};
-    // small batches: 2 subquantizers per CTA (4x the CTAs, 1/4 of the serial
-    // codeword round trips each); large ones: 8 (residuals shared by more work)
-    const bool small = uint64_t((npairs + kLutPairs - 1) / kLutPairs) * (ix.nsq / 8) < 2 * 148;
-    dim3 grid((npairs + kLutPairs - 1) / kLutPairs + 1, ix.nsq / (small ? 2 : 8));
+    const PlanArgs pa{it_tiles, scanned, items, num_items, cursor, q_item_off, gthr, pair_off, item_cap};
+    // small batches: 2 subquantizers x 8 pairs per CTA (enough CTAs to fill
+    // the GPU); large ones: 4 x 32 (codewords reused by 4x more pairs)
+    const bool small = uint64_t((npairs + 31) / 32) * (ix.nsq / 4) < 148;
+    const uint32_t ppc = small ? 8 : 32;
+    dim3 grid((npairs + ppc - 1) / ppc + 1, ix.nsq / (small ? 2 : 4));
 #define PG_LUT(MM, SS)                                                                                          \
     do {                                                                                                        \
         if (small)                                                                                              \
-            PG_CUDA(launch_pdl(lut_image_kernel<MM, SS, 2>, grid, dim3(256), 0, s, queries, ix.centroids,       \
+            PG_CUDA(launch_pdl(lut_image_kernel<MM, SS, 2, 1>, grid, dim3(256), 0, s, queries, ix.centroids,    \
                                ix.codewordsT, probe, ix.list_len, nq, nprobe, ix.d, ix.sub_dim, luts, pa));       \
         else                                                                                                    \
-            PG_CUDA(launch_pdl(lut_image_kernel<MM, SS, 8>, grid, dim3(256), 0, s, queries, ix.centroids,       \
+            PG_CUDA(launch_pdl(lut_image_kernel<MM, SS, 4, 4>, grid, dim3(256), 0, s, queries, ix.centroids,    \
                                ix.codewordsT, probe, ix.list_len, nq, nprobe, ix.d, ix.sub_dim, luts, pa));       \
     } while (0)
     if (ix.nsq == 32 && ix.sub_dim == 12)
@@ -965,20 +1120,19 @@ int launch_lut_images(const DeviceIndex& ix, const float* queries, const uint32_
 
 int launch_scan_skew(const DeviceIndex& ix, const uint4* items, const uint32_t* num_items, uint32_t* cursor,
                      const uint32_t* probe, const float* luts, uint32_t nprobe, uint32_t k, uint32_t* gthr,
-                     const uint32_t* q_item_off, uint32_t* pool_cnt, uint32_t* pool_key, uint64_t* pool_id,
-                     int grid, cudaStream_t s) {
+                     uint32_t* pool_key, uint64_t* pool_id, int grid, cudaStream_t s) {
     if (ix.nsq == 32) {
         const size_t smem = skew_smem_bytes<32>();
         PG_CUDA(cudaFuncSetAttribute(scan_skew_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         PG_CUDA(launch_pdl(scan_skew_kernel<32>, dim3(grid), dim3(SkewSmem<32>::threads), smem, s, items, num_items,
                            cursor, probe, ix.list_len, ix.skew_off, ix.skew_codes, ix.list_off, ix.ids, luts, nprobe, k,
-                           gthr, q_item_off, pool_cnt, pool_key, pool_id));
+                           gthr, pool_key, pool_id));
     } else {
         const size_t smem = skew_smem_bytes<64>();
         PG_CUDA(cudaFuncSetAttribute(scan_skew_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         PG_CUDA(launch_pdl(scan_skew_kernel<64>, dim3(grid), dim3(SkewSmem<64>::threads), smem, s, items, num_items,
                            cursor, probe, ix.list_len, ix.skew_off, ix.skew_codes, ix.list_off, ix.ids, luts, nprobe, k,
-                           gthr, q_item_off, pool_cnt, pool_key, pool_id));
+                           gthr, pool_key, pool_id));
     }
     return check("scan_skew");
 }

@@ -184,6 +184,29 @@ int main() {
     }
     kats();
     {
+        // prag::gpu::train_index == prag::train_index on the same embeddings
+        SplitMix64 rng(77);
+        Corpus corpus;
+        for (int i = 0; i < 40; ++i) corpus.documents.push_back(random_tokens(rng, 6400));
+        Database db = build_database(corpus, 64, 96, 7);
+        TrainParams p;
+        p.nlist = 24;
+        p.n_subquantizers = 24;
+        p.train_sample_cap = 2000;
+        auto [ri, rc] = train_index(db.embeddings, p);
+        auto [gi, gc] = gpu::train_index(db.embeddings, p);
+        bool same = ri.nlist == gi.nlist && ri.d == gi.d && ri.centroids == gi.centroids &&
+                    rc.n_subquantizers == gc.n_subquantizers && rc.sub_dim == gc.sub_dim &&
+                    rc.codewords == gc.codewords && ri.postings.size() == gi.postings.size();
+        for (std::size_t l = 0; same && l < ri.postings.size(); ++l) {
+            same = ri.postings[l].size() == gi.postings[l].size();
+            for (std::size_t e = 0; same && e < ri.postings[l].size(); ++e)
+                same = ri.postings[l][e].chunk_id == gi.postings[l][e].chunk_id &&
+                       ri.postings[l][e].code == gi.postings[l][e].code;
+        }
+        report(same, "gpu::train_index == prag::train_index (" + std::to_string(db.size()) + " chunks, d=96)");
+    }
+    {
         Fixture fx(60, 32, 32, 0);  // d=32, nsq=8 (reference defaults): generic scan path
         dropin_parity(fx, "d32/m8");
     }
