@@ -282,12 +282,56 @@ public:
           embedder_(make_embedder(db, embed_seed, gpu_.describe().device)), perf_(perf),
           safety_margin_(safety_margin) {}
 
+    // pipeline.hpp:224-226: the directive's nprobe (auto: from the perf model).
+    std::uint32_t resolve_nprobe(const ::prag::NprobeDirective& directive) const {
+        return directive.auto_mode ? ::prag::select_nprobe(perf_, directive.budget_s, nlist_, safety_margin_)
+                                   : std::min(directive.nprobe, nlist_);
+    }
+
+    // Several queries that share k and nprobe in one embed + one batched
+    // search (the serving path: GpuRetrievalService coalesces concurrent
+    // requests through this). Outcome i is what retrieve(*queries[i], ...)
+    // returns.
+    std::vector<::prag::RetrievalOutcome> retrieve_batch(const std::vector<const ::prag::TokenChunk*>& queries,
+                                                         std::uint32_t k, std::uint32_t nprobe) {
+        ::prag::Stopwatch clock;
+        const std::uint32_t nq = static_cast<std::uint32_t>(queries.size());
+        std::vector<::prag::RetrievalOutcome> out(nq);
+        if (nq == 0) return out;
+        std::vector<float> emb(std::size_t(nq) * db_->d);
+        const std::size_t m = queries[0]->size();
+        bool same_len = true;
+        for (const auto* q : queries) same_len = same_len && q->size() == m;
+        {
+            std::lock_guard<std::mutex> lk(embed_mu_);
+            if (same_len) {
+                std::vector<::prag::TokenId> toks;
+                toks.reserve(nq * m);
+                for (const auto* q : queries) toks.insert(toks.end(), q->begin(), q->end());
+                check(prag_gpu_embed(embedder_.get(), toks.data(), nq, std::uint32_t(m), emb.data(), nullptr));
+            } else {
+                for (std::uint32_t i = 0; i < nq; ++i)
+                    check(prag_gpu_embed(embedder_.get(), queries[i]->data(), 1, std::uint32_t(queries[i]->size()),
+                                         emb.data() + std::size_t(i) * db_->d, nullptr));
+            }
+        }
+        auto found = search_batch(gpu_, emb.data(), nq, SearchParams{nprobe, k, false});
+        const double t = clock.elapsed_s();
+        for (std::uint32_t i = 0; i < nq; ++i) {
+            out[i].nprobe_used = nprobe;
+            for (const auto& hit : found[i].neighbors) {
+                const auto& rec = db_->records[hit.chunk_id];
+                out[i].neighbors.push_back({rec.tokens, rec.continuation, hit.distance});
+            }
+            out[i].server_latency_s = t;
+        }
+        return out;
+    }
+
     ::prag::RetrievalOutcome retrieve(const ::prag::TokenChunk& query_tokens, std::uint32_t k,
                                       ::prag::NprobeDirective directive) override {
         ::prag::Stopwatch clock;
-        const std::uint32_t nprobe = directive.auto_mode
-                                         ? ::prag::select_nprobe(perf_, directive.budget_s, nlist_, safety_margin_)
-                                         : std::min(directive.nprobe, nlist_);
+        const std::uint32_t nprobe = resolve_nprobe(directive);
         std::vector<float> query(db_->d);
         {
             std::lock_guard<std::mutex> lk(embed_mu_);
