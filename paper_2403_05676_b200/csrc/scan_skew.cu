@@ -25,6 +25,7 @@
 //    memory (atomicMin on the k-th distance) prunes candidates; ids are
 //    loaded only for candidates that pass.
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <utility>
 
@@ -364,8 +365,8 @@ __global__ void __launch_bounds__(256, 2) lut_image_kernel(const float* __restri
                 plan_items_regs<1>(probe, list_len, nq, nprobe, pa);
             else if (P <= 4 * blockDim.x)
                 plan_items_regs<4>(probe, list_len, nq, nprobe, pa);
-            else if (P <= 16 * blockDim.x)
-                plan_items_regs<16>(probe, list_len, nq, nprobe, pa);
+            else if (P <= 8 * blockDim.x)
+                plan_items_regs<8>(probe, list_len, nq, nprobe, pa);
             else
                 plan_items(probe, list_len, nq, nprobe, pa);
         }
@@ -417,9 +418,14 @@ __global__ void __launch_bounds__(256, 2) lut_image_kernel(const float* __restri
                 if (j < int(sub)) wn[j] = __ldg(codewordsT + (size_t(sq0 + i + 1) * sub + j) * 256 + code);
         }
         const float* rr = resid + (i * 16) * P;
-#pragma unroll
+#pragma unroll 1
         for (int c = 0; c < PCH; ++c) {
             if (uint32_t(c * 8) >= nlive) break;
+            // FADD2 (r - w) and FMUL2 (square) two pairs at a time, scalar
+            // FADD accumulation: every step separately rounded, and no
+            // FMUL2 -> FADD2 pair for ptxas to contract into an FFMA2. (A
+            // packed accumulation measured slower: the packed FP32 ops do
+            // not raise the FMA-pipe rate this kernel is bound by.)
             float acc[8];
 #pragma unroll
             for (int p = 0; p < 8; ++p) acc[p] = 0.0f;
@@ -428,7 +434,7 @@ __global__ void __launch_bounds__(256, 2) lut_image_kernel(const float* __restri
                 if (j < int(sub)) {
                     const float4 ra = *reinterpret_cast<const float4*>(rr + j * P + c * 8);
                     const float4 rb = *reinterpret_cast<const float4*>(rr + j * P + c * 8 + 4);
-                    float sq[8];  // fl(fl(r - w)^2), two pairs per FADD2 / FMUL2
+                    float sq[8];  // fl(fl(r - w)^2)
                     subsq2_bcast(ra.x, ra.y, w[j], sq[0], sq[1]);
                     subsq2_bcast(ra.z, ra.w, w[j], sq[2], sq[3]);
                     subsq2_bcast(rb.x, rb.y, w[j], sq[4], sq[5]);
@@ -1092,19 +1098,39 @@ int launch_lut_images(const DeviceIndex& ix, const float* queries, const uint32_
                       uint32_t* pair_off, uint64_t item_cap, cudaStream_t s) {
     const uint32_t npairs = nq * nprobe;
     const PlanArgs pa{it_tiles, scanned, items, num_items, cursor, q_item_off, gthr, pair_off, item_cap};
-    // small batches: 2 subquantizers x 8 pairs per CTA (enough CTAs to fill
-    // the GPU); large ones: 4 x 32 (codewords reused by 4x more pairs)
-    const bool small = uint64_t((npairs + 31) / 32) * (ix.nsq / 4) < 148;
-    const uint32_t ppc = small ? 8 : 32;
-    dim3 grid((npairs + ppc - 1) / ppc + 1, ix.nsq / (small ? 2 : 4));
+    // CTA shape (subquantizers x 8*PCH pairs), from tools/sweep_lut.sh:
+    // small batches 2 x 8 (enough CTAs to fill the GPU), large ones 2 x 16.
+    // The kernel sits near its FP32-pipe bound either way (3 separately
+    // rounded ops per (code, pair, dim) term). PRAG_GPU_LUT_CFG="SQB,PCH"
+    // overrides (tuning knob).
+    static const int cfg_env = [] {
+        const char* e = getenv("PRAG_GPU_LUT_CFG");
+        int a = 0, b = 0;
+        return (e && sscanf(e, "%d,%d", &a, &b) == 2) ? a * 16 + b : 0;
+    }();
+    int sqb, pch;
+    if (cfg_env) {
+        sqb = cfg_env / 16;
+        pch = cfg_env % 16;
+    } else {
+        const bool small = uint64_t((npairs + 15) / 16) * (ix.nsq / 2) < 2 * 148;
+        sqb = 2;
+        pch = small ? 1 : 2;
+    }
+    const uint32_t ppc = 8u * pch;
+    dim3 grid((npairs + ppc - 1) / ppc + 1, ix.nsq / sqb);
+#define PG_LUT1(MM, SS, Q, C)                                                                                   \
+    PG_CUDA(launch_pdl(lut_image_kernel<MM, SS, Q, C>, grid, dim3(256), 0, s, queries, ix.centroids,            \
+                       ix.codewordsT, probe, ix.list_len, nq, nprobe, ix.d, ix.sub_dim, luts, pa))
 #define PG_LUT(MM, SS)                                                                                          \
     do {                                                                                                        \
-        if (small)                                                                                              \
-            PG_CUDA(launch_pdl(lut_image_kernel<MM, SS, 2, 1>, grid, dim3(256), 0, s, queries, ix.centroids,    \
-                               ix.codewordsT, probe, ix.list_len, nq, nprobe, ix.d, ix.sub_dim, luts, pa));       \
-        else                                                                                                    \
-            PG_CUDA(launch_pdl(lut_image_kernel<MM, SS, 4, 4>, grid, dim3(256), 0, s, queries, ix.centroids,    \
-                               ix.codewordsT, probe, ix.list_len, nq, nprobe, ix.d, ix.sub_dim, luts, pa));       \
+        if (sqb == 2 && pch == 1) PG_LUT1(MM, SS, 2, 1);                                                        \
+        else if (sqb == 2 && pch == 2) PG_LUT1(MM, SS, 2, 2);                                                   \
+        else if (sqb == 2 && pch == 4) PG_LUT1(MM, SS, 2, 4);                                                   \
+        else if (sqb == 4 && pch == 1) PG_LUT1(MM, SS, 4, 1);                                                   \
+        else if (sqb == 4 && pch == 2) PG_LUT1(MM, SS, 4, 2);                                                   \
+        else if (sqb == 8 && pch == 1) PG_LUT1(MM, SS, 8, 1);                                                   \
+        else PG_LUT1(MM, SS, 4, 4);                                                                             \
     } while (0)
     if (ix.nsq == 32 && ix.sub_dim == 12)
         PG_LUT(32, 12);
@@ -1114,6 +1140,7 @@ int launch_lut_images(const DeviceIndex& ix, const float* queries, const uint32_
         PG_LUT(64, 6);
     else
         PG_LUT(64, 0);
+#undef PG_LUT1
 #undef PG_LUT
     return check("lut_images");
 }
