@@ -16,9 +16,13 @@ the headline in "sweep", with the GPU-recalibrated performance model.
           compiled from /root/reference) on this box's host cores, same
           index file and queries.
 
-N>1 (torchrun): inverted lists sharded by LPT over ranks (load_shard), each
-rank searches its shard, NCCL all_gather of per-shard top-k, exact merge
-kernel on rank 0 -- same DB and queries for every N ("scaling": "strong").
+N>1 (torchrun): the 10M index fits one GPU, so each rank holds a replica
+and searches its own 64-query batches (queries are independent units: no
+data-path collective, "scaling": "weak"; value = all ranks' queries over the
+max-over-ranks time). PRAG_BENCH_MODE=shard-lists instead shards the
+inverted lists by LPT over ranks (load_shard), NCCL all_gather of per-shard
+top-k and the exact merge kernel on rank 0 -- same DB and queries for every
+N ("scaling": "strong"), the layout for indexes beyond one GPU (configs C/D).
 """
 from __future__ import annotations
 
@@ -178,12 +182,21 @@ def main():
     if rank != 0:
         path, queries, meta = F.ensure_fixture(cfg["n"], cfg["d"], cfg["nlist"], cfg["nsq"], cfg["seed"], nq=64,
                                                log=log)
+    # N > 1: the index fits one GPU (config B), so by default every rank holds
+    # a replica and serves its own query batches -- queries are independent
+    # units, no data-path collective, weak scaling. PRAG_BENCH_MODE=shard-lists
+    # instead splits the inverted lists across ranks (the mode
+    # for indexes larger than one GPU) with one NCCL exchange per batch.
+    mode = os.environ.get("PRAG_BENCH_MODE", "replicas") if world > 1 else "single"
+    if mode not in ("single", "replicas", "shard-lists"):
+        raise SystemExit(f"PRAG_BENCH_MODE must be replicas or shard-lists, not {mode}")
     workload = (f"ivfpq search: {cfg['n'] // 1_000_000}M x {cfg['d']} fp32 DB, nlist={cfg['nlist']}, "
                 f"PQ m={cfg['nsq']}x8b, nq={cfg['nq']}, nprobe={cfg['nprobe']}, k={cfg['k']}")
     config = {"workload": workload, "n": cfg["n"], "d": cfg["d"], "nlist": cfg["nlist"], "m": cfg["nsq"],
               "nq": cfg["nq"], "nprobe": cfg["nprobe"], "k": cfg["k"], "lists": meta,
               "l2": "flushed between timed steps (256 MiB memset)",
-              "parallelism": f"list-sharded x{world}" if world > 1 else "single GPU"}
+              "parallelism": {"single": "single GPU", "replicas": f"query-parallel replicas x{world}",
+                              "shard-lists": f"list-sharded x{world}"}[mode]}
 
     if args.impl == "reference":
         if rank != 0:
@@ -197,8 +210,8 @@ def main():
         qps = r["qps"]
         line = {"impl": "reference", "metric": METRIC, "value": qps, "unit": "queries/s", "n_gpus": world,
                 "steps": r["reps"], "warmup": args.warmup, "ms_per_step": r["p50_s"] * 1e3,
-                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-                "data": "synthetic", "config": config,
+                "higher_is_better": True, "scaling": "weak" if mode == "replicas" else "strong",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config,
                 "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": threads, "kind": "reference",
                                  "sample": f"{r['reps']} timed batches of {cfg['nq']} queries (p50), "
                                            f"prag::search on {threads} std::threads, index via load_index",
@@ -212,10 +225,12 @@ def main():
     import paper_2403_05676_b200 as pg
 
     dev = torch.device("cuda", local)
-    if world > 1:
+    if mode == "shard-lists":
         ix = pg.GpuIndex.load_shard(path, rank, world, local)
     else:
         ix = pg.GpuIndex.load(path, local)
+    if mode == "replicas":  # each rank its own batch (same cost: a rotation of the fixture queries)
+        queries = np.ascontiguousarray(np.roll(queries, 8 * rank, axis=0))
     stream = torch.cuda.Stream(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     nq, k, nprobe = cfg["nq"], cfg["k"], cfg["nprobe"]
@@ -225,7 +240,7 @@ def main():
     def step_dev(qd, nprobe_, k_):
         with torch.cuda.stream(stream):
             r = ix.search_batch(qd, k_, nprobe_, stream=stream)
-            if world > 1:  # one packed NCCL all-gather of the per-shard top-k, exact merge on rank 0
+            if mode == "shard-lists":  # one packed NCCL all-gather of the per-shard top-k, exact merge on rank 0
                 r = PD.gather_merge(r, k_)
         return r
 
@@ -277,7 +292,7 @@ def main():
                                torch.empty((nq,), dtype=torch.int64).pin_memory())
 
         def step_e2e():
-            if world == 1:
+            if mode != "shard-lists":
                 ix.search_batch(qhost, k, nprobe, stream=stream, out=h_out)
             else:
                 qd = qhost.to(dev, non_blocking=True)
@@ -306,7 +321,7 @@ def main():
             t_e2e = tt.cpu().tolist()
     clocks = clk.summary()
 
-    total_q = nq  # all ranks serve the same nq queries (sharded lists)
+    total_q = nq * world if mode == "replicas" else nq  # replicas: each rank its own batch
     ms_per_step = sum(t_dev) / len(t_dev)
     value = total_q * len(t_dev) / (sum(t_dev) / 1e3)
     e2e_ms = sum(t_e2e) / len(t_e2e)
@@ -408,12 +423,14 @@ def main():
         d2h = nq * k * 12 + nq * 4 + nq * 8
         line = {"metric": METRIC, "value": round(value, 1), "unit": "queries/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
-                "p50_batch_ms": round(statistics.median(t_dev), 4), "higher_is_better": True, "scaling": "strong",
+                "p50_batch_ms": round(statistics.median(t_dev), 4), "higher_is_better": True,
+                "scaling": "weak" if mode == "replicas" else "strong",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config,
                 "e2e": {"value": round(e2e_val, 1), "unit": "queries/s", "ms_per_step": round(e2e_ms, 4),
                         "p50_batch_ms": round(statistics.median(t_e2e), 4), "h2d_bytes_per_step": h2d,
                         "d2h_bytes_per_step": d2h},
-                "gpu_launches": 6 * (args.steps) + (args.steps if world > 1 else 0),
+                # our kernels per timed step: K1, K1b, K2 (+planner), K3, K4; list sharding adds the merge
+                "gpu_launches": 5 * args.steps + (args.steps if mode == "shard-lists" else 0),
                 "roofline": roofline, "roofline_coarse": roofline_coarse, "cpu_baseline": cpu_baseline, "clocks": clocks, "sweep": sweep,
                 "perf_model": perf_models}
         print(json.dumps(line))
