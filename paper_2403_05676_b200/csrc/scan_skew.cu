@@ -457,17 +457,22 @@ template <int M>
 struct SkewCfg;
 template <>
 struct SkewCfg<32> {
-    static constexpr int kWarps = 13;  // consumer warps; + 1 producer + 2 expander warps, 1 CTA per SM
+    // consumer warps; + 1 producer + kExp expander warps, 1 CTA per SM. 12 + 3
+    // measured best (config B K3: 13 + 2 138.6 us, 12 + 3 132.1, 11 + 4 140.1,
+    // 13 + 3 164 -- register spills): with two expanders the consumers waited
+    // on the next item's image ~13% of the time.
+    static constexpr int kWarps = 12;
+    static constexpr int kExp = 3;
     static constexpr int kDepth = 4;   // cp.async ring slots per consumer warp
     static constexpr int kBufs = 2;    // SMEM images: item i+1's is built while item i is scanned
 };
 template <>
 struct SkewCfg<64> {
     static constexpr int kWarps = 12;
+    static constexpr int kExp = 2;
     static constexpr int kDepth = 2;
     static constexpr int kBufs = 1;    // 128 KiB image: single-buffered
 };
-constexpr int kExpWarps = 2;
 
 constexpr uint32_t kEndItem = 0xffffffffu;
 constexpr uint32_t kMinWarpTiles = 4;  // a warp re-reads one tail tile per range: keep ranges >= 4 tiles
@@ -502,7 +507,7 @@ struct SkewSmem {
     static constexpr uint32_t bytes = 232448;                // 227 KiB: the opt-in maximum
     // worst case: a pad just below one ring (nothing fits in it)
     static constexpr uint32_t worst = (kRing - 16) + NB * kImg + kStage + W * kRing + kTail;
-    static constexpr int threads = (W + 1 + kExpWarps) * 32;
+    static constexpr int threads = (W + 1 + SkewCfg<M>::kExp) * 32;
 };
 
 template <int M>
@@ -862,6 +867,7 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
                      uint64_t* __restrict__ pool_id) {
     using L = SkewSmem<M>;
     constexpr int W = L::W, NB = L::NB;
+    constexpr int kExpWarps = SkewCfg<M>::kExp;
     constexpr uint32_t kImgBytes = L::kImg;
     constexpr uint32_t kStageBytes = L::kStage;
     constexpr uint32_t kHalves = M / 32;  // staging rounds per item (32 subquantizers each)
@@ -984,11 +990,13 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
                 // walks the 8 groups of 4 subquantizers diagonally (group
                 // (g + L) mod 8), so every LDS.128 (4 codes of one staged row)
                 // and STS.128 (4 columns of one image row) is conflict-free
-#pragma unroll 1
-                for (uint32_t cb = ew * 128; cb < 256; cb += 128 * kExpWarps) {
-                    const uint32_t c4 = cb + 4 * lane;
+                // units (code block of 128, subquantizer group step): 2 x 8,
+                // dealt round-robin to the expander warps
 #pragma unroll 2
-                    for (uint32_t g = 0; g < 8; ++g) {
+                for (uint32_t u = ew; u < 16; u += kExpWarps) {
+                    const uint32_t c4 = (u >> 3) * 128 + 4 * lane;
+                    {
+                        const uint32_t g = u & 7u;
                         const uint32_t sq0 = 4 * ((g + lane) & 7u);  // local subquantizer group
                         float4 v[4];
 #pragma unroll
