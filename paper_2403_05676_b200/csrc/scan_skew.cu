@@ -468,7 +468,7 @@ struct SkewCfg<32> {
 };
 template <>
 struct SkewCfg<64> {
-    static constexpr int kWarps = 12;
+    static constexpr int kWarps = 12;  // 11 + 3 measured no better for m = 64 (single-buffered image)
     static constexpr int kExp = 2;
     static constexpr int kDepth = 2;
     static constexpr int kBufs = 1;    // 128 KiB image: single-buffered

@@ -24,6 +24,7 @@ ap.add_argument("--n", type=int, default=1_000_000_000)
 ap.add_argument("--nlist", type=int, default=16384)
 ap.add_argument("--m", type=int, default=64)
 ap.add_argument("--reps", type=int, default=7)
+ap.add_argument("--no-model", action="store_true", help="rows only (skip the perf-model budget picks)")
 a = ap.parse_args()
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 hbm = float(json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))["hbm_gbs"])
@@ -65,7 +66,7 @@ def measure(nq, nprobe):
 
 rows = [measure(nq, npb) for nq, npb in [(1, 16), (1, 64), (1, 128), (8, 64), (64, 16), (64, 64)]]
 models = {}
-for nq in (1, 64):
+for nq in (() if a.no_model else (1, 64)):
     m, lat = pg.calibrate_gpu(ix, q[:nq], 10, [1, 4, 16, 64, 128, 256], repeats=5, warmups=2)
     picks = {}
     for budget in (0.5e-3, 1e-3, 2e-3, 5e-3):
