@@ -168,6 +168,20 @@ int prag_gpu_search(prag_gpu_index* index, const float* queries, uint32_t nq, ui
                     uint32_t k, uint64_t* out_ids, float* out_dist, uint32_t* out_count,
                     uint64_t* out_scanned_vectors, void* stream);
 
+/* Exact rerank (SearchParams::exact_rerank, annindex.hpp:307-312): raw
+ * embeddings [n][d] fp32 row-major indexed by chunk id (host or device
+ * pointer; copied into HBM). Every resident chunk id must be < n. n = 0
+ * detaches. */
+int prag_gpu_index_set_embeddings(prag_gpu_index* index, const float* embeddings, uint64_t n);
+/* prag::search(..., {nprobe, k, true}, &embeddings): the probed candidates'
+ * distances replaced by the full-precision squared_l2(embeddings[id], query)
+ * before the (distance, chunk_id) top-k. Same arguments and outputs as
+ * prag_gpu_search; PRAG_GPU_CONFIG "search: exact_rerank requires raw
+ * embeddings" when none are attached. */
+int prag_gpu_search_rerank(prag_gpu_index* index, const float* queries, uint32_t nq, uint32_t nprobe, uint32_t k,
+                           uint64_t* out_ids, float* out_dist, uint32_t* out_count, uint64_t* out_scanned,
+                           void* stream);
+
 /* Coarse quantizer only (annindex.hpp:277-281): the first nprobe lists of
  * each query in (distance, list id) order, out_lists[q*nprobe + p]. */
 int prag_gpu_probe(prag_gpu_index* index, const float* queries, uint32_t nq, uint32_t nprobe,

@@ -145,6 +145,15 @@ public:
 
     prag_gpu_index* handle() const { return h_.get(); }
     std::uint32_t nlist() const { return prag_gpu_index_nlist(h_.get()); }
+    // Raw embeddings [n][d] by chunk id for exact rerank (annindex.hpp:307-312).
+    void set_embeddings(const float* rows, std::uint64_t n) { check(prag_gpu_index_set_embeddings(h_.get(), rows, n)); }
+    void set_embeddings(const std::vector<std::vector<float>>& e) {
+        std::vector<float> flat;
+        for (const auto& r : e) flat.insert(flat.end(), r.begin(), r.end());
+        set_embeddings(flat.data(), e.size());
+        attached_ = &e;
+    }
+    const void* attached() const { return attached_; }
     prag_gpu_index_desc describe() const {
         prag_gpu_index_desc d{};
         check(prag_gpu_index_describe(h_.get(), &d));
@@ -157,21 +166,23 @@ private:
     };
     explicit Index(prag_gpu_index* h) : h_(h) {}
     std::unique_ptr<prag_gpu_index, Free> h_;
+    const void* attached_ = nullptr;  // the embeddings object last given to set_embeddings
 };
 
 // Batch search; queries row-major nq x d (host or device pointer). Returns one
 // SearchResult per query, exactly as nq calls of prag::search would.
+// exact_rerank uses the embeddings attached with Index::set_embeddings
+// (ConfigError "search: exact_rerank requires raw embeddings" otherwise).
 inline std::vector<SearchResult> search_batch(const Index& index, const float* queries, std::uint32_t nq,
                                               SearchParams params, void* stream = nullptr) {
-    if (params.exact_rerank)  // annindex.hpp:269-271; rerank is off on the hot path (pipeline.hpp:228)
-        throw ConfigError("search: exact_rerank requires raw embeddings");
     const std::uint32_t k = params.k;
     std::vector<std::uint64_t> ids(std::size_t(nq) * (k ? k : 1));
     std::vector<float> dist(ids.size());
     std::vector<std::uint32_t> cnt(nq);
     std::vector<std::uint64_t> scanned(nq);
-    check(prag_gpu_search(index.handle(), queries, nq, params.nprobe, k, ids.data(), dist.data(), cnt.data(),
-                          scanned.data(), stream));
+    auto fn = params.exact_rerank ? prag_gpu_search_rerank : prag_gpu_search;
+    check(fn(index.handle(), queries, nq, params.nprobe, k, ids.data(), dist.data(), cnt.data(), scanned.data(),
+             stream));
     std::vector<SearchResult> out(nq);
     for (std::uint32_t q = 0; q < nq; ++q) {
         out[q].scanned_vectors = scanned[q];
@@ -187,6 +198,16 @@ inline std::vector<SearchResult> search_batch(const Index& index, const float* q
 inline SearchResult search(const Index& index, const std::vector<float>& query, SearchParams params) {
     if (query.size() != index.describe().d) throw ConfigError("search: query dimension mismatch");
     return std::move(search_batch(index, query.data(), 1, params)[0]);
+}
+
+// prag::search(index, codebook, query, params, embeddings) (annindex.hpp:262-264):
+// with exact_rerank the embeddings are attached to the device index (once per object).
+inline SearchResult search(Index& index, const std::vector<float>& query, SearchParams params,
+                           const std::vector<std::vector<float>>* embeddings) {
+    if (params.exact_rerank && embeddings == nullptr)  // annindex.hpp:269-271
+        throw ConfigError("search: exact_rerank requires raw embeddings");
+    if (params.exact_rerank && index.attached() != embeddings) index.set_embeddings(*embeddings);
+    return search(static_cast<const Index&>(index), query, params);
 }
 
 // perfmodel.hpp:92-117 fed with the GPU batch-latency curve: host queries in,

@@ -15,6 +15,7 @@
 //   bench   <index> <queries.f32> <nq> <nprobe> <k> <threads> <reps> <warmups> [max_seconds]
 //   calibrate <index> <queries.f32> <nq> <k> <grid_csv> <repeats>
 //   brute   <vectors.f32> <n> <d> <queries.f32> <nq> <k> <out.bin>
+//   rerank  <index> <vectors.f32> <n> <queries.f32> <nq> <nprobe> <k> <out.bin>   (exact_rerank = true)
 //   embed   <tokens.u32> <nchunks> <m> <d> <seed> <out.f32>   (prag::ChunkEmbedder::embed)
 #include <atomic>
 #include <chrono>
@@ -121,6 +122,18 @@ int main(int argc, char** argv) {
             std::vector<prag::SearchResult> res;
             for (const auto& q : qs) res.push_back(prag::search(index, codebook, q, {nprobe, k, false}));
             write_results(argv[7], res, k);
+            return 0;
+        }
+        if (cmd == "rerank" && argc == 10) {  // search with exact_rerank (annindex.hpp:307-312)
+            auto [index, codebook] = prag::load_index(argv[2]);
+            std::size_t n = std::stoull(argv[4]);
+            auto vecs = rows(read_f32(argv[3], n * index.d), n, index.d);
+            std::size_t nq = std::stoull(argv[6]);
+            std::uint32_t nprobe = std::stoul(argv[7]), k = std::stoul(argv[8]);
+            auto qs = rows(read_f32(argv[5], nq * index.d), nq, index.d);
+            std::vector<prag::SearchResult> res;
+            for (const auto& q : qs) res.push_back(prag::search(index, codebook, q, {nprobe, k, true}, &vecs));
+            write_results(argv[9], res, k);
             return 0;
         }
         if (cmd == "brute" && argc == 9) {

@@ -431,9 +431,9 @@ int search_pass_skew(prag_gpu_index* ix, Workspace* w, const float* dq, uint32_t
 // pointers. All launches on stream s.
 int search_pass(prag_gpu_index* ix, Workspace* w, const float* dq, uint32_t nq, uint32_t nprobe, uint32_t k,
                 uint64_t* o_ids, float* o_dist, uint32_t* o_count, uint64_t* o_scanned, cudaStream_t s,
-                prag_gpu_timings* tm) {
+                prag_gpu_timings* tm, bool rerank) {
     const DeviceIndex& d = ix->dev;
-    if (d.code_layout == 1 && k <= 32 && ix->scan_path == 0)
+    if (!rerank && d.code_layout == 1 && k <= 32 && ix->scan_path == 0)
         return search_pass_skew(ix, w, dq, nq, nprobe, k, o_ids, o_dist, o_count, o_scanned, s, tm);
     const uint64_t max_cand_q = ix->top_prefix[nprobe];
     const uint64_t cand_cap = std::max<uint64_t>(1, max_cand_q * nq);
@@ -502,6 +502,7 @@ int search_pass(prag_gpu_index* ix, Workspace* w, const float* dq, uint32_t nq, 
     PG_TRY(launch_plan(d, b, s));
     if (prof) cudaEventRecord(w->ev[3], s);
     PG_TRY(launch_scan(d, b, s, grid, gl));
+    if (rerank) PG_TRY(launch_rerank(d, b, ix->emb, max_cand_q, s));
     if (prof) cudaEventRecord(w->ev[4], s);
     PG_TRY(launch_final(d, b, fkey, ftie, pw_f, s));
     if (prof) {
@@ -547,8 +548,17 @@ int validate(const prag_gpu_index* ix, uint32_t nprobe, uint32_t k) {
 }
 
 int do_search(prag_gpu_index* ix, const float* queries, uint32_t nq, uint32_t nprobe, uint32_t k,
-              uint64_t* out_ids, float* out_dist, uint32_t* out_count, uint64_t* out_scanned, cudaStream_t s) {
+              uint64_t* out_ids, float* out_dist, uint32_t* out_count, uint64_t* out_scanned, cudaStream_t s,
+              bool rerank = false) {
     PG_TRY(validate(ix, nprobe, k));
+    if (rerank && !ix->emb) {  // annindex.hpp:269-271
+        set_error("search: exact_rerank requires raw embeddings");
+        return PRAG_GPU_CONFIG;
+    }
+    if (rerank && !ix->dev.plain_codes) {
+        set_error("search: exact_rerank needs the plain code layout (not a device-built synthetic index)");
+        return PRAG_GPU_CONFIG;
+    }
     if (nq == 0) return PRAG_GPU_OK;
     if (!queries || !out_ids || !out_dist || !out_count) {
         set_error("search: null query/output pointer");
@@ -563,7 +573,7 @@ int do_search(prag_gpu_index* ix, const float* queries, uint32_t nq, uint32_t np
     const uint64_t max_cand_q = std::max<uint64_t>(1, ix->top_prefix[nprobe]);
     const uint64_t kSlots = 192ull << 20;
     uint32_t chunk = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(nq, kSlots / max_cand_q)));
-    if (d.code_layout == 1 && k <= 32 && ix->scan_path == 0) {
+    if (!rerank && d.code_layout == 1 && k <= 32 && ix->scan_path == 0) {
         // fast path: bound the per-pass LUT images (nq * nprobe * m * 2 KiB) to ~1 GiB
         const uint64_t img_q = uint64_t(nprobe) * skew_lut_bytes(d.nsq);
         chunk = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(nq, (1ull << 30) / img_q)));
@@ -619,7 +629,7 @@ int do_search(prag_gpu_index* ix, const float* queries, uint32_t nq, uint32_t np
             oc = cv.take<uint32_t>(n);
             os = cv.take<uint64_t>(n);
         }
-        PG_TRY(search_pass(ix, w, dq, n, nprobe, k, oi, od, oc, os, s, tmp));
+        PG_TRY(search_pass(ix, w, dq, n, nprobe, k, oi, od, oc, os, s, tmp, rerank));
         if (!o_dev) {
             // device -> pinned -> caller
             char* h = static_cast<char*>(w->host);
@@ -860,6 +870,7 @@ void prag_gpu_index_free(prag_gpu_index* ix) {
             delete w;
         }
         free_device_index(ix->dev);
+        cudaFree(ix->emb);
     }
     delete ix;
 }
@@ -905,6 +916,56 @@ int prag_gpu_search(prag_gpu_index* ix, const float* queries, uint32_t nq, uint3
     }
     return do_search(ix, queries, nq, nprobe, k, out_ids, out_dist, out_count, out_scanned,
                      static_cast<cudaStream_t>(stream));
+}
+
+int prag_gpu_search_rerank(prag_gpu_index* ix, const float* queries, uint32_t nq, uint32_t nprobe, uint32_t k,
+                           uint64_t* out_ids, float* out_dist, uint32_t* out_count, uint64_t* out_scanned,
+                           void* stream) {
+    if (!ix) {
+        set_error("null index");
+        return PRAG_GPU_CONFIG;
+    }
+    return do_search(ix, queries, nq, nprobe, k, out_ids, out_dist, out_count, out_scanned,
+                     static_cast<cudaStream_t>(stream), true);
+}
+
+int prag_gpu_index_set_embeddings(prag_gpu_index* ix, const float* emb, uint64_t n) {
+    if (!ix || (!emb && n)) {
+        set_error("null argument");
+        return PRAG_GPU_CONFIG;
+    }
+    DeviceGuard g(ix->device);
+    PG_CUDA(cudaDeviceSynchronize());
+    cudaFree(ix->emb);
+    ix->emb = nullptr;
+    ix->emb_n = 0;
+    if (n == 0) return PRAG_GPU_OK;
+    // every resident chunk id must have a row (annindex.hpp:310 indexes by chunk id)
+    uint64_t max_id = 0;
+    {
+        const size_t npad = ix->dev.npadded;
+        std::vector<uint64_t> h(npad);
+        PG_CUDA(cudaMemcpy(h.data(), ix->dev.ids, npad * 8, cudaMemcpyDeviceToHost));
+        for (uint64_t v : h)
+            if (v != ~0ull && v > max_id) max_id = v;
+    }
+    if (ix->dev.ntotal && max_id >= n) {
+        set_error("set_embeddings: chunk id " + std::to_string(max_id) + " has no embedding row (n = " +
+                  std::to_string(n) + ")");
+        return PRAG_GPU_CONFIG;
+    }
+    const size_t bytes = size_t(n) * ix->dev.d * 4;
+    float* e = nullptr;
+    PG_CUDA(cudaMalloc(&e, bytes));
+    const cudaError_t err = cudaMemcpy(e, emb, bytes, cudaMemcpyDefault);
+    if (err != cudaSuccess) {
+        cudaFree(e);
+        set_error(std::string("CUDA error (set_embeddings): ") + cudaGetErrorString(err));
+        return PRAG_GPU_CUDA;
+    }
+    ix->emb = e;
+    ix->emb_n = n;
+    return PRAG_GPU_OK;
 }
 
 int prag_gpu_probe(prag_gpu_index* ix, const float* queries, uint32_t nq, uint32_t nprobe, uint32_t* out_lists,

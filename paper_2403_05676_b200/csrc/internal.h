@@ -146,6 +146,8 @@ struct prag_gpu_index {
     int scan_path = 0;                            // 0 auto, 1 force generic
     int coarse_path = 0;                          // 0 auto (tensor cores when eligible), 1 force exact SIMT
     prag_gpu_timings last{};
+    float* emb = nullptr;                         // raw embeddings [emb_n][d] for exact rerank (annindex.hpp:307-312)
+    uint64_t emb_n = 0;
     std::mutex mu;                                // guards pool and `last`
     std::vector<pg::Workspace*> pool;
 };
@@ -181,6 +183,10 @@ int launch_select_probe(const DeviceIndex& ix, const float* coarse, uint32_t nq,
                         uint32_t* probe, float* probe_dist, uint32_t* gkey, uint64_t* gtie, cudaStream_t s);
 int launch_plan(const DeviceIndex& ix, const SearchBuffers& b, cudaStream_t s);
 int launch_scan(const DeviceIndex& ix, const SearchBuffers& b, cudaStream_t s, int grid, float* glut);
+// exact rerank (annindex.hpp:307-312): every candidate's distance becomes
+// squared_l2(emb[chunk_id], q) at full precision; max_cand_q bounds a query's candidates
+int launch_rerank(const DeviceIndex& ix, const SearchBuffers& b, const float* emb, uint64_t max_cand_q,
+                  cudaStream_t s);
 int launch_final(const DeviceIndex& ix, const SearchBuffers& b, uint32_t* gkey, uint64_t* gtie, uint32_t pw,
                  cudaStream_t s);
 int launch_merge(const uint64_t* ids, const float* dist, const uint32_t* count, const uint64_t* scanned,

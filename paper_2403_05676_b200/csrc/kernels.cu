@@ -861,6 +861,58 @@ int launch_scan(const DeviceIndex& ix, const SearchBuffers& b, cudaStream_t s, i
     return check_launch("scan");
 }
 
+namespace {
+// One thread per candidate of query blockIdx.y: the full-precision
+// squared_l2(embeddings[chunk_id], query) of common.hpp:73-80, in the
+// argument order of annindex.hpp:310 (diff = e - q), FMA-free.
+__global__ void __launch_bounds__(256) rerank_kernel(const float* __restrict__ queries, uint32_t d,
+                                                     const uint64_t* __restrict__ q_cand_off,
+                                                     const uint32_t* __restrict__ cand_entry,
+                                                     const uint64_t* __restrict__ ids, const float* __restrict__ emb,
+                                                     float* __restrict__ cand_dist) {
+    extern __shared__ float qs[];
+    const uint32_t q = blockIdx.y;
+    for (uint32_t j = threadIdx.x; j < d; j += blockDim.x) qs[j] = queries[size_t(q) * d + j];
+    __syncthreads();
+    const uint64_t b0 = q_cand_off[q], b1 = q_cand_off[q + 1];
+    const uint64_t o = b0 + uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (o >= b1) return;
+    const float* row = emb + size_t(ids[cand_entry[o]]) * d;
+    float acc = 0.0f;
+    if ((d & 3u) == 0) {
+        const float4* r4 = reinterpret_cast<const float4*>(row);
+        for (uint32_t j4 = 0; j4 < d / 4; ++j4) {
+            const float4 e = __ldg(r4 + j4);
+            const float ev[4] = {e.x, e.y, e.z, e.w};
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const float diff = __fsub_rn(ev[t], qs[4 * j4 + t]);
+                acc = __fadd_rn(acc, __fmul_rn(diff, diff));
+            }
+        }
+    } else {
+        for (uint32_t j = 0; j < d; ++j) {
+            const float diff = __fsub_rn(__ldg(row + j), qs[j]);
+            acc = __fadd_rn(acc, __fmul_rn(diff, diff));
+        }
+    }
+    cand_dist[o] = acc;
+}
+}  // namespace
+
+int launch_rerank(const DeviceIndex& ix, const SearchBuffers& b, const float* emb, uint64_t max_cand_q,
+                  cudaStream_t s) {
+    if (b.nq == 0 || max_cand_q == 0) return PRAG_GPU_OK;
+    const uint64_t gx = (max_cand_q + 255) / 256;
+    if (gx > 0x7fffffffull) {
+        set_error("rerank: too many candidates per query");
+        return PRAG_GPU_CONFIG;
+    }
+    rerank_kernel<<<dim3(uint32_t(gx), b.nq), 256, size_t(ix.d) * 4, s>>>(b.queries, ix.d, b.q_cand_off,
+                                                                          b.cand_entry, ix.ids, emb, b.cand_dist);
+    return check_launch("rerank");
+}
+
 int launch_final(const DeviceIndex& ix, const SearchBuffers& b, uint32_t* gkey, uint64_t* gtie, uint32_t pw,
                  cudaStream_t s) {
     PG_TRY(set_sel_smem(reinterpret_cast<const void*>(select_final_kernel)));

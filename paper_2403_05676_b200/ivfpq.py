@@ -163,11 +163,28 @@ class GpuIndex:
         check(lib().prag_gpu_index_list_sizes(self._h, _ptr(out)))
         return out
 
-    def search_batch(self, queries, k: int, nprobe: int, stream=None, out: Optional[BatchResult] = None
-                     ) -> BatchResult:
+    def set_embeddings(self, embeddings) -> None:
+        """Raw embeddings [n, d] (indexed by chunk id) for exact rerank
+        (annindex.hpp:307-312); None detaches."""
+        if embeddings is None:
+            check(lib().prag_gpu_index_set_embeddings(self._h, None, 0))
+            self._emb_key = None
+            return
+        if torch is not None and isinstance(embeddings, torch.Tensor) and embeddings.is_cuda:
+            e = embeddings.contiguous()
+            n = e.shape[0]
+        else:
+            e = np.ascontiguousarray(embeddings, dtype=np.float32).reshape(-1, self.d)
+            n = e.shape[0]
+        check(lib().prag_gpu_index_set_embeddings(self._h, _ptr(e), n))
+        self._emb_key = id(embeddings)
+
+    def search_batch(self, queries, k: int, nprobe: int, stream=None, out: Optional[BatchResult] = None,
+                     exact_rerank: bool = False) -> BatchResult:
         """Batch prag::search: queries [nq, d] float32, host (numpy / CPU tensor)
         or device (CUDA tensor). Device queries -> device outputs, asynchronous
-        on `stream` (default: torch's current stream)."""
+        on `stream` (default: torch's current stream). exact_rerank uses the
+        embeddings given to set_embeddings()."""
         on_dev = torch is not None and isinstance(queries, torch.Tensor) and queries.is_cuda
         if on_dev:
             q = queries.contiguous()
@@ -191,8 +208,9 @@ class GpuIndex:
                                   np.zeros(nq, dtype=np.uint32), np.zeros(nq, dtype=np.uint64))
         if (not on_dev) and q.shape[1] != self.d:
             raise ConfigError(f"query dimension {q.shape[1]} != index d {self.d}")
-        check(lib().prag_gpu_search(self._h, _ptr(q), nq, nprobe, k, _ptr(out.ids), _ptr(out.dist),
-                                    _ptr(out.count), _ptr(out.scanned), _stream_ptr(stream)))
+        fn = lib().prag_gpu_search_rerank if exact_rerank else lib().prag_gpu_search
+        check(fn(self._h, _ptr(q), nq, nprobe, k, _ptr(out.ids), _ptr(out.dist), _ptr(out.count),
+                 _ptr(out.scanned), _stream_ptr(stream)))
         return out
 
     def probe(self, queries, nprobe: int):
@@ -327,12 +345,12 @@ def load_index(path: str, device: int = 0) -> GpuIndex:
 def search(index: GpuIndex, query, params: SearchParams, embeddings=None) -> SearchResult:
     """prag::search (annindex.hpp:262-315) for one query."""
     if params.exact_rerank:
-        # annindex.hpp:269-271 error path; rerank is off on the hot path
-        # (pipeline.hpp:228) and not offered by the GPU build.
-        if embeddings is None:
+        if embeddings is None:  # annindex.hpp:269-271
             raise ConfigError("search: exact_rerank requires raw embeddings")
-        raise ConfigError("search: exact_rerank is not supported by the GPU path")
-    r = index.search_batch(np.asarray(query, dtype=np.float32).reshape(1, -1), params.k, params.nprobe)
+        if getattr(index, "_emb_key", None) != id(embeddings):
+            index.set_embeddings(embeddings)
+    r = index.search_batch(np.asarray(query, dtype=np.float32).reshape(1, -1), params.k, params.nprobe,
+                           exact_rerank=params.exact_rerank)
     return r.result(0, params.nprobe)
 
 
