@@ -617,6 +617,7 @@ int do_search(prag_gpu_index* ix, const float* queries, uint32_t nq, uint32_t np
         float* od;
         uint32_t* oc;
         uint64_t* os;
+        size_t stage_out_bytes = 0;
         if (o_dev) {
             oi = out_ids + size_t(q0) * k;
             od = out_dist + size_t(q0) * k;
@@ -628,20 +629,19 @@ int do_search(prag_gpu_index* ix, const float* queries, uint32_t nq, uint32_t np
             od = cv.take<float>(size_t(n) * k);
             oc = cv.take<uint32_t>(n);
             os = cv.take<uint64_t>(n);
+            stage_out_bytes = cv.off;
         }
         PG_TRY(search_pass(ix, w, dq, n, nprobe, k, oi, od, oc, os, s, tmp, rerank));
         if (!o_dev) {
-            // device -> pinned -> caller
+            // device -> pinned -> caller: the four outputs sit in one staged
+            // block, so one copy brings them back (same carve offsets)
             char* h = static_cast<char*>(w->host);
             Carver hv{h};
             uint64_t* hi = hv.take<uint64_t>(size_t(n) * k);
             float* hd = hv.take<float>(size_t(n) * k);
             uint32_t* hc = hv.take<uint32_t>(n);
             uint64_t* hs = hv.take<uint64_t>(n);
-            PG_CUDA(cudaMemcpyAsync(hi, oi, size_t(n) * k * 8, cudaMemcpyDeviceToHost, s));
-            PG_CUDA(cudaMemcpyAsync(hd, od, size_t(n) * k * 4, cudaMemcpyDeviceToHost, s));
-            PG_CUDA(cudaMemcpyAsync(hc, oc, size_t(n) * 4, cudaMemcpyDeviceToHost, s));
-            PG_CUDA(cudaMemcpyAsync(hs, os, size_t(n) * 8, cudaMemcpyDeviceToHost, s));
+            PG_CUDA(cudaMemcpyAsync(h, do_stage, stage_out_bytes, cudaMemcpyDeviceToHost, s));
             PG_CUDA(cudaStreamSynchronize(s));
             std::memcpy(out_ids + size_t(q0) * k, hi, size_t(n) * k * 8);
             std::memcpy(out_dist + size_t(q0) * k, hd, size_t(n) * k * 4);
