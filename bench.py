@@ -237,9 +237,17 @@ def main():
     qdev = torch.from_numpy(queries[:nq]).to(dev)
     from paper_2403_05676_b200 import distributed as PD
 
+    out_bufs = {}  # device result buffers per (nq, k), reused across steps as a serving loop would
+
     def step_dev(qd, nprobe_, k_):
+        key = (qd.shape[0], k_)
+        if key not in out_bufs:
+            out_bufs[key] = pg.BatchResult(torch.empty(key, dtype=torch.int64, device=dev),
+                                           torch.empty(key, dtype=torch.float32, device=dev),
+                                           torch.empty((key[0],), dtype=torch.int32, device=dev),
+                                           torch.empty((key[0],), dtype=torch.int64, device=dev))
         with torch.cuda.stream(stream):
-            r = ix.search_batch(qd, k_, nprobe_, stream=stream)
+            r = ix.search_batch(qd, k_, nprobe_, stream=stream, out=out_bufs[key])
             if mode == "shard-lists":  # one packed NCCL all-gather of the per-shard top-k, exact merge on rank 0
                 r = PD.gather_merge(r, k_)
         return r
