@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(kWinThreads) select_window_kernel(
     unsigned long long* __restrict__ win_stat) {
     extern __shared__ __align__(1024) unsigned char sm[];
     uint32_t* hist = reinterpret_cast<uint32_t*>(sm);          // [256]
-    uint32_t* misc = hist + 256;                               // [8]: [1] rank, [2..3] selected key, [4] count, [5..6] two-level U
+    uint32_t* misc = hist + 256;                               // [8]: [1] rank, [2..3] selected key, [4] count, [5..7] two-level U
     uint32_t* win = misc + 8;                                  // [kWinCap] list ids
     float* wd = reinterpret_cast<float*>(win + kWinCap);       // [kWinCap] exact distances
     float* sq = wd + kWinCap;                                  // [d] the query
@@ -454,7 +454,35 @@ __global__ void __launch_bounds__(kWinThreads) select_window_kernel(
         uint32_t kmin[1] = {key[0]};
 #pragma unroll
         for (uint32_t i = 1; i < VPT; ++i) kmin[0] = min(kmin[0], key[i]);
-        const uint32_t ub = block_select_kth<1>(kmin, kWinThreads, nprobe, hist, misc);
+        uint32_t ub;
+        if (nprobe <= 32) {
+            // G >= nprobe groups of s lanes (s a power of two <= 32): the
+            // nprobe-th smallest group minimum is itself >= U (an order
+            // statistic of a subset), found by one warp ranking <= 32 values
+            uint32_t sz = 32;
+            while (sz > 1 && kWinThreads / (sz / 2) <= 32 && kWinThreads / sz < nprobe) sz >>= 1;
+            // (kWinThreads / sz groups; sz = 32 gives 16 groups)
+            const uint32_t G = kWinThreads / sz;
+            uint32_t gm = kmin[0];
+            for (uint32_t o = 1; o < sz; o <<= 1) gm = min(gm, __shfl_xor_sync(0xffffffffu, gm, o));
+            if ((tid & (sz - 1)) == 0) hist[tid / sz] = gm;  // hist[] is free until the radix fallback
+            __syncthreads();
+            if (tid < 32) {
+                const uint32_t lane = tid;
+                const uint32_t v = lane < G ? hist[lane] : 0xffffffffu;
+                uint32_t less = 0, eq = 0;
+                for (uint32_t j = 0; j < 32; ++j) {
+                    const uint32_t x = __shfl_sync(0xffffffffu, v, j);
+                    less += x < v;
+                    eq += x == v;
+                }
+                if (lane < G && less < nprobe && nprobe <= less + eq) misc[7] = v;
+            }
+            __syncthreads();
+            ub = misc[7];
+        } else {
+            ub = block_select_kth<1>(kmin, kWinThreads, nprobe, hist, misc);
+        }
         uint32_t* cand = reinterpret_cast<uint32_t*>(wd);  // scratch until the window is rescored
         if (tid == 0) misc[5] = 0;
         __syncthreads();
@@ -524,11 +552,13 @@ __global__ void __launch_bounds__(kWinThreads) select_window_kernel(
         auto stage_batch = [&](uint32_t b0, uint32_t buf) {
             const uint32_t nb = min(kStageRows, W - b0);
             float* dst = rows + buf * kStageRows * rs;
-            for (uint32_t idx = tid; idx < nb * d; idx += kWinThreads) {
-                const uint32_t r = idx / d, j = idx - r * d;
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst + r * rs + j)),
-                             "l"(centroids + size_t(win[b0 + r]) * d + j)
-                             : "memory");
+            // warp w stages rows w, w + 16, ...; lanes stride the row (no division)
+            for (uint32_t r = tid >> 5; r < nb; r += kWinThreads / 32) {
+                const float* src = centroids + size_t(win[b0 + r]) * d;
+                const uint32_t drow = smem_addr(dst + r * rs);
+                for (uint32_t j = tid & 31u; j < d; j += 32)
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(drow + 4 * j), "l"(src + j)
+                                 : "memory");
             }
             asm volatile("cp.async.commit_group;" ::: "memory");
         };
