@@ -1076,11 +1076,11 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
 
 uint32_t skew_item_tiles(uint64_t est_tiles, uint32_t grid) {
     // enough items for ~per_cta per CTA, within [kMinItemTiles, kMaxItemTiles]
-    // (PRAG_GPU_ITEMS_PER_CTA overrides the default of 3; tuning knob)
+    // (PRAG_GPU_ITEMS_PER_CTA overrides the default of 1, best in tools/sweep_items.sh; tuning knob)
     static const uint64_t per_cta = [] {
         const char* e = getenv("PRAG_GPU_ITEMS_PER_CTA");
         const long v = e ? atol(e) : 0;
-        return uint64_t(v > 0 ? v : 3);
+        return uint64_t(v > 0 ? v : 1);
     }();
     uint64_t want = est_tiles / (uint64_t(grid) * per_cta + 1);
     uint32_t it = kMinItemTiles;
