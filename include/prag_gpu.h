@@ -182,6 +182,13 @@ int prag_gpu_search_rerank(prag_gpu_index* index, const float* queries, uint32_t
                            uint64_t* out_ids, float* out_dist, uint32_t* out_count, uint64_t* out_scanned,
                            void* stream);
 
+/* prag::brute_force_search (annindex.hpp:244-257) on the device: exact
+ * top-k of n rows [n][d] (host or device) by full-precision squared L2 in the
+ * reference's rounding, ties by lower row id; outputs [nq][k] host or device.
+ * For recall evaluation (acceptance C1/C2), not the serving path. */
+int prag_gpu_brute_force(const float* vectors, uint64_t n, uint32_t d, const float* queries, uint32_t nq,
+                         uint32_t k, int device, uint64_t* out_ids, float* out_dist, uint32_t* out_count);
+
 /* Coarse quantizer only (annindex.hpp:277-281): the first nprobe lists of
  * each query in (distance, list id) order, out_lists[q*nprobe + p]. */
 int prag_gpu_probe(prag_gpu_index* index, const float* queries, uint32_t nq, uint32_t nprobe,

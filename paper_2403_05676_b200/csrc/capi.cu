@@ -968,6 +968,59 @@ int prag_gpu_index_set_embeddings(prag_gpu_index* ix, const float* emb, uint64_t
     return PRAG_GPU_OK;
 }
 
+int prag_gpu_brute_force(const float* vectors, uint64_t n, uint32_t d, const float* queries, uint32_t nq,
+                         uint32_t k, int device, uint64_t* out_ids, float* out_dist, uint32_t* out_count) {
+    if (k < 1) {  // annindex.hpp:246
+        set_error("brute_force_search: k must be >= 1");
+        return PRAG_GPU_CONFIG;
+    }
+    if (nq == 0) return PRAG_GPU_OK;
+    if ((!vectors && n) || !queries || !out_ids || !out_dist || !out_count || d == 0) {
+        set_error("null argument");
+        return PRAG_GPU_CONFIG;
+    }
+    if (n > 0xffffffffull) {
+        set_error("brute_force_search: the device path takes n < 2^32 rows");
+        return PRAG_GPU_CONFIG;
+    }
+    PG_TRY(require_device(device));
+    DeviceGuard g(device);
+    struct Bufs {
+        void* p[8] = {};
+        ~Bufs() {
+            for (void* x : p) cudaFree(x);
+        }
+    } b;
+    const float* emb = vectors;
+    if (!is_device_ptr(vectors) && n) {
+        PG_CUDA(cudaMalloc(&b.p[0], size_t(n) * d * 4));
+        PG_CUDA(cudaMemcpy(b.p[0], vectors, size_t(n) * d * 4, cudaMemcpyHostToDevice));
+        emb = static_cast<float*>(b.p[0]);
+    }
+    const uint32_t pw = pow2_at_least(k);
+    // queries per pass: the [chunk][n] distance scratch stays <= 1 GiB
+    const uint32_t chunk = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(nq, (1ull << 28) / std::max<uint64_t>(n, 1))));
+    PG_CUDA(cudaMalloc(&b.p[1], std::max<size_t>(size_t(chunk) * n * 4, 4)));
+    PG_CUDA(cudaMalloc(&b.p[2], size_t(chunk) * pw * 4));
+    PG_CUDA(cudaMalloc(&b.p[3], size_t(chunk) * pw * 8));
+    PG_CUDA(cudaMalloc(&b.p[4], size_t(chunk) * d * 4));
+    PG_CUDA(cudaMalloc(&b.p[5], size_t(chunk) * k * 8));
+    PG_CUDA(cudaMalloc(&b.p[6], size_t(chunk) * k * 4));
+    PG_CUDA(cudaMalloc(&b.p[7], size_t(chunk) * 4));
+    for (uint32_t q0 = 0; q0 < nq; q0 += chunk) {
+        const uint32_t m = std::min(chunk, nq - q0);
+        PG_CUDA(cudaMemcpy(b.p[4], queries + size_t(q0) * d, size_t(m) * d * 4, cudaMemcpyDefault));
+        PG_TRY(launch_brute_force(emb, n, d, static_cast<float*>(b.p[4]), m, k, static_cast<float*>(b.p[1]),
+                                  static_cast<uint32_t*>(b.p[2]), static_cast<uint64_t*>(b.p[3]), pw,
+                                  static_cast<uint64_t*>(b.p[5]), static_cast<float*>(b.p[6]),
+                                  static_cast<uint32_t*>(b.p[7]), nullptr));
+        PG_CUDA(cudaMemcpy(out_ids + size_t(q0) * k, b.p[5], size_t(m) * k * 8, cudaMemcpyDefault));
+        PG_CUDA(cudaMemcpy(out_dist + size_t(q0) * k, b.p[6], size_t(m) * k * 4, cudaMemcpyDefault));
+        PG_CUDA(cudaMemcpy(out_count + q0, b.p[7], size_t(m) * 4, cudaMemcpyDefault));
+    }
+    return PRAG_GPU_OK;
+}
+
 int prag_gpu_probe(prag_gpu_index* ix, const float* queries, uint32_t nq, uint32_t nprobe, uint32_t* out_lists,
                    float* out_dist, void* stream) {
     if (!ix) {

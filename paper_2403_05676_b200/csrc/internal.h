@@ -187,6 +187,11 @@ int launch_scan(const DeviceIndex& ix, const SearchBuffers& b, cudaStream_t s, i
 // squared_l2(emb[chunk_id], q) at full precision; max_cand_q bounds a query's candidates
 int launch_rerank(const DeviceIndex& ix, const SearchBuffers& b, const float* emb, uint64_t max_cand_q,
                   cudaStream_t s);
+// brute_force_search (annindex.hpp:244-257) for nq device queries over n device rows;
+// dist is [nq][n] scratch, gkey/gtie [nq][pw] with pw = pow2 >= k
+int launch_brute_force(const float* emb, uint64_t n, uint32_t d, const float* queries, uint32_t nq, uint32_t k,
+                       float* dist, uint32_t* gkey, uint64_t* gtie, uint32_t pw, uint64_t* out_ids, float* out_dist,
+                       uint32_t* out_count, cudaStream_t s);
 int launch_final(const DeviceIndex& ix, const SearchBuffers& b, uint32_t* gkey, uint64_t* gtie, uint32_t pw,
                  cudaStream_t s);
 int launch_merge(const uint64_t* ids, const float* dist, const uint32_t* count, const uint64_t* scanned,

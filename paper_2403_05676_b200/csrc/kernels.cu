@@ -900,6 +900,59 @@ __global__ void __launch_bounds__(256) rerank_kernel(const float* __restrict__ q
 }
 }  // namespace
 
+namespace {
+// brute_force_search (annindex.hpp:244-257): the full-precision distance of
+// every row, then the (distance, row id) top-k.
+__global__ void __launch_bounds__(256) brute_dist_kernel(const float* __restrict__ emb, uint64_t n, uint32_t d,
+                                                         const float* __restrict__ queries,
+                                                         float* __restrict__ dist) {
+    extern __shared__ float qs[];
+    const uint32_t q = blockIdx.y;
+    for (uint32_t j = threadIdx.x; j < d; j += blockDim.x) qs[j] = queries[size_t(q) * d + j];
+    __syncthreads();
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float* row = emb + i * d;
+    float acc = 0.0f;
+    for (uint32_t j = 0; j < d; ++j) {  // squared_l2(embeddings[i], query): diff = e - q
+        const float diff = __fsub_rn(__ldg(row + j), qs[j]);
+        acc = __fadd_rn(acc, __fmul_rn(diff, diff));
+    }
+    dist[size_t(q) * n + i] = acc;
+}
+
+struct RowSrc {
+    const float* d;
+    __device__ uint32_t key(uint32_t i) const { return ord_key(d[i]); }
+    __device__ uint64_t tie(uint32_t i) const { return i; }
+};
+
+__global__ void __launch_bounds__(kSelThreads) brute_select_kernel(const float* __restrict__ dist, uint32_t n,
+                                                                   uint32_t k, uint32_t* gkey, uint64_t* gtie,
+                                                                   uint32_t pw, float* __restrict__ out_dist,
+                                                                   uint64_t* __restrict__ out_ids,
+                                                                   uint32_t* __restrict__ out_count) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    SelShared& sm = *reinterpret_cast<SelShared*>(smraw);
+    const uint32_t q = blockIdx.x;
+    block_topk(RowSrc{dist + size_t(q) * n}, n, k, sm, gkey + size_t(q) * pw, gtie + size_t(q) * pw,
+               out_dist + size_t(q) * k, out_ids + size_t(q) * k, out_count + q);
+}
+}  // namespace
+
+int launch_brute_force(const float* emb, uint64_t n, uint32_t d, const float* queries, uint32_t nq, uint32_t k,
+                       float* dist, uint32_t* gkey, uint64_t* gtie, uint32_t pw, uint64_t* out_ids, float* out_dist,
+                       uint32_t* out_count, cudaStream_t s) {
+    if (nq == 0) return PRAG_GPU_OK;
+    brute_dist_kernel<<<dim3(uint32_t((n + 255) / 256), nq), 256, size_t(d) * 4, s>>>(emb, n, d, queries, dist);
+    PG_TRY(check_launch("brute_dist"));
+    PG_CUDA(cudaFuncSetAttribute(brute_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(sizeof(SelShared))));
+    brute_select_kernel<<<nq, kSelThreads, sizeof(SelShared), s>>>(dist, uint32_t(n), k, gkey, gtie, pw, out_dist,
+                                                                   out_ids, out_count);
+    return check_launch("brute_select");
+}
+
 int launch_rerank(const DeviceIndex& ix, const SearchBuffers& b, const float* emb, uint64_t max_cand_q,
                   cudaStream_t s) {
     if (b.nq == 0 || max_cand_q == 0) return PRAG_GPU_OK;

@@ -354,6 +354,27 @@ def search(index: GpuIndex, query, params: SearchParams, embeddings=None) -> Sea
     return r.result(0, params.nprobe)
 
 
+def brute_force_search(vectors, queries, k: int, device: int = 0) -> BatchResult:
+    """prag::brute_force_search (annindex.hpp:244-257) for a batch, on the
+    device: exact top-k by full-precision squared L2, ties by lower row id."""
+    v = np.ascontiguousarray(vectors, dtype=np.float32)
+    q = np.ascontiguousarray(queries, dtype=np.float32).reshape(-1, v.shape[1])
+    nq = q.shape[0]
+    out = BatchResult(np.zeros((nq, k), dtype=np.uint64), np.zeros((nq, k), dtype=np.float32),
+                      np.zeros(nq, dtype=np.uint32), np.full(nq, v.shape[0], dtype=np.uint64))
+    check(lib().prag_gpu_brute_force(_ptr(v), v.shape[0], v.shape[1], _ptr(q), nq, k, device, _ptr(out.ids),
+                                     _ptr(out.dist), _ptr(out.count)))
+    return out
+
+
+def recall_at_k(approx: SearchResult, exact: SearchResult) -> float:
+    """annindex.hpp:317-327: |approx ∩ exact| / |exact| over chunk ids (1.0 if exact is empty)."""
+    if not exact.neighbors:
+        return 1.0
+    got = {n.chunk_id for n in approx.neighbors}
+    return sum(1 for e in exact.neighbors if e.chunk_id in got) / len(exact.neighbors)
+
+
 # ------------------------------------------------------------ multi-GPU
 def plan_shards(list_sizes: Sequence[int], world: int) -> np.ndarray:
     s = np.ascontiguousarray(list_sizes, dtype=np.uint64)

@@ -3,7 +3,8 @@ the GPU build: the reference's data recipe (SplitMix64(104) Gaussian mixture,
 bit-exact through the oracle's SplitMix64), the index from
 prag_gpu_train_index (bit-exact with train_index, tests/test_gpu_train.py),
 searches with exact_rerank (prag_gpu_search_rerank) and recall@2 against the
-brute-force top-2 (annindex.hpp:244-257, the oracle). Recall must be
+brute-force top-2 (annindex.hpp:244-257; prag_gpu_brute_force, itself
+checked against the oracle) via recall_at_k (annindex.hpp:317-327). Recall must be
 non-decreasing in nprobe and >= 0.8 at nprobe = nlist/4 -- the reference's
 own pass condition."""
 import os
@@ -46,19 +47,20 @@ def test_acceptance_c2_recall_monotone_in_nprobe():
     t = pg.train_index(pts, pg.TrainParams(nlist=64))
     ix = t.to_gpu()
     ix.set_embeddings(pts)
+    # exact top-2 on the GPU (brute_force_search), checked against the oracle
+    bf = pg.brute_force_search(pts, qs, 2)
     exact = []
-    for q in qs:
+    for i, q in enumerate(qs):
         ids = np.zeros(2, np.uint64)
         dist = np.zeros(2, np.float32)
         cnt = np.zeros(1, np.uint32)
         assert O.lib().ora_brute_force(O._p(pts), 20000, 32, O._p(q), 2, O._p(ids), O._p(dist), O._p(cnt)) == 0
-        exact.append(set(int(x) for x in ids[:int(cnt[0])]))
+        assert (bf.ids[i] == ids).all() and (bf.dist[i].view(np.uint32) == dist.view(np.uint32)).all()
+        exact.append(bf.result(i, 0))
     curve = []
     for nprobe in (1, 2, 4, 8, 16, 32, 64):
         r = ix.search_batch(qs, 2, nprobe, exact_rerank=True)
-        rec = [len(exact[i] & set(int(x) for x in r.ids[i, :int(r.count[i])])) / len(exact[i])
-               for i in range(len(qs))]
-        curve.append(float(np.mean(rec)))
+        curve.append(float(np.mean([pg.recall_at_k(r.result(i, nprobe), exact[i]) for i in range(len(qs))])))
     print("recall@2 curve:", curve)
     assert all(b >= a - 1e-12 for a, b in zip(curve, curve[1:])), curve
     assert curve[4] >= 0.8, curve
@@ -66,3 +68,26 @@ def test_acceptance_c2_recall_monotone_in_nprobe():
     # the reference's own run of criterion 2 prints "recall curve: 0.995 1 1 1 1 1 1"
     # (acceptance.cpp compiled from /root/reference with the Release flags)
     assert curve == [0.995, 1.0, 1.0, 1.0, 1.0, 1.0, 1.0], curve
+
+
+def test_brute_force_ties_and_errors():
+    """Ties by lower row id (duplicated rows), k > n, and the k >= 1 check."""
+    import _oracle as O
+    import paper_2403_05676_b200 as pg
+    base = O.random_vectors(50, 24, 9)
+    v = np.concatenate([base, base, base[:7]]).astype(np.float32)  # exact duplicates
+    q = O.noisy_queries(v, 6, 4, 0.05)
+    for k in (1, 5, 200):
+        r = pg.brute_force_search(v, q, k)
+        for i in range(len(q)):
+            ids = np.zeros(k, np.uint64)
+            dist = np.zeros(k, np.float32)
+            cnt = np.zeros(1, np.uint32)
+            assert O.lib().ora_brute_force(O._p(v), len(v), 24, O._p(q[i]), k, O._p(ids), O._p(dist),
+                                           O._p(cnt)) == 0
+            c = int(cnt[0])
+            assert int(r.count[i]) == c
+            assert (r.ids[i, :c] == ids[:c]).all()
+            assert (r.dist[i, :c].view(np.uint32) == dist[:c].view(np.uint32)).all()
+    with pytest.raises(pg.ConfigError, match="k must be >= 1"):
+        pg.brute_force_search(v, q, 0)
