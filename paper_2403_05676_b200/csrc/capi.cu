@@ -2,12 +2,15 @@
 // index lifecycle (PRAGIX01 -> HBM layout), search orchestration on a CUDA
 // stream, shard planning/merge, and the GPU-fed performance model.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstring>
 #include <functional>
 #include <memory>
 #include <numeric>
+
+#include <map>
 
 #include "internal.h"
 
@@ -43,6 +46,37 @@ int require_device(int device) {
     }
     return PRAG_GPU_OK;
 }
+
+}  // namespace
+int sm_count(int device) {
+    static std::atomic<int> cache[64];
+    if (device < 0 || device >= 64) {
+        int n = 148;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
+        return n;
+    }
+    int n = cache[device].load(std::memory_order_relaxed);
+    if (n == 0) {
+        n = 148;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
+        cache[device].store(n, std::memory_order_relaxed);
+    }
+    return n;
+}
+
+cudaError_t ensure_smem(const void* kernel, size_t bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, size_t> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& have = done[{kernel, dev}];
+    if (have >= bytes && have) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+    if (e == cudaSuccess) have = bytes;
+    return e;
+}
+namespace {
 
 bool is_device_ptr(const void* p) {
     if (p == nullptr) return false;
@@ -340,8 +374,7 @@ int search_pass_skew(prag_gpu_index* ix, Workspace* w, const float* dq, uint32_t
                      uint64_t* o_ids, float* o_dist, uint32_t* o_count, uint64_t* o_scanned, cudaStream_t s,
                      prag_gpu_timings* tm) {
     const DeviceIndex& d = ix->dev;
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ix->device);
+    const int sms = sm_count(ix->device);
     const int grid = sms;  // persistent: one CTA per SM
     // item size from the worst-case tile count of this shape (host-side, so a
     // given (nq, nprobe) always plans the same way)
@@ -441,8 +474,7 @@ int search_pass(prag_gpu_index* ix, Workspace* w, const float* dq, uint32_t nq, 
     const uint64_t item_cap = uint64_t(nq) * (nprobe + (max_cand_q + C - 1) / C) + 1;
     const uint32_t pw_p = pow2_at_least(nprobe);
     const uint32_t pw_f = pow2_at_least(std::max<uint64_t>(1, std::min<uint64_t>(k, max_cand_q)));
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ix->device);
+    const int sms = sm_count(ix->device);
     const int per_sm = blocks_per_sm_scan(ix);
     const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>(item_cap, uint64_t(sms) * per_sm)));
     const size_t lut_bytes = size_t(d.nsq) * 1024 + ((d.d + 3) & ~3u) * 4;

@@ -658,7 +658,7 @@ int launch_coarse_tc(const DeviceIndex& ix, const float* queries, uint32_t nq, f
     const size_t kA = 2 * kTcRows * kTcKBlock * 4, kBp = size_t(n_tile) * kTcKBlock * 4;
     const size_t smem = kTcSliceBlocks * kA + kTcSliceBlocks * 2 * kBp +
                         size_t(n_tile) * kTcSliceBlocks * kTcKBlock * 4 + 2 * 8 + 16;
-    PG_CUDA(cudaFuncSetAttribute(coarse_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    PG_CUDA(ensure_smem(reinterpret_cast<const void*>(coarse_tc_kernel), int(smem)));
     dim3 grid(ix.nlist / kTcRows, (nq + n_tile - 1) / n_tile, tc_slices(ix.d));
     cudaError_t e = launch_pdl(coarse_tc_kernel, grid, dim3(128), smem, s, ix.cent_tc, queries, nq, ix.nlist, ix.d,
                                n_tile, partial);
@@ -675,7 +675,7 @@ int launch_select_window(const DeviceIndex& ix, float* partial, const float* que
     const size_t smem = tc_window_smem(ix.d);
 #define PG_WIN(V)                                                                                              \
     do {                                                                                                       \
-        PG_CUDA(cudaFuncSetAttribute(select_window_kernel<V>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+        PG_CUDA(ensure_smem(reinterpret_cast<const void*>(select_window_kernel<V>), \
                                      int(smem)));                                                              \
         PG_CUDA(launch_pdl(select_window_kernel<V>, dim3(nq), dim3(kWinThreads), smem, s, partial,           \
                            tc_slices(ix.d), ix.cent_norm, tc_bound_c(ix.d), ix.centroids, queries, nq, ix.nlist, \

@@ -41,6 +41,10 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
 // ---------------------------------------------------------------- errors
 void set_error(const std::string& msg);
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device)
+// and size: a hot-path launch does not pay the driver call every time.
+cudaError_t ensure_smem(const void* kernel, size_t bytes);
+
 struct Status {
     int code = PRAG_GPU_OK;
     static Status ok() { return {}; }

@@ -778,8 +778,7 @@ int launch_select_pool(const uint32_t* pool_key, const uint64_t* pool_id, const 
                        const uint32_t* q_item_off, const uint32_t* gthr, uint32_t nq, uint32_t k, uint64_t* out_ids,
                        float* out_dist, uint32_t* out_count, uint32_t* gkey, uint64_t* gtie, uint32_t pw,
                        cudaStream_t s) {
-    PG_CUDA(cudaFuncSetAttribute(select_pool_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(sizeof(PoolShared))));
+    PG_CUDA(ensure_smem(reinterpret_cast<const void*>(select_pool_kernel), int(sizeof(PoolShared))));
     cudaError_t e = launch_pdl(select_pool_kernel, dim3(nq), dim3(kSelThreads), sizeof(PoolShared), s, pool_key,
                                pool_id, scanned, q_item_off, gthr, k, out_ids, out_dist, out_count, gkey, gtie, pw);
     if (e == cudaSuccess) e = cudaGetLastError();
@@ -806,7 +805,7 @@ int launch_coarse(const DeviceIndex& ix, const float* queries, uint32_t nq, floa
         dim3 grid((ix.nlist + 127) / 128, (nq + 1) / 2);
         const size_t smem = size_t(2) * ix.d * sizeof(float);
         if (smem > 48 * 1024)
-            PG_CUDA(cudaFuncSetAttribute(coarse_exact4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            PG_CUDA(ensure_smem(reinterpret_cast<const void*>(coarse_exact4_kernel), int(smem)));
         coarse_exact4_kernel<<<grid, 128, smem, s>>>(reinterpret_cast<const float4*>(ix.centroids4), queries, nq,
                                                      ix.nlist, ix.d, out);
         return check_launch("coarse4");
@@ -815,15 +814,14 @@ int launch_coarse(const DeviceIndex& ix, const float* queries, uint32_t nq, floa
     dim3 grid((ix.nlist + 127) / 128, (nq + QB - 1) / QB);
     size_t smem = size_t(QB) * ix.d * sizeof(float);
     if (smem > 48 * 1024)
-        PG_CUDA(cudaFuncSetAttribute(coarse_exact_kernel<QB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(smem)));
+        PG_CUDA(ensure_smem(reinterpret_cast<const void*>(coarse_exact_kernel<QB>), int(smem)));
     coarse_exact_kernel<QB><<<grid, 128, smem, s>>>(ix.centroidsT, queries, nq, ix.nlist, ix.d, out);
     return check_launch("coarse");
 }
 
 static int set_sel_smem(const void* fn) {
     static_assert(sizeof(SelShared) < 227 * 1024, "selection smem");
-    PG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(SelShared))));
+    PG_CUDA(ensure_smem(reinterpret_cast<const void*>(fn), int(sizeof(SelShared))));
     return PRAG_GPU_OK;
 }
 
@@ -847,13 +845,13 @@ int launch_scan(const DeviceIndex& ix, const SearchBuffers& b, cudaStream_t s, i
     const bool smem_lut = lut_bytes + res_bytes <= 200 * 1024;
     if (smem_lut) {
         const size_t smem = lut_bytes + res_bytes;
-        PG_CUDA(cudaFuncSetAttribute(scan_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        PG_CUDA(ensure_smem(reinterpret_cast<const void*>(scan_kernel<true>), int(smem)));
         scan_kernel<true><<<grid, 256, smem, s>>>(b.queries, ix.centroids, ix.codewordsT, ix.list_off, ix.list_len,
                                                   ix.codes, ix.d, ix.nsq, ix.sub_dim, b.items, b.num_items,
                                                   b.item_cursor, b.cand_dist, b.cand_entry, nullptr);
     } else {
         const size_t smem = res_bytes;
-        PG_CUDA(cudaFuncSetAttribute(scan_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        PG_CUDA(ensure_smem(reinterpret_cast<const void*>(scan_kernel<false>), int(smem)));
         scan_kernel<false><<<grid, 256, smem, s>>>(b.queries, ix.centroids, ix.codewordsT, ix.list_off,
                                                    ix.list_len, ix.codes, ix.d, ix.nsq, ix.sub_dim, b.items,
                                                    b.num_items, b.item_cursor, b.cand_dist, b.cand_entry, glut);
@@ -946,8 +944,7 @@ int launch_brute_force(const float* emb, uint64_t n, uint32_t d, const float* qu
     if (nq == 0) return PRAG_GPU_OK;
     brute_dist_kernel<<<dim3(uint32_t((n + 255) / 256), nq), 256, size_t(d) * 4, s>>>(emb, n, d, queries, dist);
     PG_TRY(check_launch("brute_dist"));
-    PG_CUDA(cudaFuncSetAttribute(brute_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(sizeof(SelShared))));
+    PG_CUDA(ensure_smem(reinterpret_cast<const void*>(brute_select_kernel), int(sizeof(SelShared))));
     brute_select_kernel<<<nq, kSelThreads, sizeof(SelShared), s>>>(dist, uint32_t(n), k, gkey, gtie, pw, out_dist,
                                                                    out_ids, out_count);
     return check_launch("brute_select");

@@ -1158,13 +1158,13 @@ int launch_scan_skew(const DeviceIndex& ix, const uint4* items, const uint32_t* 
                      uint32_t* pool_key, uint64_t* pool_id, int grid, cudaStream_t s) {
     if (ix.nsq == 32) {
         const size_t smem = skew_smem_bytes<32>();
-        PG_CUDA(cudaFuncSetAttribute(scan_skew_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        PG_CUDA(ensure_smem(reinterpret_cast<const void*>(scan_skew_kernel<32>), int(smem)));
         PG_CUDA(launch_pdl(scan_skew_kernel<32>, dim3(grid), dim3(SkewSmem<32>::threads), smem, s, items, num_items,
                            cursor, probe, ix.list_len, ix.skew_off, ix.skew_codes, ix.list_off, ix.ids, luts, nprobe, k,
                            gthr, pool_key, pool_id));
     } else {
         const size_t smem = skew_smem_bytes<64>();
-        PG_CUDA(cudaFuncSetAttribute(scan_skew_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        PG_CUDA(ensure_smem(reinterpret_cast<const void*>(scan_skew_kernel<64>), int(smem)));
         PG_CUDA(launch_pdl(scan_skew_kernel<64>, dim3(grid), dim3(SkewSmem<64>::threads), smem, s, items, num_items,
                            cursor, probe, ix.list_len, ix.skew_off, ix.skew_codes, ix.list_off, ix.ids, luts, nprobe, k,
                            gthr, pool_key, pool_id));
