@@ -974,13 +974,7 @@ int prag_gpu_index_set_embeddings(prag_gpu_index* ix, const float* emb, uint64_t
     if (n == 0) return PRAG_GPU_OK;
     // every resident chunk id must have a row (annindex.hpp:310 indexes by chunk id)
     uint64_t max_id = 0;
-    {
-        const size_t npad = ix->dev.npadded;
-        std::vector<uint64_t> h(npad);
-        PG_CUDA(cudaMemcpy(h.data(), ix->dev.ids, npad * 8, cudaMemcpyDeviceToHost));
-        for (uint64_t v : h)
-            if (v != ~0ull && v > max_id) max_id = v;
-    }
+    PG_TRY(max_chunk_id(ix->dev.ids, ix->dev.npadded, &max_id));
     if (ix->dev.ntotal && max_id >= n) {
         set_error("set_embeddings: chunk id " + std::to_string(max_id) + " has no embedding row (n = " +
                   std::to_string(n) + ")");

@@ -193,6 +193,7 @@ int launch_rerank(const DeviceIndex& ix, const SearchBuffers& b, const float* em
                   cudaStream_t s);
 // brute_force_search (annindex.hpp:244-257) for nq device queries over n device rows;
 // dist is [nq][n] scratch, gkey/gtie [nq][pw] with pw = pow2 >= k
+int max_chunk_id(const uint64_t* ids, uint64_t n, uint64_t* out);
 int launch_brute_force(const float* emb, uint64_t n, uint32_t d, const float* queries, uint32_t nq, uint32_t k,
                        float* dist, uint32_t* gkey, uint64_t* gtie, uint32_t pw, uint64_t* out_ids, float* out_dist,
                        uint32_t* out_count, cudaStream_t s);

@@ -938,6 +938,30 @@ __global__ void __launch_bounds__(kSelThreads) brute_select_kernel(const float* 
 }
 }  // namespace
 
+namespace {
+__global__ void max_id_kernel(const uint64_t* __restrict__ ids, uint64_t n, unsigned long long* out) {
+    unsigned long long m = 0;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+        if (ids[i] != ~0ull && ids[i] > m) m = ids[i];
+    for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+}  // namespace
+
+// largest chunk id among the padded slots (padding slots hold ~0)
+int max_chunk_id(const uint64_t* ids, uint64_t n, uint64_t* out) {
+    unsigned long long* d = nullptr;
+    PG_CUDA(cudaMalloc(&d, 8));
+    cudaMemset(d, 0, 8);
+    if (n) max_id_kernel<<<592, 256>>>(ids, n, d);
+    unsigned long long h = 0;
+    const cudaError_t e = cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    PG_CUDA(e);
+    *out = h;
+    return PRAG_GPU_OK;
+}
+
 int launch_brute_force(const float* emb, uint64_t n, uint32_t d, const float* queries, uint32_t nq, uint32_t k,
                        float* dist, uint32_t* gkey, uint64_t* gtie, uint32_t pw, uint64_t* out_ids, float* out_dist,
                        uint32_t* out_count, cudaStream_t s) {
