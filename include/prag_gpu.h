@@ -10,6 +10,13 @@
  * reference's C++ shapes (SearchResult, Retriever) and INTEGRATION.md shows
  * the binding a maintainer adds.
  *
+ * Around the search path, also bit-exact with the reference:
+ * exact rerank (prag_gpu_search_rerank), brute force (prag_gpu_brute_force),
+ * the index build (prag_gpu_train_index = prag::train_index), query
+ * embedding (prag_gpu_embed = ChunkEmbedder::embed), the perf-model
+ * calibration, and the synthetic decode step of the PipeRAG loop. The
+ * PRAGRPC1 service lives in include/prag_gpu_service.hpp (C++ over this ABI).
+ *
  * Conventions
  *  - Every function returns int status: 0 OK, 1 CONFIG (reference ConfigError),
  *    2 FORMAT (reference FormatError), 3 CUDA, 4 NCCL, 5 OOM, 6 NO_DEVICE.
