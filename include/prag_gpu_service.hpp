@@ -141,34 +141,11 @@ public:
 
     ~GpuRetrievalService() { stop(); }
 
+    // Listens on address:port (0 = ephemeral); returns the bound port.
     std::uint16_t start(const std::string& address = "127.0.0.1", std::uint16_t port = 0) {
-        listen_fd_ = ::socket(AF_INET, SOCK_STREAM, 0);
-        if (listen_fd_ < 0) throw ConfigError("service: socket() failed");
-        int one = 1;
-        ::setsockopt(listen_fd_, SOL_SOCKET, SO_REUSEADDR, &one, sizeof(one));
-        sockaddr_in addr{};
-        addr.sin_family = AF_INET;
-        addr.sin_port = htons(port);
-        if (::inet_pton(AF_INET, address.c_str(), &addr.sin_addr) != 1)
-            throw ConfigError("service: invalid bind address " + address);
-        if (::bind(listen_fd_, reinterpret_cast<sockaddr*>(&addr), sizeof(addr)) != 0)
-            throw ConfigError("service: bind failed on " + address + ":" + std::to_string(port));
-        if (::listen(listen_fd_, 64) != 0) throw ConfigError("service: listen failed");
-        socklen_t len = sizeof(addr);
-        ::getsockname(listen_fd_, reinterpret_cast<sockaddr*>(&addr), &len);
-        port_ = ntohs(addr.sin_port);
+        listen_fd_ = open_listener(address, port, &port_);
         running_ = true;
-        acceptor_ = std::thread([this] {
-            while (running_) {
-                const int fd = ::accept(listen_fd_, nullptr, nullptr);
-                if (fd < 0) break;
-                int nd = 1;
-                ::setsockopt(fd, IPPROTO_TCP, TCP_NODELAY, &nd, sizeof(nd));
-                std::lock_guard<std::mutex> lk(conn_mu_);
-                conns_.insert(fd);
-                workers_.emplace_back([this, fd] { serve(fd); });
-            }
-        });
+        acceptor_ = std::thread([this] { accept_connections(); });
         return port_;
     }
 
@@ -191,52 +168,109 @@ public:
     }
 
 private:
-    // One connection: frames in, frames out (service.hpp:307-350 semantics).
-    void serve(int fd) {
-        using ::prag::detail::read_exact;
-        using ::prag::detail::send_frame;
-        for (bool open = true; open;) {
-            char magic[8];
-            if (read_exact(fd, magic, 8) != 0) break;
-            if (std::memcmp(magic, ::prag::kWireMagic, 8) != 0) {
-                // same protocol name, other version: framing is lost for good
-                const bool skew = std::memcmp(magic, ::prag::kWireMagic, 7) == 0;
-                send_frame(fd, ::prag::kMsgError,
-                           ::prag::encode_error({skew ? ::prag::kErrBadVersion : ::prag::kErrBadMagic,
-                                                 skew ? "unsupported protocol version" : "bad frame magic"}));
-                if (skew) break;
-                continue;
-            }
-            std::uint32_t n = 0;
-            if (read_exact(fd, &n, 4) != 0) break;
-            if (n < 1 || n > ::prag::kMaxFrameLen) {
-                send_frame(fd, ::prag::kMsgError, ::prag::encode_error({::prag::kErrBadPayload, "bad frame length"}));
-                break;
-            }
-            std::vector<std::uint8_t> body(n);
-            if (read_exact(fd, body.data(), n) != 0) break;
-            if (body[0] != ::prag::kMsgRequest) {
-                send_frame(fd, ::prag::kMsgError,
-                           ::prag::encode_error({::prag::kErrBadType, "unexpected message type"}));
-                continue;
-            }
-            try {
-                const auto req = ::prag::decode_request(std::vector<std::uint8_t>(body.begin() + 1, body.end()));
-                ::prag::Stopwatch clock;
-                auto outcome = batcher_.retrieve(req.query_tokens, req.k, req.directive);
-                ::prag::RetrievalResponse resp;
-                resp.request_id = req.request_id;
-                resp.nprobe_used = outcome.nprobe_used;
-                resp.server_latency_s = clock.elapsed_s();
-                resp.neighbors = std::move(outcome.neighbors);
-                open = send_frame(fd, ::prag::kMsgResponse, ::prag::encode_response(resp));
-            } catch (const std::exception& e) {
-                send_frame(fd, ::prag::kMsgError, ::prag::encode_error({::prag::kErrBadPayload, e.what()}));
-            }
+    static int open_listener(const std::string& address, std::uint16_t port, std::uint16_t* bound) {
+        sockaddr_in sa{};
+        sa.sin_family = AF_INET;
+        sa.sin_port = htons(port);
+        if (::inet_pton(AF_INET, address.c_str(), &sa.sin_addr) != 1)
+            throw ConfigError("service: invalid bind address " + address);
+        const int fd = ::socket(AF_INET, SOCK_STREAM, 0);
+        if (fd < 0) throw ConfigError("service: socket() failed");
+        const int reuse = 1;
+        ::setsockopt(fd, SOL_SOCKET, SO_REUSEADDR, &reuse, sizeof reuse);
+        if (::bind(fd, reinterpret_cast<const sockaddr*>(&sa), sizeof sa) != 0) {
+            ::close(fd);
+            throw ConfigError("service: bind failed on " + address + ":" + std::to_string(port));
         }
-        ::close(fd);
-        std::lock_guard<std::mutex> lk(conn_mu_);
-        conns_.erase(fd);
+        if (::listen(fd, 64) != 0) {
+            ::close(fd);
+            throw ConfigError("service: listen failed");
+        }
+        socklen_t sl = sizeof sa;
+        ::getsockname(fd, reinterpret_cast<sockaddr*>(&sa), &sl);
+        *bound = ntohs(sa.sin_port);
+        return fd;
+    }
+
+    void accept_connections() {
+        for (;;) {
+            const int fd = running_ ? ::accept(listen_fd_, nullptr, nullptr) : -1;
+            if (fd < 0) return;
+            const int nodelay = 1;
+            ::setsockopt(fd, IPPROTO_TCP, TCP_NODELAY, &nodelay, sizeof nodelay);
+            std::lock_guard<std::mutex> lk(conn_mu_);
+            conns_.insert(fd);
+            workers_.emplace_back([this, fd] {
+                serve(fd);
+                ::close(fd);
+                std::lock_guard<std::mutex> g(conn_mu_);
+                conns_.erase(fd);
+            });
+        }
+    }
+
+    static bool send_error(int fd, std::uint32_t code, const std::string& what) {
+        return ::prag::detail::send_frame(fd, ::prag::kMsgError, ::prag::encode_error({code, what}));
+    }
+
+    // What one read of the connection produced (service.hpp:307-350 semantics).
+    enum class Got { Closed, Skip, Drop, Request };
+
+    static Got next_request(int fd, ::prag::RetrievalRequest* req) {
+        using ::prag::detail::read_exact;
+        char head[8];
+        if (read_exact(fd, head, sizeof head) != 0) return Got::Closed;
+        if (std::memcmp(head, ::prag::kWireMagic, sizeof head) != 0) {
+            // a different version of the same protocol: framing is lost
+            const bool version_skew = std::memcmp(head, ::prag::kWireMagic, 7) == 0;
+            if (version_skew) {
+                send_error(fd, ::prag::kErrBadVersion, "unsupported protocol version");
+                return Got::Drop;
+            }
+            send_error(fd, ::prag::kErrBadMagic, "bad frame magic");
+            return Got::Skip;
+        }
+        std::uint32_t len = 0;
+        if (read_exact(fd, &len, sizeof len) != 0) return Got::Closed;
+        if (len == 0 || len > ::prag::kMaxFrameLen) {
+            send_error(fd, ::prag::kErrBadPayload, "bad frame length");
+            return Got::Drop;
+        }
+        std::vector<std::uint8_t> frame(len);
+        if (read_exact(fd, frame.data(), len) != 0) return Got::Closed;
+        if (frame.front() != ::prag::kMsgRequest) {
+            send_error(fd, ::prag::kErrBadType, "unexpected message type");
+            return Got::Skip;
+        }
+        try {
+            *req = ::prag::decode_request(std::vector<std::uint8_t>(frame.begin() + 1, frame.end()));
+        } catch (const std::exception& e) {
+            send_error(fd, ::prag::kErrBadPayload, e.what());
+            return Got::Skip;
+        }
+        return Got::Request;
+    }
+
+    void serve(int fd) {
+        for (;;) {
+            ::prag::RetrievalRequest req;
+            const Got got = next_request(fd, &req);
+            if (got == Got::Closed || got == Got::Drop) return;
+            if (got == Got::Skip) continue;
+            ::prag::RetrievalResponse resp;
+            resp.request_id = req.request_id;
+            try {
+                ::prag::Stopwatch timer;
+                auto out = batcher_.retrieve(req.query_tokens, req.k, req.directive);
+                resp.server_latency_s = timer.elapsed_s();
+                resp.nprobe_used = out.nprobe_used;
+                resp.neighbors = std::move(out.neighbors);
+            } catch (const std::exception& e) {
+                send_error(fd, ::prag::kErrBadPayload, e.what());
+                continue;
+            }
+            if (!::prag::detail::send_frame(fd, ::prag::kMsgResponse, ::prag::encode_response(resp))) return;
+        }
     }
 
     GpuRetriever gpu_;
