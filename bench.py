@@ -127,6 +127,15 @@ def reference_arm(args, path, queries, cfg):
                           str(args.steps), str(args.warmup), str(args.ref_seconds)], capture_output=True, text=True,
                          check=True)
     r = json.loads(out.stdout.strip().splitlines()[-1])
+    # the reference's own protocol is one thread running queries in sequence
+    # (perfmodel_main.cpp:57-63): one bounded batch on a single core beside it
+    one = subprocess.run([tool, "bench", path, qp, str(cfg["nq"]), str(cfg["nprobe"]), str(cfg["k"]), "1", "1", "0",
+                          "1"], capture_output=True, text=True)
+    if one.returncode == 0:
+        try:
+            r["single_thread_qps"] = json.loads(one.stdout.strip().splitlines()[-1])["qps"]
+        except Exception:
+            pass
     return r, threads
 
 
@@ -213,6 +222,7 @@ def main():
                 "higher_is_better": True, "scaling": "weak" if mode == "replicas" else "strong",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config,
                 "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": threads, "kind": "reference",
+                                 "single_thread_value": r.get("single_thread_qps"),
                                  "sample": f"{r['reps']} timed batches of {cfg['nq']} queries (p50), "
                                            f"prag::search on {threads} std::threads, index via load_index",
                                  "cpu": cpu_model()},
@@ -418,6 +428,7 @@ def main():
             if isinstance(res, tuple):
                 r, threads = res
                 cpu_baseline = {"value": r["qps"], "unit": "queries/s", "cores": threads, "kind": "reference",
+                                "single_thread_value": r.get("single_thread_qps"),
                                 "sample": f"{r['reps']} batches x {cfg['nq']} queries, nprobe={nprobe}, k={k} "
                                           f"(p50 {r['p50_s'] * 1e3:.1f} ms/batch), prag::search on {threads} "
                                           f"threads, same PRAGIX01 file", "cpu": cpu_model()}
