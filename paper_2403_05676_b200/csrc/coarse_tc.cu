@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(128, 1) coarse_tc_kernel(const float* __restri
 // ------------------------------------------------------------------ K1b
 constexpr uint32_t kWinThreads = 512;
 constexpr uint32_t kWinCap = 1024;   // window slots (ids + exact distances in SMEM)
-constexpr uint32_t kStageRows = 32;  // centroid rows staged per rescoring batch
+constexpr uint32_t kStageRowsMax = 64;  // centroid rows staged per rescoring batch (fewer for large d)
 
 __device__ __forceinline__ uint32_t fkey(float f) {
     const uint32_t u = __float_as_uint(f);
@@ -368,14 +368,14 @@ __global__ void __launch_bounds__(kWinThreads) select_window_kernel(
     float* __restrict__ partial, uint32_t nslices, const float* __restrict__ cent_norm, float bound_c,
     const float* __restrict__ centroids, const float* __restrict__ queries, uint32_t nq, uint32_t nlist, uint32_t d,
     uint32_t nprobe, uint32_t* __restrict__ probe, float* __restrict__ probe_dist,
-    unsigned long long* __restrict__ win_stat) {
+    unsigned long long* __restrict__ win_stat, uint32_t kStageRows) {
     extern __shared__ __align__(1024) unsigned char sm[];
     uint32_t* hist = reinterpret_cast<uint32_t*>(sm);          // [256]
     uint32_t* misc = hist + 256;                               // [8]: [1] rank, [2..3] selected key, [4] count, [5..7] two-level U
     uint32_t* win = misc + 8;                                  // [kWinCap] list ids
     float* wd = reinterpret_cast<float*>(win + kWinCap);       // [kWinCap] exact distances
     float* sq = wd + kWinCap;                                  // [d] the query
-    float* rows = sq + ((d + 3) & ~3u);                        // [2][kStageRows][d + 1]
+    float* rows = sq + ((d + 3) & ~3u);                        // [2][kStageRows][d + 1] (kStageRows: launch arg)
     float* red = rows + 2 * kStageRows * (d + 1);              // [kWinThreads / 32] reduction scratch
 
     const uint32_t q = blockIdx.x, tid = threadIdx.x;
@@ -607,8 +607,18 @@ __global__ void __launch_bounds__(kWinThreads) select_window_kernel(
 
 }  // namespace
 
+// rows per rescoring batch: up to kStageRowsMax while the double-buffered
+// staging fits the 227 KiB opt-in (more rows fold in parallel for large nprobe)
+static uint32_t window_stage_rows(uint32_t d) {
+    const size_t fixed = (256 + 8 + 2 * kWinCap) * 4 + ((d + 3) & ~3u) * 4 + (kWinThreads / 32) * 4;
+    const size_t per_row = 2 * size_t(d + 1) * 4;
+    const size_t fit = fixed < 227 * 1024 ? (227 * 1024 - fixed) / per_row : 0;
+    return uint32_t(std::min<size_t>(kStageRowsMax, fit));
+}
+
 size_t tc_window_smem(uint32_t d) {
-    return (256 + 8 + 2 * kWinCap) * 4 + ((d + 3) & ~3u) * 4 + 2 * size_t(kStageRows) * (d + 1) * 4 +
+    const uint32_t rows = std::max<uint32_t>(window_stage_rows(d), 8);
+    return (256 + 8 + 2 * kWinCap) * 4 + ((d + 3) & ~3u) * 4 + 2 * size_t(rows) * (d + 1) * 4 +
            (kWinThreads / 32) * 4;
 }
 
@@ -679,7 +689,8 @@ int launch_select_window(const DeviceIndex& ix, float* partial, const float* que
                                      int(smem)));                                                              \
         PG_CUDA(launch_pdl(select_window_kernel<V>, dim3(nq), dim3(kWinThreads), smem, s, partial,           \
                            tc_slices(ix.d), ix.cent_norm, tc_bound_c(ix.d), ix.centroids, queries, nq, ix.nlist, \
-                           ix.d, nprobe, probe, probe_dist, win_stat));                                         \
+                           ix.d, nprobe, probe, probe_dist, win_stat,                                           \
+                           std::max<uint32_t>(window_stage_rows(ix.d), 8)));                                    \
     } while (0)
     const uint32_t vpt = (ix.nlist + kWinThreads - 1) / kWinThreads;
     if (vpt <= 2)
