@@ -162,3 +162,27 @@ def test_no_fma_contraction_in_sass():
         if any(t.startswith("FFMA2") for t in toks):
             ffma2_funcs.add(func)
     assert ffma2_funcs and all("scan_skew_kernel" in f for f in ffma2_funcs), ffma2_funcs
+
+
+def test_headers_compile_standalone(tmp_path):
+    """The boundary headers stand alone: prag_gpu.h as C99 (any FFI's view),
+    prag_gpu.hpp as C++17 without the reference tree, and a program linking
+    libprag_gpu.so runs (no GPU needed for prag_gpu_device_count)."""
+    import shutil
+    import subprocess
+    inc = os.path.join(REPO, "include")
+    if not shutil.which("gcc") or not shutil.which("g++"):
+        pytest.skip("no host compiler")
+    c = tmp_path / "t.c"
+    c.write_text('#include "prag_gpu.h"\nint f(void) { prag_gpu_train_params p = {0}; (void)p;'
+                 ' return prag_gpu_version(); }\n')
+    subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-I" + inc, "-c", str(c), "-o", str(tmp_path / "t.o")],
+                   check=True)
+    cpp = tmp_path / "t.cpp"
+    cpp.write_text('#include "prag_gpu.hpp"\nint main() { prag::gpu::SearchParams p; p.nprobe = 4; (void)p;'
+                   ' return prag_gpu_device_count() >= 0 ? 0 : 1; }\n')
+    libdir = os.path.dirname(_lib.LIB_PATH)
+    exe = tmp_path / "t"
+    subprocess.run(["g++", "-std=c++17", "-Wall", "-Wextra", "-Werror", "-DPRAG_GPU_NO_REFERENCE", "-I" + inc,
+                    str(cpp), "-L" + libdir, "-lprag_gpu", "-Wl,-rpath," + libdir, "-o", str(exe)], check=True)
+    assert subprocess.run([str(exe)]).returncode == 0
