@@ -156,6 +156,12 @@ int prag_gpu_train_index(const float* vectors, uint64_t n, uint32_t d, const pra
                          int device, float* centroids, float* codewords, uint64_t* list_off, uint64_t* ids,
                          uint8_t* codes);
 
+/* Replaces prag::store_index (annindex.hpp:335-359): writes the resident
+ * index as PRAGIX01 (byte-identical to the file it was loaded from, or to
+ * store_index of the same IvfIndex/PqCodebook). Full (unsharded) indexes with
+ * the plain code layout only. */
+int prag_gpu_index_store(const prag_gpu_index* index, const char* pragix01_path);
+
 void prag_gpu_index_free(prag_gpu_index* index);
 int prag_gpu_index_describe(const prag_gpu_index* index, prag_gpu_index_desc* out);
 /* IvfIndex::nlist, as prag::Retriever::nlist() (pipeline.hpp:207). */

@@ -85,6 +85,7 @@ SYMBOLS = [
      [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64, C.c_double, P, P, C.c_int, C.POINTER(P)]),
     ("prag_gpu_train_index", C.c_int,
      [P, C.c_uint64, C.c_uint32, C.POINTER(TrainParamsC), C.c_int, P, P, P, P, P]),
+    ("prag_gpu_index_store", C.c_int, [P, C.c_char_p]),
     ("prag_gpu_index_free", None, [P]),
     ("prag_gpu_index_describe", C.c_int, [P, C.POINTER(IndexDesc)]),
     ("prag_gpu_index_nlist", C.c_uint32, [P]),

@@ -5,6 +5,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <functional>
 #include <memory>
@@ -948,6 +949,63 @@ int prag_gpu_search(prag_gpu_index* ix, const float* queries, uint32_t nq, uint3
     }
     return do_search(ix, queries, nq, nprobe, k, out_ids, out_dist, out_count, out_scanned,
                      static_cast<cudaStream_t>(stream));
+}
+
+int prag_gpu_index_store(const prag_gpu_index* ix, const char* path) {
+    if (!ix || !path) {
+        set_error("null argument");
+        return PRAG_GPU_CONFIG;
+    }
+    const DeviceIndex& d = ix->dev;
+    if (ix->shard_world > 1) {
+        set_error("store: a shard holds only part of the lists; store the full index");
+        return PRAG_GPU_CONFIG;
+    }
+    if (!d.plain_codes) {
+        set_error("store: this index has no plain code copy (device-built synthetic index)");
+        return PRAG_GPU_CONFIG;
+    }
+    DeviceGuard g(ix->device);
+    const uint32_t nl = d.nlist, sub = d.d / d.nsq;
+    std::vector<float> cent(size_t(nl) * d.d), words(size_t(d.nsq) * 256 * sub);
+    std::vector<uint64_t> off(size_t(nl) + 1), ids(d.npadded);
+    std::vector<uint32_t> len(nl);
+    std::vector<uint8_t> codes(d.npadded * d.nsq);
+    PG_CUDA(cudaMemcpy(cent.data(), d.centroids, cent.size() * 4, cudaMemcpyDeviceToHost));
+    PG_CUDA(cudaMemcpy(words.data(), d.codewords, words.size() * 4, cudaMemcpyDeviceToHost));
+    PG_CUDA(cudaMemcpy(off.data(), d.list_off, off.size() * 8, cudaMemcpyDeviceToHost));
+    PG_CUDA(cudaMemcpy(len.data(), d.list_len, len.size() * 4, cudaMemcpyDeviceToHost));
+    PG_CUDA(cudaMemcpy(ids.data(), d.ids, ids.size() * 8, cudaMemcpyDeviceToHost));
+    PG_CUDA(cudaMemcpy(codes.data(), d.codes, codes.size(), cudaMemcpyDeviceToHost));
+    // annindex.hpp:335-359 layout, written to a temporary then renamed
+    const std::string tmp = std::string(path) + ".tmp";
+    FILE* f = fopen(tmp.c_str(), "wb");
+    if (!f) {
+        set_error(std::string("cannot open for writing: ") + path);
+        return PRAG_GPU_FORMAT;
+    }
+    const uint32_t hdr[4] = {1u, nl, d.d, d.nsq};
+    bool ok = fwrite("PRAGIX01", 1, 8, f) == 8 && fwrite(hdr, 4, 4, f) == 4 &&
+              fwrite(cent.data(), 4, cent.size(), f) == cent.size() &&
+              fwrite(words.data(), 4, words.size(), f) == words.size();
+    std::vector<uint8_t> rec;
+    for (uint32_t l = 0; ok && l < nl; ++l) {
+        const uint64_t n = len[l];
+        ok = fwrite(&n, 8, 1, f) == 1;
+        rec.resize(size_t(n) * (8 + d.nsq));
+        for (uint64_t e = 0; e < n; ++e) {
+            std::memcpy(&rec[e * (8 + d.nsq)], &ids[off[l] + e], 8);
+            std::memcpy(&rec[e * (8 + d.nsq) + 8], &codes[(off[l] + e) * d.nsq], d.nsq);
+        }
+        ok = ok && (n == 0 || fwrite(rec.data(), 1, rec.size(), f) == rec.size());
+    }
+    ok = (fclose(f) == 0) && ok;
+    if (!ok || std::rename(tmp.c_str(), path) != 0) {
+        std::remove(tmp.c_str());
+        set_error(std::string("write failed: ") + path);
+        return PRAG_GPU_FORMAT;
+    }
+    return PRAG_GPU_OK;
 }
 
 int prag_gpu_search_rerank(prag_gpu_index* ix, const float* queries, uint32_t nq, uint32_t nprobe, uint32_t k,

@@ -146,6 +146,10 @@ class GpuIndex:
                                              device, C.byref(h)))
         return cls(h)
 
+    def store(self, path: str) -> None:
+        """prag::store_index (annindex.hpp:335-359) of the resident index."""
+        check(lib().prag_gpu_index_store(self._h, str(path).encode()))
+
     def close(self) -> None:
         if getattr(self, "_h", None):
             lib().prag_gpu_index_free(self._h)

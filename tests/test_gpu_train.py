@@ -117,3 +117,15 @@ def test_train_matches_oracle_larger():
     ref = O.train_index(v, 160, 16, 7, 6, 6000)
     for x, y in zip((t.centroids, t.codewords, t.list_off, t.ids, t.codes), ref):
         assert _same(x, y)
+
+
+@pytest.mark.parametrize("case", [c["name"] for c in CASES["cases"]][:6])
+def test_store_roundtrip_is_byte_identical(case, tmp_path):
+    """prag_gpu_index_store (annindex.hpp:335-359): load a reference-written
+    PRAGIX01 into HBM, store it back: the same bytes."""
+    import paper_2403_05676_b200 as pg
+    src = os.path.join(HERE, "golden", case + ".pragix")
+    ix = pg.GpuIndex.load(src)
+    out = tmp_path / "back.pragix"
+    ix.store(str(out))
+    assert out.read_bytes() == open(src, "rb").read()
