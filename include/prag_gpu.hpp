@@ -144,6 +144,8 @@ public:
     Index& operator=(Index&&) noexcept = default;
 
     prag_gpu_index* handle() const { return h_.get(); }
+    // prag::store_index (annindex.hpp:335-359) of the resident index.
+    void store(const std::string& pragix01_path) const { check(prag_gpu_index_store(h_.get(), pragix01_path.c_str())); }
     std::uint32_t nlist() const { return prag_gpu_index_nlist(h_.get()); }
     // Raw embeddings [n][d] by chunk id for exact rerank (annindex.hpp:307-312).
     void set_embeddings(const float* rows, std::uint64_t n) { check(prag_gpu_index_set_embeddings(h_.get(), rows, n)); }
