@@ -23,8 +23,9 @@ namespace pg {
 namespace {
 
 constexpr int kSelThreads = 1024;
-constexpr uint32_t kSortCap = 2048;
-constexpr uint32_t kRankDirect = 128;  // select_pool: this few survivors are ranked by counting   // elements sorted in SMEM; larger k sorts in global scratch
+constexpr uint32_t kSortCap = 2048;   // elements sorted in SMEM; larger k sorts in global scratch
+constexpr int kPoolThreads = 256;     // select_pool CTA
+constexpr uint32_t kPoolCap = 2048;   // select_pool: survivors kept in SMEM
 constexpr uint32_t kChunk = 4096;     // entries per scan work item
 
 // Monotone float -> uint32 map (total order == float order for non-NaN).
@@ -144,14 +145,6 @@ struct SelShared {
     uint64_t stie[kSortCap];
 };
 
-// select_pool's survivors of the threshold pass (kept apart from SelShared,
-// which the selection itself uses).
-struct PoolShared {
-    SelShared sel;
-    uint32_t nsurv;
-    uint32_t vkey[kSortCap];
-    uint64_t vid[kSortCap];
-};
 
 __device__ __forceinline__ void warp_hist_add(uint32_t* hist, uint32_t bucket, bool active) {
     // Warp-aggregated shared-memory histogram increment (distances share
@@ -583,193 +576,96 @@ __global__ void __launch_bounds__(kSelThreads) merge_kernel(
                out_ids + size_t(q) * k, out_count + q);
 }
 
-// k-th smallest (1-based rank) of the CTA's register-resident keys (VPT per
-// thread, slot i*blockDim + tid valid when < n); 8-bit radix passes over SMEM
-// histograms.
-template <int VPT>
-__device__ uint32_t block_kth_reg(const uint32_t (&key)[VPT], uint32_t n, uint32_t rank, SelShared& sm) {
-    const uint32_t tid = threadIdx.x, nth = blockDim.x;
-    __syncthreads();
-    if (tid == 0) {
-        sm.prefix = 0;
-        sm.rank = rank;
-    }
-    uint32_t mask = 0;
-    for (int shift = 24; shift >= 0; shift -= 8) {
-        for (uint32_t i = tid; i < 256; i += nth) sm.hist[i] = 0;
-        __syncthreads();
-        const uint32_t prefix = sm.prefix;
-#pragma unroll
-        for (int i = 0; i < VPT; ++i) {
-            const bool act = i * nth + tid < n && (key[i] & mask) == prefix;
-            warp_hist_add(sm.hist, (key[i] >> shift) & 255u, act);
-        }
-        __syncthreads();
-        hist_pick(sm, shift, false);
-        __syncthreads();
-        mask |= 0xffu << shift;
-    }
-    return sm.prefix;
-}
-
-// Pool selection from registers for pools of at most VPT * 1024 candidates
-// (VPT picked from the pool size, so small pools do not pay for 16 register
-// slots): radix select of the k-th key, then the <= kSortCap survivors ranked
-// by (distance, chunk_id). Returns false if more than kSortCap keys tie at
-// or below the k-th (the caller falls back to block_topk).
-template <int VPT, class Src>
-__device__ __noinline__ bool pool_fast(Src src, uint32_t n, uint32_t q, uint32_t k, uint32_t total,
-                                       uint64_t* __restrict__ out_ids, float* __restrict__ out_dist,
-                                       uint32_t* __restrict__ out_count, SelShared& sm) {
-    const uint32_t tid = threadIdx.x;
-    uint32_t key[VPT];
-#pragma unroll
-    for (int i = 0; i < VPT; ++i) {
-        const uint32_t idx = i * kSelThreads + tid;
-        key[i] = idx < n ? src.key(idx) : 0xffffffffu;
-    }
-    const uint32_t T = n > k ? block_kth_reg<VPT>(key, n, k, sm) : 0xffffffffu;
-    if (tid == 0) sm.nsel = 0;
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < VPT; ++i) {
-        const uint32_t idx = i * kSelThreads + tid;
-        const bool take = idx < n && key[i] <= T;
-        const unsigned bal = __ballot_sync(0xffffffffu, take);
-        uint32_t base = 0;
-        if ((tid & 31) == 0 && bal) base = atomicAdd(&sm.nsel, __popc(bal));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (take) {
-            const uint32_t pos = base + __popc(bal & ((1u << (tid & 31)) - 1));
-            if (pos < kSortCap) {
-                sm.skey[pos] = key[i];
-                sm.stie[pos] = src.tie(idx);
-            }
-        }
-    }
-    __syncthreads();
-    const uint32_t c = sm.nsel;
-    if (c > kSortCap) return false;
-    for (uint32_t i = tid; i < c; i += kSelThreads) {
-        const uint32_t ki = sm.skey[i];
-        const uint64_t ti = sm.stie[i];
-        uint32_t r = 0;
-        for (uint32_t j = 0; j < c; ++j) {
-            const uint32_t kj = sm.skey[j];
-            r += kj < ki || (kj == ki && sm.stie[j] < ti);
-        }
-        if (r < k) {
-            out_dist[size_t(q) * k + r] = key_float(ki);
-            out_ids[size_t(q) * k + r] = ti;
-        }
-    }
-    if (tid == 0) out_count[q] = total;
-    return true;
-}
-
-// K4 (fast path): exact top-k of a query's candidate pool: the fused scan
-// leaves, per work item, the CTA's exact top-k of that item (k slots,
-// +inf sentinels when the item had fewer entries), so a query's pool is
-// k x its item count, contiguous. One streaming pass keeps only the keys <=
-// the query's final shared threshold T0 (some item left k candidates <= T0,
-// so every top-k member is <= T0); few survivors are ranked by counting,
-// more go through the register radix select; the general paths remain for
-// anything else. count =
-// min(scanned_vectors, k) as in annindex.hpp:313.
-__global__ void __launch_bounds__(kSelThreads) select_pool_kernel(
+// K4 (fast path): exact top-k of a query's candidate pool. The fused scan
+// leaves, per work item, the CTA's exact top-k of that item (k slots, +inf
+// sentinels), so a query's pool is k x its item count, contiguous. The CTA
+// keeps the keys <= the query's final shared threshold T0 (some item left k
+// candidates <= T0, so every top-k member is <= T0) in SMEM, then one warp
+// runs an exact (distance, chunk_id) insertion top-k over them
+// (annindex.hpp:54-60); if more than kPoolCap keys survive, the warp streams
+// the whole pool instead. count = min(scanned_vectors, k) (annindex.hpp:313).
+__global__ void __launch_bounds__(kPoolThreads) select_pool_kernel(
     const uint32_t* __restrict__ pool_key, const uint64_t* __restrict__ pool_id,
     const uint64_t* __restrict__ scanned, const uint32_t* __restrict__ q_item_off, const uint32_t* __restrict__ gthr,
-    uint32_t k, uint64_t* __restrict__ out_ids, float* __restrict__ out_dist, uint32_t* __restrict__ out_count,
-    uint32_t* gkey, uint64_t* gtie, uint32_t pw) {
-    extern __shared__ __align__(16) unsigned char smraw[];
-    PoolShared& ps = *reinterpret_cast<PoolShared*>(smraw);
-    SelShared& sm = ps.sel;
-    const uint32_t q = blockIdx.x, tid = threadIdx.x;
+    uint32_t k, uint64_t* __restrict__ out_ids, float* __restrict__ out_dist, uint32_t* __restrict__ out_count) {
+    __shared__ uint32_t vkey[kPoolCap];
+    __shared__ uint64_t vid[kPoolCap];
+    __shared__ uint32_t nsurv;
+    const uint32_t q = blockIdx.x, tid = threadIdx.x, lane = tid & 31u;
     pdl_wait();  // the pool (and its offsets, from the planner) come from earlier kernels
     const size_t off = size_t(q_item_off[q]) * k;
     const uint32_t n = (q_item_off[q + 1] - q_item_off[q]) * k;
     const uint32_t total = uint32_t(min(scanned[q], uint64_t(k)));
-    const MergeSrc gsrc{pool_key + off, pool_id + off};
-    if (total == 0) {
-        if (tid == 0) out_count[q] = 0;
-        return;
-    }
     const uint32_t graw = gthr[q];  // raw distance bits (distances are >= 0); the pool holds ord_key()s
-    if (graw != 0xffffffffu) {
-        const uint32_t T0 = ord_key(__uint_as_float(graw));
-        if (tid == 0) ps.nsurv = 0;
-        __syncthreads();
-        for (uint32_t b0 = 0; b0 < n; b0 += 4 * kSelThreads) {
-            uint32_t key[4];
+    const uint32_t T0 = graw != 0xffffffffu ? ord_key(__uint_as_float(graw)) : 0xfffffffeu;
+    if (tid == 0) nsurv = 0;
+    __syncthreads();
+    for (uint32_t b0 = 0; b0 < n; b0 += 4 * kPoolThreads) {
+        uint32_t key[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const uint32_t idx = b0 + u * kSelThreads + tid;
-                key[u] = idx < n ? gsrc.key(idx) : 0xffffffffu;
-            }
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t i = b0 + u * kPoolThreads + tid;
+            key[u] = i < n ? pool_key[off + i] : 0xffffffffu;
+        }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const uint32_t idx = b0 + u * kSelThreads + tid;
-                const bool take = idx < n && key[u] <= T0;
-                const unsigned bal = __ballot_sync(0xffffffffu, take);
-                uint32_t base = 0;
-                if ((tid & 31) == 0 && bal) base = atomicAdd(&ps.nsurv, __popc(bal));
-                base = __shfl_sync(0xffffffffu, base, 0);
-                if (take) {
-                    const uint32_t pos = base + __popc(bal & ((1u << (tid & 31)) - 1));
-                    if (pos < kSortCap) {
-                        ps.vkey[pos] = key[u];
-                        ps.vid[pos] = gsrc.tie(idx);
-                    }
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t i = b0 + u * kPoolThreads + tid;
+            const bool take = key[u] <= T0;  // also drops the +inf sentinels and the tail
+            const unsigned bal = __ballot_sync(0xffffffffu, take);
+            uint32_t base = 0;
+            if (lane == 0 && bal) base = atomicAdd(&nsurv, __popc(bal));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (take) {
+                const uint32_t pos = base + __popc(bal & ((1u << lane) - 1));
+                if (pos < kPoolCap) {
+                    vkey[pos] = key[u];
+                    vid[pos] = pool_id[off + i];
                 }
             }
         }
-        __syncthreads();
-        const uint32_t c = ps.nsurv;
-        if (c >= total && c <= kRankDirect) {
-            // few survivors: rank each by counting
-            for (uint32_t i = tid; i < c; i += kSelThreads) {
-                const uint32_t ki = ps.vkey[i];
-                const uint64_t ti = ps.vid[i];
-                uint32_t r = 0;
-                for (uint32_t j = 0; j < c; ++j) {
-                    const uint32_t kj = ps.vkey[j];
-                    r += kj < ki || (kj == ki && ps.vid[j] < ti);
-                }
-                if (r < k) {
-                    out_dist[size_t(q) * k + r] = key_float(ki);
-                    out_ids[size_t(q) * k + r] = ti;
-                }
-            }
-            if (tid == 0) out_count[q] = total;
-            return;
-        }
-        const MergeSrc vsrc{ps.vkey, ps.vid};
-        bool ok = false;
-        if (c < total) {
-            // not expected (the item that set T0 left k entries <= T0): use the full pool
-        } else if (c <= kSelThreads) {
-            ok = pool_fast<1>(vsrc, c, q, k, total, out_ids, out_dist, out_count, sm);
-        } else if (c <= kSortCap) {
-            ok = pool_fast<2>(vsrc, c, q, k, total, out_ids, out_dist, out_count, sm);
-        }
-        if (ok) return;
-        __syncthreads();
     }
-    bool done = false;
-    if (n <= 1 * kSelThreads)
-        done = pool_fast<1>(gsrc, n, q, k, total, out_ids, out_dist, out_count, sm);
-    else if (n <= 2 * kSelThreads)
-        done = pool_fast<2>(gsrc, n, q, k, total, out_ids, out_dist, out_count, sm);
-    else if (n <= 4 * kSelThreads)
-        done = pool_fast<4>(gsrc, n, q, k, total, out_ids, out_dist, out_count, sm);
-    else if (n <= 16 * kSelThreads)
-        done = pool_fast<16>(gsrc, n, q, k, total, out_ids, out_dist, out_count, sm);
-    if (done) return;
     __syncthreads();
-    block_topk(gsrc, n, k, sm, gkey + size_t(q) * pw, gtie + size_t(q) * pw, out_dist + size_t(q) * k,
-               out_ids + size_t(q) * k, out_count + q);
-    __syncthreads();
-    if (tid == 0) out_count[q] = total;
+    if (tid >= 32) return;
+    const uint32_t c = nsurv;
+    const bool from_smem = c <= kPoolCap;
+    const uint32_t m = from_smem ? c : n;
+    // lane r holds the r-th best (key, id); (thk, thid) is the k-th
+    uint32_t lk = 0xffffffffu, thk = 0xffffffffu;
+    uint64_t lid = ~0ull, thid = ~0ull;
+    for (uint32_t i0 = 0; i0 < m; i0 += 32) {
+        const uint32_t i = i0 + lane;
+        uint32_t key = 0xffffffffu;
+        if (i < m) key = from_smem ? vkey[i] : pool_key[off + i];
+        const bool pre = key <= min(T0, thk);
+        unsigned bal = __ballot_sync(0xffffffffu, pre);
+        if (!bal) continue;
+        const uint64_t id = pre ? (from_smem ? vid[i] : pool_id[off + i]) : ~0ull;
+        while (bal) {
+            const int src = __ffs(bal) - 1;
+            bal &= bal - 1;
+            const uint32_t ck = __shfl_sync(0xffffffffu, key, src);
+            const uint64_t cid = __shfl_sync(0xffffffffu, id, src);
+            if (ck > thk || (ck == thk && cid >= thid)) continue;
+            const unsigned gm = __ballot_sync(0xffffffffu, lk > ck || (lk == ck && lid > cid));
+            const int pos = gm ? __ffs(gm) - 1 : 32;
+            const uint32_t uk = __shfl_up_sync(0xffffffffu, lk, 1);
+            const uint64_t ui = __shfl_up_sync(0xffffffffu, lid, 1);
+            if (int(lane) > pos) {
+                lk = uk;
+                lid = ui;
+            } else if (int(lane) == pos) {
+                lk = ck;
+                lid = cid;
+            }
+            thk = __shfl_sync(0xffffffffu, lk, k - 1);
+            thid = __shfl_sync(0xffffffffu, lid, k - 1);
+        }
+    }
+    if (lane < total) {
+        out_dist[size_t(q) * k + lane] = key_float(lk);
+        out_ids[size_t(q) * k + lane] = lid;
+    }
+    if (lane == 0) out_count[q] = total;
 }
 
 }  // namespace
@@ -778,9 +674,11 @@ int launch_select_pool(const uint32_t* pool_key, const uint64_t* pool_id, const 
                        const uint32_t* q_item_off, const uint32_t* gthr, uint32_t nq, uint32_t k, uint64_t* out_ids,
                        float* out_dist, uint32_t* out_count, uint32_t* gkey, uint64_t* gtie, uint32_t pw,
                        cudaStream_t s) {
-    PG_CUDA(ensure_smem(reinterpret_cast<const void*>(select_pool_kernel), int(sizeof(PoolShared))));
-    cudaError_t e = launch_pdl(select_pool_kernel, dim3(nq), dim3(kSelThreads), sizeof(PoolShared), s, pool_key,
-                               pool_id, scanned, q_item_off, gthr, k, out_ids, out_dist, out_count, gkey, gtie, pw);
+    (void)gkey;
+    (void)gtie;
+    (void)pw;
+    cudaError_t e = launch_pdl(select_pool_kernel, dim3(nq), dim3(kPoolThreads), 0, s, pool_key, pool_id, scanned,
+                               q_item_off, gthr, k, out_ids, out_dist, out_count);
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) {
         set_error(std::string("CUDA launch failed (select_pool): ") + cudaGetErrorString(e));
