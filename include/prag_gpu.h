@@ -181,6 +181,13 @@ int prag_gpu_search(prag_gpu_index* index, const float* queries, uint32_t nq, ui
                     uint32_t k, uint64_t* out_ids, float* out_dist, uint32_t* out_count,
                     uint64_t* out_scanned_vectors, void* stream);
 
+/* prag_gpu_search for callers whose queries and outputs are all device
+ * memory (asynchronous on `stream`): the same work without the per-call
+ * pointer-kind queries. Passing host memory here is undefined. */
+int prag_gpu_search_device(prag_gpu_index* index, const float* queries, uint32_t nq, uint32_t nprobe, uint32_t k,
+                           uint64_t* out_ids, float* out_dist, uint32_t* out_count, uint64_t* out_scanned,
+                           void* stream);
+
 /* Exact rerank (SearchParams::exact_rerank, annindex.hpp:307-312): raw
  * embeddings [n][d] fp32 row-major indexed by chunk id (host or device
  * pointer; copied into HBM). Every resident chunk id must be < n. n = 0

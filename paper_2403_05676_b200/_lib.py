@@ -93,6 +93,7 @@ SYMBOLS = [
     ("prag_gpu_search", C.c_int, [P, P, C.c_uint32, C.c_uint32, C.c_uint32, P, P, P, P, P]),
     ("prag_gpu_probe", C.c_int, [P, P, C.c_uint32, C.c_uint32, P, P, P]),
     ("prag_gpu_index_set_embeddings", C.c_int, [P, P, C.c_uint64]),
+    ("prag_gpu_search_device", C.c_int, [P, P, C.c_uint32, C.c_uint32, C.c_uint32, P, P, P, P, P]),
     ("prag_gpu_search_rerank", C.c_int, [P, P, C.c_uint32, C.c_uint32, C.c_uint32, P, P, P, P, P]),
     ("prag_gpu_brute_force", C.c_int, [P, C.c_uint64, C.c_uint32, P, C.c_uint32, C.c_uint32, C.c_int, P, P, P]),
     ("prag_gpu_plan_shards", C.c_int, [P, C.c_uint32, C.c_uint32, P]),

@@ -582,7 +582,7 @@ int validate(const prag_gpu_index* ix, uint32_t nprobe, uint32_t k) {
 
 int do_search(prag_gpu_index* ix, const float* queries, uint32_t nq, uint32_t nprobe, uint32_t k,
               uint64_t* out_ids, float* out_dist, uint32_t* out_count, uint64_t* out_scanned, cudaStream_t s,
-              bool rerank = false) {
+              bool rerank = false, bool all_device = false) {
     PG_TRY(validate(ix, nprobe, k));
     if (rerank && !ix->emb) {  // annindex.hpp:269-271
         set_error("search: exact_rerank requires raw embeddings");
@@ -599,9 +599,11 @@ int do_search(prag_gpu_index* ix, const float* queries, uint32_t nq, uint32_t np
     }
     DeviceGuard g(ix->device);
     const DeviceIndex& d = ix->dev;
-    const bool q_dev = is_device_ptr(queries);
-    const bool o_dev = is_device_ptr(out_ids) && is_device_ptr(out_dist) && is_device_ptr(out_count) &&
-                       (out_scanned == nullptr || is_device_ptr(out_scanned));
+    // (all_device: the caller vouches that every pointer is device memory,
+    // which skips five pointer-attribute queries on the launch path)
+    const bool q_dev = all_device || is_device_ptr(queries);
+    const bool o_dev = all_device || (is_device_ptr(out_ids) && is_device_ptr(out_dist) && is_device_ptr(out_count) &&
+                                      (out_scanned == nullptr || is_device_ptr(out_scanned)));
     // Bound candidate memory: chunk the batch so a pass holds <= 192M slots.
     const uint64_t max_cand_q = std::max<uint64_t>(1, ix->top_prefix[nprobe]);
     const uint64_t kSlots = 192ull << 20;
@@ -1006,6 +1008,17 @@ int prag_gpu_index_store(const prag_gpu_index* ix, const char* path) {
         return PRAG_GPU_FORMAT;
     }
     return PRAG_GPU_OK;
+}
+
+int prag_gpu_search_device(prag_gpu_index* ix, const float* queries, uint32_t nq, uint32_t nprobe, uint32_t k,
+                           uint64_t* out_ids, float* out_dist, uint32_t* out_count, uint64_t* out_scanned,
+                           void* stream) {
+    if (!ix) {
+        set_error("null index");
+        return PRAG_GPU_CONFIG;
+    }
+    return do_search(ix, queries, nq, nprobe, k, out_ids, out_dist, out_count, out_scanned,
+                     static_cast<cudaStream_t>(stream), false, true);
 }
 
 int prag_gpu_search_rerank(prag_gpu_index* ix, const float* queries, uint32_t nq, uint32_t nprobe, uint32_t k,

@@ -212,7 +212,12 @@ class GpuIndex:
                                   np.zeros(nq, dtype=np.uint32), np.zeros(nq, dtype=np.uint64))
         if (not on_dev) and q.shape[1] != self.d:
             raise ConfigError(f"query dimension {q.shape[1]} != index d {self.d}")
-        fn = lib().prag_gpu_search_rerank if exact_rerank else lib().prag_gpu_search
+        all_dev = on_dev and all(torch is not None and isinstance(x, torch.Tensor) and x.is_cuda
+                                 for x in (out.ids, out.dist, out.count, out.scanned))
+        if exact_rerank:
+            fn = lib().prag_gpu_search_rerank
+        else:
+            fn = lib().prag_gpu_search_device if all_dev else lib().prag_gpu_search
         check(fn(self._h, _ptr(q), nq, nprobe, k, _ptr(out.ids), _ptr(out.dist), _ptr(out.count),
                  _ptr(out.scanned), _stream_ptr(stream)))
         return out
