@@ -247,17 +247,22 @@ def main():
     qdev = torch.from_numpy(queries[:nq]).to(dev)
     from paper_2403_05676_b200 import distributed as PD
 
-    out_bufs = {}  # device result buffers per (nq, k), reused across steps as a serving loop would
+    # a serving loop reuses its device buffers: each (query buffer, nprobe, k)
+    # gets result buffers and a captured search (prag_gpu_plan: one CUDA-graph
+    # launch for the five kernels) on first use
+    plans = {}
 
     def step_dev(qd, nprobe_, k_):
-        key = (qd.shape[0], k_)
-        if key not in out_bufs:
-            out_bufs[key] = pg.BatchResult(torch.empty(key, dtype=torch.int64, device=dev),
-                                           torch.empty(key, dtype=torch.float32, device=dev),
-                                           torch.empty((key[0],), dtype=torch.int32, device=dev),
-                                           torch.empty((key[0],), dtype=torch.int64, device=dev))
+        key = (qd.data_ptr(), qd.shape[0], nprobe_, k_)
+        if key not in plans:
+            nq_ = qd.shape[0]
+            out = pg.BatchResult(torch.empty((nq_, k_), dtype=torch.int64, device=dev),
+                                 torch.empty((nq_, k_), dtype=torch.float32, device=dev),
+                                 torch.empty((nq_,), dtype=torch.int32, device=dev),
+                                 torch.empty((nq_,), dtype=torch.int64, device=dev))
+            plans[key] = ix.plan(qd, k_, nprobe_, out, stream=stream)
         with torch.cuda.stream(stream):
-            r = ix.search_batch(qd, k_, nprobe_, stream=stream, out=out_bufs[key])
+            r = plans[key].launch(stream=stream)
             if mode == "shard-lists":  # one packed NCCL all-gather of the per-shard top-k, exact merge on rank 0
                 r = PD.gather_merge(r, k_)
         return r
@@ -302,16 +307,37 @@ def main():
             if stop:
                 break
         t_dev = timed(lambda: step_dev(qdev, nprobe, k), args.steps, args.warmup)
-        # e2e: pinned host queries -> host results through the C ABI
+        # e2e: pinned host queries -> host results through the public API: the
+        # query batch is copied into a captured plan's device buffer, the plan
+        # runs, and the four result arrays (one contiguous device block) come
+        # back in one copy
         qhost = torch.from_numpy(queries[:nq].copy()).pin_memory()
         h_out = pg.BatchResult(torch.empty((nq, k), dtype=torch.int64).pin_memory(),
                                torch.empty((nq, k), dtype=torch.float32).pin_memory(),
                                torch.empty((nq,), dtype=torch.int32).pin_memory(),
                                torch.empty((nq,), dtype=torch.int64).pin_memory())
+        o_dist = nq * k * 8
+        o_cnt = o_dist + ((nq * k * 4 + 7) & ~7)
+        o_sc = o_cnt + ((nq * 4 + 7) & ~7)
+        blk_bytes = o_sc + nq * 8
+
+        def views(blk):
+            return pg.BatchResult(blk[:o_dist].view(torch.int64).view(nq, k),
+                                  blk[o_dist:o_dist + nq * k * 4].view(torch.float32).view(nq, k),
+                                  blk[o_cnt:o_cnt + nq * 4].view(torch.int32), blk[o_sc:].view(torch.int64))
+        d_blk = torch.empty(blk_bytes, dtype=torch.uint8, device=dev)
+        h_blk = torch.empty(blk_bytes, dtype=torch.uint8).pin_memory()
+        h_out = views(h_blk)
+        q_buf = torch.empty((nq, cfg["d"]), dtype=torch.float32, device=dev)
+        e2e_plan = ix.plan(q_buf, k, nprobe, views(d_blk), stream=stream) if mode != "shard-lists" else None
 
         def step_e2e():
             if mode != "shard-lists":
-                ix.search_batch(qhost, k, nprobe, stream=stream, out=h_out)
+                with torch.cuda.stream(stream):
+                    q_buf.copy_(qhost, non_blocking=True)
+                    e2e_plan.launch(stream=stream)
+                    h_blk.copy_(d_blk, non_blocking=True)
+                stream.synchronize()
             else:
                 qd = qhost.to(dev, non_blocking=True)
                 r = step_dev(qd, nprobe, k)

@@ -188,6 +188,18 @@ int prag_gpu_search_device(prag_gpu_index* index, const float* queries, uint32_t
                            uint64_t* out_ids, float* out_dist, uint32_t* out_count, uint64_t* out_scanned,
                            void* stream);
 
+/* A captured search (CUDA graph) for a fixed batch shape and fixed device
+ * buffers: create once with the buffers a serving loop reuses, then
+ * prag_gpu_plan_launch per batch after writing the queries into them. One
+ * graph launch replaces the five kernel launches (host cost), results are
+ * identical to prag_gpu_search. The batch must fit one pass. */
+typedef struct prag_gpu_plan prag_gpu_plan;
+int prag_gpu_plan_create(prag_gpu_index* index, const float* queries, uint32_t nq, uint32_t nprobe, uint32_t k,
+                         uint64_t* out_ids, float* out_dist, uint32_t* out_count, uint64_t* out_scanned,
+                         void* stream, prag_gpu_plan** out);
+int prag_gpu_plan_launch(prag_gpu_plan* plan, void* stream);
+void prag_gpu_plan_free(prag_gpu_plan* plan);
+
 /* Exact rerank (SearchParams::exact_rerank, annindex.hpp:307-312): raw
  * embeddings [n][d] fp32 row-major indexed by chunk id (host or device
  * pointer; copied into HBM). Every resident chunk id must be < n. n = 0

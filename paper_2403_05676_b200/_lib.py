@@ -93,6 +93,9 @@ SYMBOLS = [
     ("prag_gpu_search", C.c_int, [P, P, C.c_uint32, C.c_uint32, C.c_uint32, P, P, P, P, P]),
     ("prag_gpu_probe", C.c_int, [P, P, C.c_uint32, C.c_uint32, P, P, P]),
     ("prag_gpu_index_set_embeddings", C.c_int, [P, P, C.c_uint64]),
+    ("prag_gpu_plan_create", C.c_int, [P, P, C.c_uint32, C.c_uint32, C.c_uint32, P, P, P, P, P, C.POINTER(P)]),
+    ("prag_gpu_plan_launch", C.c_int, [P, P]),
+    ("prag_gpu_plan_free", None, [P]),
     ("prag_gpu_search_device", C.c_int, [P, P, C.c_uint32, C.c_uint32, C.c_uint32, P, P, P, P, P]),
     ("prag_gpu_search_rerank", C.c_int, [P, P, C.c_uint32, C.c_uint32, C.c_uint32, P, P, P, P, P]),
     ("prag_gpu_brute_force", C.c_int, [P, C.c_uint64, C.c_uint32, P, C.c_uint32, C.c_uint32, C.c_int, P, P, P]),

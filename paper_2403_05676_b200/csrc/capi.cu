@@ -1021,6 +1021,105 @@ int prag_gpu_search_device(prag_gpu_index* ix, const float* queries, uint32_t nq
                      static_cast<cudaStream_t>(stream), false, true);
 }
 
+}  // extern "C"
+
+struct prag_gpu_plan {
+    prag_gpu_index* ix = nullptr;
+    pg::Workspace* w = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+};
+
+extern "C" {
+
+int prag_gpu_plan_create(prag_gpu_index* ix, const float* queries, uint32_t nq, uint32_t nprobe, uint32_t k,
+                         uint64_t* out_ids, float* out_dist, uint32_t* out_count, uint64_t* out_scanned,
+                         void* stream, prag_gpu_plan** out) {
+    if (!ix || !out || !queries || !out_ids || !out_dist || !out_count || !out_scanned || nq == 0) {
+        set_error("plan: null argument or empty batch");
+        return PRAG_GPU_CONFIG;
+    }
+    *out = nullptr;
+    PG_TRY(validate(ix, nprobe, k));
+    if (!(is_device_ptr(queries) && is_device_ptr(out_ids) && is_device_ptr(out_dist) && is_device_ptr(out_count) &&
+          is_device_ptr(out_scanned))) {
+        set_error("plan: queries and outputs must be device memory");
+        return PRAG_GPU_CONFIG;
+    }
+    const DeviceIndex& d = ix->dev;
+    if (d.code_layout == 1 && k <= 32 && ix->scan_path == 0) {
+        const uint64_t img_q = uint64_t(nprobe) * skew_lut_bytes(d.nsq);
+        if (uint64_t(nq) * img_q > (1ull << 30)) {
+            set_error("plan: batch too large for one pass (split it)");
+            return PRAG_GPU_CONFIG;
+        }
+    } else if (uint64_t(nq) * std::max<uint64_t>(1, ix->top_prefix[nprobe]) > (192ull << 20)) {
+        set_error("plan: batch too large for one pass (split it)");
+        return PRAG_GPU_CONFIG;
+    }
+    DeviceGuard g(ix->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    auto plan = std::make_unique<prag_gpu_plan>();
+    plan->ix = ix;
+    plan->w = new Workspace();
+    plan->w->device = ix->device;
+    PG_CUDA(cudaEventCreateWithFlags(&plan->w->done, cudaEventDisableTiming));
+    struct Cleanup {
+        prag_gpu_plan* p;
+        ~Cleanup() {
+            if (!p) return;
+            if (p->exec) cudaGraphExecDestroy(p->exec);
+            if (p->graph) cudaGraphDestroy(p->graph);
+            cudaFree(p->w->buf);
+            cudaFree(p->w->stage);
+            cudaEventDestroy(p->w->done);
+            delete p->w;
+        }
+    } cleanup{plan.get()};
+    // one ordinary pass sizes the plan's own workspace, then the same pass is
+    // captured (no allocation or host synchronisation inside it)
+    PG_TRY(search_pass(ix, plan->w, queries, nq, nprobe, k, out_ids, out_dist, out_count, out_scanned, s, nullptr,
+                       false));
+    PG_CUDA(cudaStreamSynchronize(s));
+    PG_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    const int rc = search_pass(ix, plan->w, queries, nq, nprobe, k, out_ids, out_dist, out_count, out_scanned, s,
+                               nullptr, false);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(s, &graph);
+    if (rc != PRAG_GPU_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return rc;
+    }
+    PG_CUDA(ce);
+    plan->graph = graph;
+    PG_CUDA(cudaGraphInstantiate(&plan->exec, graph, 0));
+    cleanup.p = nullptr;
+    *out = plan.release();
+    return PRAG_GPU_OK;
+}
+
+int prag_gpu_plan_launch(prag_gpu_plan* plan, void* stream) {
+    if (!plan || !plan->exec) {
+        set_error("plan: null plan");
+        return PRAG_GPU_CONFIG;
+    }
+    PG_CUDA(cudaGraphLaunch(plan->exec, static_cast<cudaStream_t>(stream)));
+    return PRAG_GPU_OK;
+}
+
+void prag_gpu_plan_free(prag_gpu_plan* plan) {
+    if (!plan) return;
+    DeviceGuard g(plan->ix->device);
+    cudaDeviceSynchronize();
+    if (plan->exec) cudaGraphExecDestroy(plan->exec);
+    if (plan->graph) cudaGraphDestroy(plan->graph);
+    cudaFree(plan->w->buf);
+    cudaFree(plan->w->stage);
+    cudaEventDestroy(plan->w->done);
+    delete plan->w;
+    delete plan;
+}
+
 int prag_gpu_search_rerank(prag_gpu_index* ix, const float* queries, uint32_t nq, uint32_t nprobe, uint32_t k,
                            uint64_t* out_ids, float* out_dist, uint32_t* out_count, uint64_t* out_scanned,
                            void* stream) {

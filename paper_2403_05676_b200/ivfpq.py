@@ -222,6 +222,17 @@ class GpuIndex:
                  _ptr(out.scanned), _stream_ptr(stream)))
         return out
 
+    def plan(self, queries, k: int, nprobe: int, out: BatchResult, stream=None) -> "SearchPlan":
+        """A captured search (prag_gpu_plan_create) over fixed CUDA buffers:
+        write new queries into `queries`, then SearchPlan.launch()."""
+        if not (torch is not None and isinstance(queries, torch.Tensor) and queries.is_cuda):
+            raise ConfigError("plan: queries must be a CUDA tensor")
+        h = C.c_void_p()
+        nq = queries.shape[0] if queries.dim() == 2 else 1
+        check(lib().prag_gpu_plan_create(self._h, _ptr(queries), nq, nprobe, k, _ptr(out.ids), _ptr(out.dist),
+                                         _ptr(out.count), _ptr(out.scanned), _stream_ptr(stream), C.byref(h)))
+        return SearchPlan(h, self, queries, out)
+
     def probe(self, queries, nprobe: int):
         """Coarse quantizer only (annindex.hpp:277-281)."""
         q = np.ascontiguousarray(queries, dtype=np.float32).reshape(-1, self.d)
@@ -246,6 +257,28 @@ class GpuIndex:
         t = Timings()
         check(lib().prag_gpu_last_timings(self._h, C.byref(t)))
         return {f: getattr(t, f) for f, _ in Timings._fields_}
+
+
+class SearchPlan:
+    """CUDA-graph replay of one search shape over fixed device buffers."""
+
+    def __init__(self, handle, index, queries, out):
+        self._h, self._index, self.queries, self.out = handle, index, queries, out
+
+    def launch(self, stream=None) -> BatchResult:
+        check(lib().prag_gpu_plan_launch(self._h, _stream_ptr(stream)))
+        return self.out
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib().prag_gpu_plan_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class GpuChunkEmbedder:
