@@ -111,16 +111,32 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
     for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
 
 // K1. Grid (nlist / 128, ceil(nq / N), ceil(d / 96)); 128 threads. A CTA
 // owns 128 centroids x N queries x one 96-wide K slice (3 blocks of 32), so
-// nlist = 4096, d = 384 runs 128 CTAs. Everything it needs is requested up
-// front with bulk copies on one mbarrier: the pre-split centroid blocks
-// (cent_tc, 32 KiB each) and the raw query rows of the slice; the queries
-// are then split hi/lo SMEM->SMEM into the core-matrix layout, 36 MMAs are
-// issued by one thread, and the partial dot products go out as
-// partial[slice][q][c] (summed, with the norms and the bound, by K1b).
+// nlist = 4096, d = 384 runs 128 CTAs. The pre-split centroid blocks
+// (cent_tc, 32 KiB each) are bulk-copied on one mbarrier before waiting on
+// the previous kernel; the query rows of the slice are read by all threads
+// (one float4 per lane, four rows in flight per warp) and split hi/lo straight
+// into the core-matrix layout; 36 MMAs are issued by one thread, and the
+// partial dot products go out as partial[slice][q][c] (summed, with the norms
+// and the bound, by K1b).
 __global__ void __launch_bounds__(128, 1) coarse_tc_kernel(const float* __restrict__ cent_tc,
                                                            const float* __restrict__ queries, uint32_t nq,
                                                            uint32_t nlist, uint32_t d, uint32_t n_tile,
@@ -132,11 +148,9 @@ __global__ void __launch_bounds__(128, 1) coarse_tc_kernel(const float* __restri
     const uint32_t nkb_all = d / kTcKBlock;
     const uint32_t kb0 = blockIdx.z * kTcSliceBlocks;
     const uint32_t nkb = min(kTcSliceBlocks, nkb_all - kb0);
-    const uint32_t row_bytes = nkb * kTcKBlock * 4;           // raw query bytes of the slice
     unsigned char* sA = sm;                                   // [nkb][hi | lo]
     unsigned char* sB = sA + kTcSliceBlocks * kA;             // [nkb][hi | lo][kBp]
-    float* raw = reinterpret_cast<float*>(sB + kTcSliceBlocks * 2 * kBp);  // [N][nkb * 32]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(raw + size_t(N) * kTcSliceBlocks * kTcKBlock);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kTcSliceBlocks * 2 * kBp);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
 
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -149,44 +163,58 @@ __global__ void __launch_bounds__(128, 1) coarse_tc_kernel(const float* __restri
         bar_init(bars, 1);
         bar_init(bars + 1, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        bar_expect_tx(bars, nkb * kA + nvalid * row_bytes);
-        // index data first: it does not depend on the previous kernel
+        bar_expect_tx(bars, nkb * kA);
+        // index data: it does not depend on the previous kernel
         for (uint32_t i = 0; i < nkb; ++i)
             bulk_load(sA + i * kA, cent_tc + (size_t(tile) * nkb_all + kb0 + i) * (2 * kTcRows * kTcKBlock), kA, bars);
-    }
-    pdl_wait();
-    if (tid == 0) {
-        for (uint32_t n = 0; n < nvalid; ++n)
-            bulk_load(raw + size_t(n) * nkb * kTcKBlock, queries + size_t(q0 + n) * d + kb0 * kTcKBlock, row_bytes,
-                      bars);
     }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(tmem_slot)),
                      "r"(ncols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    for (uint32_t i = nvalid * nkb * kTcKBlock + tid; i < N * nkb * kTcKBlock; i += 128) raw[i] = 0.0f;  // pad rows
+    pdl_wait();
+    // B: element (n, k) of a part at (k/4) * (N * 16) + (n/8) * 128 + (n%8) * 16 + (k%4) * 4,
+    // so the 4 consecutive k of one float4 are one 16-byte store. Lane = float4
+    // of the row (nkb * 8 <= 24 lanes busy), warp w takes rows w, w + 4, ...
+    const uint32_t k4n = nkb * (kTcKBlock / 4);
+    if (lane < k4n) {
+        const uint32_t k = lane * 4, blk = k / kTcKBlock, kk = k % kTcKBlock;
+        unsigned char* b = sB + blk * 2 * kBp + (kk >> 2) * (N * 16);
+        const float* qbase = queries + size_t(kb0) * kTcKBlock + k;
+        const bool vec = (reinterpret_cast<uintptr_t>(queries) & 15u) == 0;  // d % 32 == 0: rows stay aligned
+        // all of the warp's rows (N / 4 <= 16) in flight at once
+        constexpr uint32_t R = kTcMaxN / 4;
+        float4 x[R];
+#pragma unroll
+        for (uint32_t u = 0; u < R; ++u) {
+            const uint32_t n = warp + 4 * u;
+            x[u] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+            if (n < nvalid) {
+                const float* src = qbase + size_t(q0 + n) * d;
+                x[u] = vec ? *reinterpret_cast<const float4*>(src) : make_float4(src[0], src[1], src[2], src[3]);
+            }
+        }
+#pragma unroll
+        for (uint32_t u = 0; u < R; ++u) {
+            const uint32_t n = warp + 4 * u;
+            if (n < N) {
+                const float4 hi = make_float4(tf32_hi(x[u].x), tf32_hi(x[u].y), tf32_hi(x[u].z), tf32_hi(x[u].w));
+                const float4 lo = make_float4(__fsub_rn(x[u].x, hi.x), __fsub_rn(x[u].y, hi.y),
+                                              __fsub_rn(x[u].z, hi.z), __fsub_rn(x[u].w, hi.w));
+                const uint32_t off = (n >> 3) * 128 + (n & 7) * 16;
+                *reinterpret_cast<float4*>(b + off) = hi;
+                *reinterpret_cast<float4*>(b + kBp + off) = lo;
+            }
+        }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic STS -> tensor-core reads
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
-    bar_wait(bars, 0);
-    // B: element (n, k) of a part at (k/4) * (N * 16) + (n/8) * 128 + (n%8) * 16 + (k%4) * 4
-    const uint32_t kk_all = nkb * kTcKBlock;
-    for (uint32_t idx = tid; idx < N * kk_all; idx += 128) {
-        const uint32_t n = idx / kk_all, kg = idx - n * kk_all;
-        const uint32_t blk = kg / kTcKBlock, k = kg % kTcKBlock;
-        const float x = raw[idx];
-        const float hi = tf32_hi(x);
-        unsigned char* b = sB + blk * 2 * kBp;
-        const uint32_t off = (k >> 2) * (N * 16) + (n >> 3) * 128 + (n & 7) * 16 + (k & 3) * 4;
-        *reinterpret_cast<float*>(b + off) = hi;
-        *reinterpret_cast<float*>(b + kBp + off) = x - hi;
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic STS -> tensor-core reads
-    __syncthreads();
     if (tid == 0) {
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        bar_wait(bars, 0);
         const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((N >> 3) << 17) | ((kTcRows >> 4) << 24);
         for (uint32_t i = 0; i < nkb; ++i) {
             const uint32_t a0 = smem_addr(sA + i * kA), b0 = smem_addr(sB + i * 2 * kBp);
@@ -205,18 +233,29 @@ __global__ void __launch_bounds__(128, 1) coarse_tc_kernel(const float* __restri
         }
         mma_commit(bars + 1);
     }
+    __syncwarp();
     bar_wait(bars + 1, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     pdl_trigger();
-    // epilogue: TMEM lane = centroid row (warp w owns lanes 32w..32w+31)
+    // epilogue: TMEM lane = centroid row (warp w owns lanes 32w..32w+31);
+    // 32 columns per TMEM load
     const uint32_t c = tile * kTcRows + warp * 32 + lane;
-    float* out = partial + size_t(blockIdx.z) * nq * nlist;
-    for (uint32_t j0 = 0; j0 < N; j0 += 8) {
-        float v[8];
-        tmem_ld8(tmem + ((warp * 32) << 16) + j0, v);
+    float* out = partial + size_t(blockIdx.z) * nq * nlist + size_t(q0) * nlist + c;
+    const uint32_t trow = tmem + ((warp * 32) << 16);
+    uint32_t j0 = 0;
+    for (; j0 + 32 <= N; j0 += 32) {
+        float v[32];
+        tmem_ld32(trow + j0, v);
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-            if (j0 + j < nvalid) out[size_t(q0 + j0 + j) * nlist + c] = v[j];
+        for (uint32_t j = 0; j < 32; ++j)
+            if (j0 + j < nvalid) out[size_t(j0 + j) * nlist] = v[j];
+    }
+    for (; j0 < N; j0 += 8) {
+        float v[8];
+        tmem_ld8(trow + j0, v);
+#pragma unroll
+        for (uint32_t j = 0; j < 8; ++j)
+            if (j0 + j < nvalid) out[size_t(j0 + j) * nlist] = v[j];
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -666,8 +705,7 @@ uint32_t tc_slices(uint32_t d) { return (d / kTcKBlock + kTcSliceBlocks - 1) / k
 int launch_coarse_tc(const DeviceIndex& ix, const float* queries, uint32_t nq, float* partial, cudaStream_t s) {
     const uint32_t n_tile = std::min<uint32_t>(kTcMaxN, (nq + 7) / 8 * 8);
     const size_t kA = 2 * kTcRows * kTcKBlock * 4, kBp = size_t(n_tile) * kTcKBlock * 4;
-    const size_t smem = kTcSliceBlocks * kA + kTcSliceBlocks * 2 * kBp +
-                        size_t(n_tile) * kTcSliceBlocks * kTcKBlock * 4 + 2 * 8 + 16;
+    const size_t smem = kTcSliceBlocks * kA + kTcSliceBlocks * 2 * kBp + 2 * 8 + 16;
     PG_CUDA(ensure_smem(reinterpret_cast<const void*>(coarse_tc_kernel), int(smem)));
     dim3 grid(ix.nlist / kTcRows, (nq + n_tile - 1) / n_tile, tc_slices(ix.d));
     cudaError_t e = launch_pdl(coarse_tc_kernel, grid, dim3(128), smem, s, ix.cent_tc, queries, nq, ix.nlist, ix.d,

@@ -43,3 +43,26 @@ def test_plan_replay_equals_search(tmp_path):
                 assert (got_dist[i, :c].view(np.uint32) == ref.dist[i, :c].view(np.uint32)).all()
         plan.close()
     ix.set_scan_path(0)
+
+
+def test_unaligned_device_queries(tmp_path):
+    """Device query buffers need only 4-byte alignment (a row view of a
+    larger tensor at any float offset): same results as host queries."""
+    import torch
+    import paper_2403_05676_b200 as pg
+    from paper_2403_05676_b200 import fixtures as F
+    os.environ.setdefault("PRAG_FIXTURE_DIR", str(tmp_path))
+    p, q, _ = F.ensure_fixture(300_000, 384, 256, 32, seed=21, nq=64, log=lambda *a: None)
+    ix = pg.GpuIndex.load(p, 0)
+    nq, k, nprobe = 24, 10, 16
+    ref = ix.search_batch(q[:nq], k, nprobe)
+    for off in (1, 2, 3):
+        buf = torch.zeros(nq * q.shape[1] + off, dtype=torch.float32, device="cuda")
+        qd = buf[off:].view(nq, q.shape[1])
+        qd.copy_(torch.from_numpy(q[:nq].copy()))
+        assert qd.data_ptr() % 16 != 0
+        r = ix.search_batch(qd, k, nprobe)
+        torch.cuda.synchronize()
+        assert (r.count.cpu().numpy() == ref.count).all()
+        assert (r.ids.cpu().numpy().view(np.uint64) == ref.ids).all(), off
+        assert (r.dist.cpu().numpy().view(np.uint32) == ref.dist.view(np.uint32)).all(), off
