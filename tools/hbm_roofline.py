@@ -23,6 +23,7 @@ import torch  # noqa: E402
 
 import paper_2403_05676_b200 as pg  # noqa: E402
 from paper_2403_05676_b200 import fixtures as F  # noqa: E402
+from bench import ClockSampler  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=100_000_000)
@@ -51,13 +52,14 @@ for nq in (1, 8, 64):
             ix.search_batch(qd, 10, nprobe, stream=s)
         ix.set_profiling(True)
         ts = []
-        for _ in range(a.reps):
-            with torch.cuda.stream(s):
-                flush.zero_()
-            torch.cuda.synchronize()
-            ix.search_batch(qd, 10, nprobe, stream=s)
-            torch.cuda.synchronize()
-            ts.append(ix.last_timings())
+        with ClockSampler(0) as clk:  # long rows run near the power cap: record the clocks they saw
+            for _ in range(a.reps):
+                with torch.cuda.stream(s):
+                    flush.zero_()
+                torch.cuda.synchronize()
+                ix.search_batch(qd, 10, nprobe, stream=s)
+                torch.cuda.synchronize()
+                ts.append(ix.last_timings())
         ix.set_profiling(False)
         scan = statistics.median(t["scan_ms"] for t in ts)
         tot = statistics.median(t["total_ms"] for t in ts)
@@ -65,7 +67,7 @@ for nq in (1, 8, 64):
         r = {"nq": nq, "nprobe": nprobe, "scan_ms": round(scan, 4), "search_ms": round(tot, 4),
              "B_alg_MB": round(balg / 1e6, 2), "unique_MB": round(unique_bytes / 1e6, 2),
              "scan_GBps": round(balg / (scan / 1e3) / 1e9, 1),
-             "frac_of_hbm": round(balg / (scan / 1e3) / 1e9 / hbm, 3)}
+             "frac_of_hbm": round(balg / (scan / 1e3) / 1e9 / hbm, 3), "clocks": clk.summary()}
         rows.append(r)
         print(json.dumps(r), file=sys.stderr, flush=True)
 print(json.dumps({"workload": f"IVF-PQ {a.n // 1_000_000}M x 384, nlist={a.nlist}, m={a.m} (codes "
