@@ -241,6 +241,55 @@ int prag_gpu_merge_topk(const uint64_t* ids, const float* dist, const uint32_t* 
                         uint32_t k, uint64_t* out_ids, float* out_dist, uint32_t* out_count,
                         uint64_t* out_scanned, int device, void* stream);
 
+/* ----------------------------------------- list-sharded search (8e) */
+/* The reference's Retriever is called by C++ (pipeline.hpp:221-238, :496;
+ * service.hpp:338), so the multi-GPU path is behind this ABI too, in two
+ * forms (lists placed by LPT on bytes, centroids and codebook
+ * replicated, per-shard K1-K4, one exchange of the per-shard top-k, exact
+ * merge by (distance, chunk id) -- bit-identical to the unsharded search):
+ *
+ * (1) One process driving several GPUs: a GROUP handle. prag_gpu_search /
+ *     _device / _rerank / plan_* / calibrate on it run every shard on its
+ *     own device and stream, then ONE kernel on the root device (devices[0])
+ *     reads each shard's top-k over NVLink peer memory and merges them (the
+ *     gather fused into the merge; shards without peer access are copied to
+ *     the root first). A group is a prag_gpu_index everywhere in this ABI
+ *     (GpuRetriever, the service, the perf model take it unchanged). Devices
+ *     may repeat (several shards on one GPU). */
+int prag_gpu_index_load_sharded(const char* pragix01_path, const int* devices, int n_devices,
+                                prag_gpu_index** out);
+/* The same from host arrays in prag_gpu_index_from_host's layout. */
+int prag_gpu_index_from_host_sharded(uint32_t nlist, uint32_t d, uint32_t nsq, const float* centroids,
+                                     const float* codewords, const uint64_t* list_off, const uint64_t* ids,
+                                     const uint8_t* codes, const int* devices, int n_devices,
+                                     prag_gpu_index** out);
+/* Group of already-built shards (load_shard / synthetic_shard ranks 0..n-1
+ * of world n, any devices); takes ownership of the shard handles. */
+int prag_gpu_index_group(prag_gpu_index* const* shards, int n, prag_gpu_index** out);
+
+/* Rank `rank` of `world` of the synthetic index prag_gpu_index_synthetic
+ * builds from the same arguments (lists placed by prag_gpu_plan_shards on the
+ * synthetic list sizes; every entry keeps its global chunk id and code). */
+int prag_gpu_index_synthetic_shard(uint32_t nlist, uint32_t d, uint32_t nsq, uint64_t ntotal, uint64_t seed,
+                                   double sigma, const float* centroids, const float* codewords, int rank,
+                                   int world, int device, prag_gpu_index** out);
+
+/* (2) One process per GPU (torchrun / MPI ranks): an NCCL communicator
+ *     (NCCL is resolved at run time: libnccl.so.2, the copy the process
+ *     already has loaded if any). Attach it to the rank's shard; from then on
+ *     prag_gpu_search / plans on that shard are COLLECTIVE: every rank passes
+ *     the same queries, runs K1-K4 on its lists, the per-shard top-k blocks are
+ *     exchanged with one ncclAllGather on the search stream, and every rank
+ *     gets the merged global result. Graph-capturable (prag_gpu_plan_create,
+ *     called by all ranks). */
+typedef struct prag_gpu_comm prag_gpu_comm;
+int prag_gpu_comm_unique_id(uint8_t out_id[128]);   /* ncclGetUniqueId, on one rank */
+int prag_gpu_comm_init(const uint8_t id[128], int world, int rank, int device, prag_gpu_comm** out);
+void prag_gpu_comm_free(prag_gpu_comm* comm);
+/* shard: rank r of world w (load_shard / synthetic_shard) with comm rank r of
+ * w on the same device; comm NULL detaches. The comm must outlive its use. */
+int prag_gpu_index_attach_comm(prag_gpu_index* shard, prag_gpu_comm* comm);
+
 /* ------------------------------------------------- performance model */
 /* Replaces prag::calibrate_retrieval (perfmodel.hpp:92-117) fed with the GPU
  * latency curve: for each nprobe in grid (sorted, deduplicated; >= 2 values,
@@ -289,8 +338,10 @@ typedef struct prag_gpu_embedder prag_gpu_embedder;
 int prag_gpu_embedder_create(uint32_t d, uint64_t seed, uint32_t vocab, int device, prag_gpu_embedder** out);
 void prag_gpu_embedder_free(prag_gpu_embedder* embedder);
 /* tokens: nchunks x m token ids (PAD = 0 skipped), host or device; out:
- * nchunks x d floats, host or device. A token id >= vocab is CONFIG (checked
- * when any pointer is host memory). */
+ * nchunks x d floats, host or device. With host tokens any id is accepted:
+ * ids >= vocab get their vectors computed on the host for that call, as
+ * ChunkEmbedder::embed does for every id. Device tokens must be < vocab
+ * (CONFIG otherwise, reported when any pointer is host memory). */
 int prag_gpu_embed(prag_gpu_embedder* embedder, const uint32_t* tokens, uint32_t nchunks, uint32_t m, float* out,
                    void* stream);
 

@@ -106,6 +106,22 @@ public:
         check(prag_gpu_index_load_shard(pragix01_path.c_str(), device, rank, world, &h));
         return Index(h);
     }
+    // List-sharded over several GPUs of this process: LPT
+    // placement, per-shard K1-K4 on each device, merge on devices[0] reading
+    // the shards' top-k over NVLink. Usable wherever an Index is.
+    static Index load_sharded(const std::string& pragix01_path, const std::vector<int>& devices) {
+        prag_gpu_index* h = nullptr;
+        check(prag_gpu_index_load_sharded(pragix01_path.c_str(), devices.data(), int(devices.size()), &h));
+        return Index(h);
+    }
+    static Index from_host_sharded(std::uint32_t nlist, std::uint32_t d, std::uint32_t nsq, const float* centroids,
+                                   const float* codewords, const std::uint64_t* list_off, const std::uint64_t* ids,
+                                   const std::uint8_t* codes, const std::vector<int>& devices) {
+        prag_gpu_index* h = nullptr;
+        check(prag_gpu_index_from_host_sharded(nlist, d, nsq, centroids, codewords, list_off, ids, codes,
+                                               devices.data(), int(devices.size()), &h));
+        return Index(h);
+    }
     // Flat host arrays in the reference's logical layout (see prag_gpu.h).
     static Index from_host(std::uint32_t nlist, std::uint32_t d, std::uint32_t nsq, const float* centroids,
                            const float* codewords, const std::uint64_t* list_off, const std::uint64_t* ids,
@@ -118,6 +134,11 @@ public:
     // The reference's in-memory objects (e.g. straight from train_index):
     // AoS postings are de-interleaved into the SoA arrays the ABI takes.
     static Index from_reference(const ::prag::IvfIndex& index, const ::prag::PqCodebook& cb, int device = 0) {
+        return from_reference(index, cb, std::vector<int>{device});
+    }
+    // devices.size() > 1: list-sharded over those devices (see load_sharded)
+    static Index from_reference(const ::prag::IvfIndex& index, const ::prag::PqCodebook& cb,
+                                const std::vector<int>& devices) {
         const std::uint32_t nl = index.nlist, d = index.d, m = cb.n_subquantizers, sub = cb.sub_dim;
         std::vector<float> cent(std::size_t(nl) * d), words(std::size_t(m) * 256 * sub);
         for (std::uint32_t l = 0; l < nl; ++l)
@@ -136,7 +157,10 @@ public:
                 ids.push_back(e.chunk_id);
                 codes.insert(codes.end(), e.code.begin(), e.code.end());
             }
-        return from_host(nl, d, m, cent.data(), words.data(), off.data(), ids.data(), codes.data(), device);
+        if (devices.size() > 1)
+            return from_host_sharded(nl, d, m, cent.data(), words.data(), off.data(), ids.data(), codes.data(),
+                                     devices);
+        return from_host(nl, d, m, cent.data(), words.data(), off.data(), ids.data(), codes.data(), devices.at(0));
     }
 #endif
 
@@ -298,6 +322,13 @@ public:
                  int device = 0)
         : db_(&db), gpu_(Index::from_reference(index, codebook, device)), nlist_(index.nlist),
           embedder_(make_embedder(db, embed_seed, device)), perf_(perf), safety_margin_(safety_margin) {}
+
+    // The index list-sharded over several GPUs (devices[0] embeds and merges).
+    GpuRetriever(const ::prag::Database& db, const ::prag::IvfIndex& index, const ::prag::PqCodebook& codebook,
+                 std::uint64_t embed_seed, ::prag::RetrievalPerfModel perf, double safety_margin,
+                 const std::vector<int>& devices)
+        : db_(&db), gpu_(Index::from_reference(index, codebook, devices)), nlist_(index.nlist),
+          embedder_(make_embedder(db, embed_seed, devices.at(0))), perf_(perf), safety_margin_(safety_margin) {}
 
     GpuRetriever(const ::prag::Database& db, Index gpu_index, std::uint64_t embed_seed,
                  ::prag::RetrievalPerfModel perf = {}, double safety_margin = 0.10)

@@ -12,7 +12,8 @@
 // Commands:
 //   train   <vectors.f32> <n> <d> <nlist> <nsq> <seed> <out.pragix> [iterations] [sample_cap]
 //   search  <index> <queries.f32> <nq> <nprobe> <k> <out.bin>
-//   bench   <index> <queries.f32> <nq> <nprobe> <k> <threads> <reps> <warmups> [max_seconds]
+//   bench   <index> <queries.f32> <nq> <nprobe> <k> <threads> <reps> <warmups> [max_seconds] [out.bin]
+//           (out.bin: the last timed batch's results, for bench.py's parity check)
 //   calibrate <index> <queries.f32> <nq> <k> <grid_csv> <repeats>
 //   brute   <vectors.f32> <n> <d> <queries.f32> <nq> <k> <out.bin>
 //   rerank  <index> <vectors.f32> <n> <queries.f32> <nq> <nprobe> <k> <out.bin>   (exact_rerank = true)
@@ -148,14 +149,15 @@ int main(int argc, char** argv) {
             write_results(argv[8], res, k);
             return 0;
         }
-        if (cmd == "bench" && (argc == 10 || argc == 11)) {
+        if (cmd == "bench" && argc >= 10 && argc <= 12) {
             double t_load0 = now_s();
             auto [index, codebook] = prag::load_index(argv[2]);
             double t_load = now_s() - t_load0;
             std::size_t nq = std::stoull(argv[4]);
             std::uint32_t nprobe = std::stoul(argv[5]), k = std::stoul(argv[6]);
             int threads = std::stoi(argv[7]), reps = std::stoi(argv[8]), warm = std::stoi(argv[9]);
-            double max_s = argc == 11 ? std::stod(argv[10]) : 1e30;
+            double max_s = argc >= 11 ? std::stod(argv[10]) : 1e30;
+            std::vector<prag::SearchResult> last(nq);
             if (threads <= 0) threads = static_cast<int>(std::thread::hardware_concurrency());
             auto qs = rows(read_f32(argv[3], nq * index.d), nq, index.d);
             std::vector<double> times;
@@ -173,6 +175,7 @@ int main(int argc, char** argv) {
                             if (q >= nq) break;
                             auto res = prag::search(index, codebook, qs[q], {nprobe, k, false});
                             sc += res.scanned_vectors;
+                            last[q] = std::move(res);
                         }
                     });
                 }
@@ -182,6 +185,7 @@ int main(int argc, char** argv) {
                 scanned = sc.load();
                 if (r >= warm && now_s() - t_begin > max_s) break;
             }
+            if (argc == 12) write_results(argv[11], last, k);
             std::vector<double> sorted = times;
             std::sort(sorted.begin(), sorted.end());
             double p50 = sorted[sorted.size() / 2];

@@ -115,6 +115,17 @@ SYMBOLS = [
     ("prag_gpu_embedder_create", C.c_int, [C.c_uint32, C.c_uint64, C.c_uint32, C.c_int, C.POINTER(P)]),
     ("prag_gpu_embedder_free", None, [P]),
     ("prag_gpu_embed", C.c_int, [P, P, C.c_uint32, C.c_uint32, P, P]),
+    ("prag_gpu_index_load_sharded", C.c_int, [C.c_char_p, P, C.c_int, C.POINTER(P)]),
+    ("prag_gpu_index_group", C.c_int, [P, C.c_int, C.POINTER(P)]),
+    ("prag_gpu_index_from_host_sharded", C.c_int,
+     [C.c_uint32, C.c_uint32, C.c_uint32, P, P, P, P, P, P, C.c_int, C.POINTER(P)]),
+    ("prag_gpu_index_synthetic_shard", C.c_int,
+     [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64, C.c_double, P, P, C.c_int, C.c_int, C.c_int,
+      C.POINTER(P)]),
+    ("prag_gpu_comm_unique_id", C.c_int, [P]),
+    ("prag_gpu_comm_init", C.c_int, [P, C.c_int, C.c_int, C.c_int, C.POINTER(P)]),
+    ("prag_gpu_comm_free", None, [P]),
+    ("prag_gpu_index_attach_comm", C.c_int, [P, P]),
 ]
 
 _lib = None

@@ -20,19 +20,8 @@ namespace pg {
 static thread_local std::string g_error;
 void set_error(const std::string& msg) { g_error = msg; }
 
-namespace {
+// (orchestration helpers: declared in internal.h, shared with shard.cu)
 
-struct DeviceGuard {
-    int prev = -1;
-    explicit DeviceGuard(int dev) {
-        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
-        if (prev != dev) cudaSetDevice(dev);
-    }
-    ~DeviceGuard() {
-        int cur;
-        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
-    }
-};
 
 int require_device(int device) {
     int n = 0;
@@ -48,7 +37,7 @@ int require_device(int device) {
     return PRAG_GPU_OK;
 }
 
-}  // namespace
+
 int sm_count(int device) {
     static std::atomic<int> cache[64];
     if (device < 0 || device >= 64) {
@@ -77,7 +66,7 @@ cudaError_t ensure_smem(const void* kernel, size_t bytes) {
     if (e == cudaSuccess) have = bytes;
     return e;
 }
-namespace {
+// (orchestration helpers: declared in internal.h, shared with shard.cu)
 
 bool is_device_ptr(const void* p) {
     if (p == nullptr) return false;
@@ -156,10 +145,8 @@ int upload(prag_gpu_index* ix, const HostIndex& h) {
         set_error("more than 2^32 resident entries on one device; shard the index");
         return PRAG_GPU_CONFIG;
     }
-    std::vector<uint64_t> sorted(ix->host_list_len);
-    std::sort(sorted.begin(), sorted.end(), std::greater<uint64_t>());
-    ix->top_prefix.assign(size_t(nl) + 1, 0);
-    for (uint32_t i = 0; i < nl; ++i) ix->top_prefix[i + 1] = ix->top_prefix[i] + sorted[i];
+    ix->top_prefix = prefix_desc(ix->host_list_len);
+    if (ix->global_top_prefix.empty()) ix->global_top_prefix = ix->top_prefix;
 
     uint64_t* acct = &ix->device_bytes;
     PG_TRY(dmalloc(&d.centroids, size_t(nl) * h.d, acct));
@@ -258,6 +245,9 @@ Workspace* acquire_ws(prag_gpu_index* ix, cudaStream_t s) {
     auto* w = new Workspace();
     w->device = ix->device;
     cudaEventCreateWithFlags(&w->done, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&w->host_ev, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&w->xev, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&w->xev2, cudaEventDisableTiming);
     for (auto& e : w->ev) cudaEventCreate(&e);
     w->busy = true;
     ix->pool.push_back(w);
@@ -289,6 +279,43 @@ int ws_reserve(Workspace* w, size_t bytes, cudaStream_t s) {
     return PRAG_GPU_OK;
 }
 
+int ws_reserve_x(Workspace* w, size_t bytes, cudaStream_t s) {
+    if (w->xbuf_bytes >= bytes) return PRAG_GPU_OK;
+    if (w->xbuf) {
+        PG_CUDA(cudaStreamSynchronize(s));
+        cudaFree(w->xbuf);
+        w->xbuf = nullptr;
+        w->xbuf_bytes = 0;
+    }
+    PG_CUDA(cudaMalloc(&w->xbuf, bytes));
+    w->xbuf_bytes = bytes;
+    return PRAG_GPU_OK;
+}
+
+void free_ws(Workspace* w) {
+    if (!w) return;
+    cudaFree(w->buf);
+    cudaFree(w->stage);
+    cudaFree(w->xbuf);
+    cudaFree(w->win_stat);
+    if (w->host) cudaFreeHost(w->host);
+    if (w->done) cudaEventDestroy(w->done);
+    if (w->host_ev) cudaEventDestroy(w->host_ev);
+    if (w->xev) cudaEventDestroy(w->xev);
+    if (w->xev2) cudaEventDestroy(w->xev2);
+    for (auto& e : w->ev)
+        if (e) cudaEventDestroy(e);
+    delete w;
+}
+
+std::vector<uint64_t> prefix_desc(const std::vector<uint64_t>& sizes) {
+    std::vector<uint64_t> sorted(sizes);
+    std::sort(sorted.begin(), sorted.end(), std::greater<uint64_t>());
+    std::vector<uint64_t> p(sorted.size() + 1, 0);
+    for (size_t i = 0; i < sorted.size(); ++i) p[i + 1] = p[i] + sorted[i];
+    return p;
+}
+
 int ws_reserve_stage(Workspace* w, size_t bytes, cudaStream_t s) {
     if (w->stage_bytes >= bytes) return PRAG_GPU_OK;
     if (w->stage) {
@@ -304,6 +331,8 @@ int ws_reserve_stage(Workspace* w, size_t bytes, cudaStream_t s) {
 
 int ws_reserve_host(Workspace* w, size_t bytes) {
     if (w->host_bytes >= bytes) return PRAG_GPU_OK;
+    if (w->host_pending) PG_CUDA(cudaEventSynchronize(w->host_ev));
+    w->host_pending = false;
     if (w->host) cudaFreeHost(w->host);
     w->host = nullptr;
     size_t b = std::max(bytes, w->host_bytes * 2);
@@ -312,17 +341,6 @@ int ws_reserve_host(Workspace* w, size_t bytes) {
     return PRAG_GPU_OK;
 }
 
-struct Carver {
-    char* base;
-    size_t off = 0;
-    template <typename T>
-    T* take(size_t n) {
-        off = (off + 255) & ~size_t(255);
-        T* p = reinterpret_cast<T*>(base + off);
-        off += std::max<size_t>(n * sizeof(T), 16);
-        return p;
-    }
-};
 
 uint32_t pow2_at_least(uint64_t v) {
     uint64_t p = 1;
@@ -351,7 +369,7 @@ size_t coarse_scratch_floats(const prag_gpu_index* ix, uint32_t nq) {
 
 int run_coarse(const prag_gpu_index* ix, const float* dq, uint32_t nq, uint32_t nprobe, float* coarse,
                uint32_t* probe, float* probe_dist, uint32_t* pkey, uint64_t* ptie, cudaStream_t s,
-               Workspace* prof_ws = nullptr) {
+               Workspace* prof_ws) {
     const DeviceIndex& d = ix->dev;
     unsigned long long* win_stat = nullptr;
     if (prof_ws) {  // profiling: event between K1 and K1b, window-size counter
@@ -580,11 +598,43 @@ int validate(const prag_gpu_index* ix, uint32_t nprobe, uint32_t k) {
     return PRAG_GPU_OK;
 }
 
+bool uses_fast_path(const prag_gpu_index* ix, uint32_t k, bool rerank) {
+    return !rerank && ix->dev.code_layout == 1 && k <= 32 && ix->scan_path == 0;
+}
+
+uint32_t pass_chunk(const prag_gpu_index* ix, uint32_t nq, uint32_t nprobe, uint32_t k, bool rerank) {
+    // Bound candidate memory: chunk the batch so a pass holds <= 192M slots.
+    const std::vector<uint64_t>& tp = ix->global_top_prefix.empty() ? ix->top_prefix : ix->global_top_prefix;
+    const uint64_t max_cand_q = std::max<uint64_t>(1, tp[nprobe]);
+    const uint64_t kSlots = 192ull << 20;
+    uint32_t chunk = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(nq, kSlots / max_cand_q)));
+    if (uses_fast_path(ix, k, rerank)) {
+        // fast path: bound the per-pass LUT images (nq * nprobe * m * 2 KiB) to ~1 GiB
+        const uint64_t img_q = uint64_t(nprobe) * skew_lut_bytes(ix->dev.nsq);
+        chunk = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(nq, (1ull << 30) / img_q)));
+    }
+    return chunk;
+}
+
+// One pass of whatever this handle is: a single index (search_pass), a
+// group of shards (group_pass: per-shard passes + the peer-memory merge), or
+// a rank of a distributed index (dist_pass: local pass + NCCL all-gather +
+// merge). Device queries in, device outputs out, on stream s.
+static int any_pass(prag_gpu_index* ix, Workspace* w, const float* dq, uint32_t nq, uint32_t nprobe, uint32_t k,
+                    uint64_t* o_ids, float* o_dist, uint32_t* o_count, uint64_t* o_scanned, cudaStream_t s,
+                    prag_gpu_timings* tm, bool rerank) {
+    if (ix->is_group()) return group_pass(ix, w, dq, nq, nprobe, k, o_ids, o_dist, o_count, o_scanned, s, rerank,
+                                          nullptr);
+    if (ix->comm) return dist_pass(ix, w, dq, nq, nprobe, k, o_ids, o_dist, o_count, o_scanned, s, tm, rerank);
+    return search_pass(ix, w, dq, nq, nprobe, k, o_ids, o_dist, o_count, o_scanned, s, tm, rerank);
+}
+
 int do_search(prag_gpu_index* ix, const float* queries, uint32_t nq, uint32_t nprobe, uint32_t k,
               uint64_t* out_ids, float* out_dist, uint32_t* out_count, uint64_t* out_scanned, cudaStream_t s,
-              bool rerank = false, bool all_device = false) {
+              bool rerank, bool all_device) {
     PG_TRY(validate(ix, nprobe, k));
-    if (rerank && !ix->emb) {  // annindex.hpp:269-271
+    const bool has_emb = ix->is_group() ? ix->shards[0]->emb != nullptr : ix->emb != nullptr;
+    if (rerank && !has_emb) {  // annindex.hpp:269-271
         set_error("search: exact_rerank requires raw embeddings");
         return PRAG_GPU_CONFIG;
     }
@@ -604,15 +654,7 @@ int do_search(prag_gpu_index* ix, const float* queries, uint32_t nq, uint32_t np
     const bool q_dev = all_device || is_device_ptr(queries);
     const bool o_dev = all_device || (is_device_ptr(out_ids) && is_device_ptr(out_dist) && is_device_ptr(out_count) &&
                                       (out_scanned == nullptr || is_device_ptr(out_scanned)));
-    // Bound candidate memory: chunk the batch so a pass holds <= 192M slots.
-    const uint64_t max_cand_q = std::max<uint64_t>(1, ix->top_prefix[nprobe]);
-    const uint64_t kSlots = 192ull << 20;
-    uint32_t chunk = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(nq, kSlots / max_cand_q)));
-    if (!rerank && d.code_layout == 1 && k <= 32 && ix->scan_path == 0) {
-        // fast path: bound the per-pass LUT images (nq * nprobe * m * 2 KiB) to ~1 GiB
-        const uint64_t img_q = uint64_t(nprobe) * skew_lut_bytes(d.nsq);
-        chunk = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>(nq, (1ull << 30) / img_q)));
-    }
+    const uint32_t chunk = pass_chunk(ix, nq, nprobe, k, rerank);
 
     Workspace* w = acquire_ws(ix, s);
     struct Rel {
@@ -643,8 +685,11 @@ int do_search(prag_gpu_index* ix, const float* queries, uint32_t nq, uint32_t np
             if (q_pinned) {
                 PG_CUDA(cudaMemcpyAsync(dq_stage, src, size_t(n) * d.d * 4, cudaMemcpyHostToDevice, s));
             } else {
+                if (w->host_pending) PG_CUDA(cudaEventSynchronize(w->host_ev));
                 std::memcpy(w->host, src, size_t(n) * d.d * 4);
                 PG_CUDA(cudaMemcpyAsync(dq_stage, w->host, size_t(n) * d.d * 4, cudaMemcpyHostToDevice, s));
+                PG_CUDA(cudaEventRecord(w->host_ev, s));
+                w->host_pending = true;
             }
             dq = dq_stage;
         }
@@ -666,7 +711,7 @@ int do_search(prag_gpu_index* ix, const float* queries, uint32_t nq, uint32_t np
             os = cv.take<uint64_t>(n);
             stage_out_bytes = cv.off;
         }
-        PG_TRY(search_pass(ix, w, dq, n, nprobe, k, oi, od, oc, os, s, tmp, rerank));
+        PG_TRY(any_pass(ix, w, dq, n, nprobe, k, oi, od, oc, os, s, tmp, rerank));
         if (!o_dev) {
             // device -> pinned -> caller: the four outputs sit in one staged
             // block, so one copy brings them back (same carve offsets)
@@ -691,66 +736,23 @@ int do_search(prag_gpu_index* ix, const float* queries, uint32_t nq, uint32_t np
     return PRAG_GPU_OK;
 }
 
-}  // namespace
+
 }  // namespace pg
 
-using namespace pg;
+namespace pg {
 
-extern "C" {
-
-const char* prag_gpu_last_error(void) { return g_error.c_str(); }
-int prag_gpu_version(void) { return 1; }
-
-int prag_gpu_device_count(void) {
-    int n = 0;
-    if (cudaGetDeviceCount(&n) != cudaSuccess) {
-        cudaGetLastError();
-        return 0;
-    }
-    return n;
-}
-
-int prag_gpu_index_load(const char* path, int device, prag_gpu_index** out) {
-    if (!out || !path) {
-        set_error("null argument");
-        return PRAG_GPU_CONFIG;
-    }
-    *out = nullptr;
-    PG_TRY(require_device(device));
-    HostIndex h;
-    PG_TRY(read_pragix01(path, h, nullptr));
-    auto ix = std::make_unique<prag_gpu_index>();
-    return finish_load(ix, h, device, out);
-}
-
-int prag_gpu_index_load_shard(const char* path, int device, int rank, int world, prag_gpu_index** out) {
-    if (!out || !path || world < 1 || rank < 0 || rank >= world) {
-        set_error("invalid shard arguments");
-        return PRAG_GPU_CONFIG;
-    }
-    *out = nullptr;
-    PG_TRY(require_device(device));
-    std::vector<uint64_t> sizes;
-    PG_TRY(read_pragix01_list_sizes(path, sizes));
-    std::vector<uint32_t> owner(sizes.size());
-    plan_shards_lpt(sizes.data(), uint32_t(sizes.size()), uint32_t(world), owner.data());
-    std::vector<uint8_t> keep(sizes.size());
-    for (size_t l = 0; l < sizes.size(); ++l) keep[l] = owner[l] == uint32_t(rank);
-    HostIndex h;
-    PG_TRY(read_pragix01(path, h, &keep));
-    auto ix = std::make_unique<prag_gpu_index>();
-    ix->shard_rank = rank;
-    ix->shard_world = world;
-    return finish_load(ix, h, device, out);
-}
-
-int prag_gpu_index_synthetic(uint32_t nlist, uint32_t d, uint32_t nsq, uint64_t ntotal, uint64_t seed, double sigma,
-                             const float* centroids, const float* codewords, int device, prag_gpu_index** out) {
+int build_synthetic(uint32_t nlist, uint32_t d, uint32_t nsq, uint64_t ntotal, uint64_t seed, double sigma,
+                    const float* centroids, const float* codewords, int rank, int world, int device,
+                    prag_gpu_index** out) {
     if (!out || !centroids || !codewords) {
         set_error("null argument");
         return PRAG_GPU_CONFIG;
     }
     *out = nullptr;
+    if (world < 1 || rank < 0 || rank >= world) {
+        set_error("invalid shard arguments");
+        return PRAG_GPU_CONFIG;
+    }
     if ((nsq != 32 && nsq != 64) || d % nsq != 0 || d / nsq > 16 || d % 4 != 0 || nlist == 0) {
         set_error("synthetic index: needs m in {32, 64}, d % m == 0, d / m <= 16, d % 4 == 0, nlist >= 1");
         return PRAG_GPU_CONFIG;
@@ -766,41 +768,52 @@ int prag_gpu_index_synthetic(uint32_t nlist, uint32_t d, uint32_t nsq, uint64_t 
     dv.nsq = nsq;
     dv.sub_dim = d / nsq;
     dv.plain_codes = false;
-    std::vector<uint64_t> sizes;
+    std::vector<uint64_t> sizes;  // the whole index's lists
     synth_list_sizes(nlist, ntotal, seed, sigma, sizes);
-    std::vector<uint64_t> loff(size_t(nlist) + 1, 0), poff(size_t(nlist) + 1, 0), soff(size_t(nlist) + 1, 0);
+    // shard: the lists prag_gpu_plan_shards gives `rank`; every entry keeps
+    // its global list-major position g (chunk id g, codes from g)
+    std::vector<uint64_t> rsz(sizes);
+    if (world > 1) {
+        std::vector<uint32_t> owner(nlist);
+        plan_shards_lpt(sizes.data(), nlist, uint32_t(world), owner.data());
+        for (uint32_t l = 0; l < nlist; ++l)
+            if (owner[l] != uint32_t(rank)) rsz[l] = 0;
+    }
+    ix->shard_rank = rank;
+    ix->shard_world = world;
+    ix->global_top_prefix = prefix_desc(sizes);
+    std::vector<uint64_t> gbase(size_t(nlist) + 1, 0), poff(size_t(nlist) + 1, 0), soff(size_t(nlist) + 1, 0);
     std::vector<uint32_t> len(nlist);
     uint32_t maxlen = 0;
+    uint64_t resident = 0;
     for (uint32_t l = 0; l < nlist; ++l) {
         if (sizes[l] >= (1ull << 32)) {
             set_error("synthetic index: list exceeds 2^32 entries");
             return PRAG_GPU_CONFIG;
         }
-        len[l] = uint32_t(sizes[l]);
+        len[l] = uint32_t(rsz[l]);
         maxlen = std::max(maxlen, len[l]);
-        loff[l + 1] = loff[l] + sizes[l];
-        poff[l + 1] = poff[l] + (sizes[l] + kListPad - 1) / kListPad * kListPad;
-        soff[l + 1] = soff[l] + (sizes[l] ? (sizes[l] + 31) / 32 + 1 : 0);
+        resident += rsz[l];
+        gbase[l + 1] = gbase[l] + sizes[l];
+        poff[l + 1] = poff[l] + (rsz[l] + kListPad - 1) / kListPad * kListPad;
+        soff[l + 1] = soff[l] + (rsz[l] ? (rsz[l] + 31) / 32 + 1 : 0);
     }
     if (poff[nlist] >= (1ull << 32)) {
         set_error("more than 2^32 resident entries on one device; shard the index");
         return PRAG_GPU_CONFIG;
     }
-    dv.ntotal = ntotal;
+    dv.ntotal = resident;
     dv.npadded = poff[nlist];
     dv.max_list_len = maxlen;
-    ix->host_list_len = sizes;
-    std::vector<uint64_t> sorted(sizes);
-    std::sort(sorted.begin(), sorted.end(), std::greater<uint64_t>());
-    ix->top_prefix.assign(size_t(nlist) + 1, 0);
-    for (uint32_t i = 0; i < nlist; ++i) ix->top_prefix[i + 1] = ix->top_prefix[i] + sorted[i];
+    ix->host_list_len = rsz;
+    ix->top_prefix = prefix_desc(rsz);
     uint64_t* acct = &ix->device_bytes;
     auto fail = [&](int rc) {
         free_device_index(dv);
         return rc;
     };
     int rc = PRAG_GPU_OK;
-    uint64_t* dloff = nullptr;
+    uint64_t* dloff = nullptr;  // [2][nlist + 1]: global entry base, resident length
     const size_t cw = size_t(nsq) * 256 * (d / nsq);
     std::vector<float> t(size_t(nlist) * d);
     if ((rc = dmalloc(&dv.centroids, size_t(nlist) * d, acct)) ||
@@ -808,7 +821,7 @@ int prag_gpu_index_synthetic(uint32_t nlist, uint32_t d, uint32_t nsq, uint64_t 
         (rc = dmalloc(&dv.codewords, cw, acct)) || (rc = dmalloc(&dv.list_off, size_t(nlist) + 1, acct)) ||
         (rc = dmalloc(&dv.list_len, nlist, acct)) || (rc = dmalloc(&dv.skew_off, size_t(nlist) + 1, acct)) ||
         (rc = dmalloc(&dv.ids, dv.npadded, acct)) || (rc = dmalloc(&dv.skew_codes, soff[nlist] * 32 * nsq, acct)) ||
-        (rc = dmalloc(&dloff, size_t(nlist) + 1, nullptr)))
+        (rc = dmalloc(&dloff, 2 * (size_t(nlist) + 1), nullptr)))
         return fail(rc);
     for (uint32_t c = 0; c < nlist; ++c)
         for (uint32_t j = 0; j < d; ++j) t[(size_t(j / 4) * nlist + c) * 4 + (j % 4)] = centroids[size_t(c) * d + j];
@@ -828,14 +841,15 @@ int prag_gpu_index_synthetic(uint32_t nlist, uint32_t d, uint32_t nsq, uint64_t 
     cp(dv.list_off, poff.data(), poff.size() * 8);
     cp(dv.list_len, len.data(), len.size() * 4);
     cp(dv.skew_off, soff.data(), soff.size() * 8);
-    cp(dloff, loff.data(), loff.size() * 8);
+    cp(dloff, gbase.data(), gbase.size() * 8);
+    cp(dloff + nlist + 1, rsz.data(), size_t(nlist) * 8);
     if (e != cudaSuccess) {
         cudaFree(dloff);
         set_error(std::string("CUDA error (synthetic index upload): ") + cudaGetErrorString(e));
         return fail(PRAG_GPU_CUDA);
     }
-    rc = launch_synth_codes(nsq, dloff, dv.skew_off, nlist, seed, dv.skew_codes, soff[nlist], dv.ids, dv.list_off,
-                            dv.npadded);
+    rc = launch_synth_codes(nsq, dloff, dloff + nlist + 1, dv.skew_off, nlist, seed, dv.skew_codes, soff[nlist], dv.ids,
+                            dv.list_off, dv.npadded);
     cudaFree(dloff);
     if (rc) return fail(rc);
     dv.code_layout = 1;
@@ -856,9 +870,85 @@ int prag_gpu_index_synthetic(uint32_t nlist, uint32_t d, uint32_t nsq, uint64_t 
     return PRAG_GPU_OK;
 }
 
+
+}  // namespace pg
+
+using namespace pg;
+
+extern "C" {
+
+const char* prag_gpu_last_error(void) { return g_error.c_str(); }
+int prag_gpu_version(void) { return 1; }
+
+int prag_gpu_device_count(void) {
+    PG_API_BEGIN
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+    PG_API_END
+}
+
+int prag_gpu_index_load(const char* path, int device, prag_gpu_index** out) {
+    PG_API_BEGIN
+    if (!out || !path) {
+        set_error("null argument");
+        return PRAG_GPU_CONFIG;
+    }
+    *out = nullptr;
+    PG_TRY(require_device(device));
+    HostIndex h;
+    PG_TRY(read_pragix01(path, h, nullptr));
+    auto ix = std::make_unique<prag_gpu_index>();
+    return finish_load(ix, h, device, out);
+    PG_API_END
+}
+
+int prag_gpu_index_load_shard(const char* path, int device, int rank, int world, prag_gpu_index** out) {
+    PG_API_BEGIN
+    if (!out || !path || world < 1 || rank < 0 || rank >= world) {
+        set_error("invalid shard arguments");
+        return PRAG_GPU_CONFIG;
+    }
+    *out = nullptr;
+    PG_TRY(require_device(device));
+    std::vector<uint64_t> sizes;
+    PG_TRY(read_pragix01_list_sizes(path, sizes));
+    std::vector<uint32_t> owner(sizes.size());
+    plan_shards_lpt(sizes.data(), uint32_t(sizes.size()), uint32_t(world), owner.data());
+    std::vector<uint8_t> keep(sizes.size());
+    for (size_t l = 0; l < sizes.size(); ++l) keep[l] = owner[l] == uint32_t(rank);
+    HostIndex h;
+    PG_TRY(read_pragix01(path, h, &keep));
+    auto ix = std::make_unique<prag_gpu_index>();
+    ix->shard_rank = rank;
+    ix->shard_world = world;
+    ix->global_top_prefix = prefix_desc(sizes);
+    return finish_load(ix, h, device, out);
+    PG_API_END
+}
+
+int prag_gpu_index_synthetic(uint32_t nlist, uint32_t d, uint32_t nsq, uint64_t ntotal, uint64_t seed, double sigma,
+                             const float* centroids, const float* codewords, int device, prag_gpu_index** out) {
+    PG_API_BEGIN
+    return build_synthetic(nlist, d, nsq, ntotal, seed, sigma, centroids, codewords, 0, 1, device, out);
+    PG_API_END
+}
+
+int prag_gpu_index_synthetic_shard(uint32_t nlist, uint32_t d, uint32_t nsq, uint64_t ntotal, uint64_t seed,
+                                   double sigma, const float* centroids, const float* codewords, int rank,
+                                   int world, int device, prag_gpu_index** out) {
+    PG_API_BEGIN
+    return build_synthetic(nlist, d, nsq, ntotal, seed, sigma, centroids, codewords, rank, world, device, out);
+    PG_API_END
+}
+
 int prag_gpu_index_from_host(uint32_t nlist, uint32_t d, uint32_t nsq, const float* centroids,
                              const float* codewords, const uint64_t* list_off, const uint64_t* ids,
                              const uint8_t* codes, int device, prag_gpu_index** out) {
+    PG_API_BEGIN
     if (!out) {
         set_error("null argument");
         return PRAG_GPU_CONFIG;
@@ -888,22 +978,20 @@ int prag_gpu_index_from_host(uint32_t nlist, uint32_t d, uint32_t nsq, const flo
     h.ntotal_global = n;
     auto ix = std::make_unique<prag_gpu_index>();
     return finish_load(ix, h, device, out);
+    PG_API_END
 }
 
 void prag_gpu_index_free(prag_gpu_index* ix) {
     if (!ix) return;
+    if (ix->is_group()) {
+        free_group(ix);
+        delete ix;
+        return;
+    }
     {
         DeviceGuard g(ix->device);
         cudaDeviceSynchronize();
-        for (Workspace* w : ix->pool) {
-            cudaFree(w->buf);
-            cudaFree(w->stage);
-            cudaFree(w->win_stat);
-            if (w->host) cudaFreeHost(w->host);
-            cudaEventDestroy(w->done);
-            for (auto& e : w->ev) cudaEventDestroy(e);
-            delete w;
-        }
+        for (Workspace* w : ix->pool) free_ws(w);
         free_device_index(ix->dev);
         cudaFree(ix->emb);
     }
@@ -911,6 +999,7 @@ void prag_gpu_index_free(prag_gpu_index* ix) {
 }
 
 int prag_gpu_index_describe(const prag_gpu_index* ix, prag_gpu_index_desc* o) {
+    PG_API_BEGIN
     if (!ix || !o) {
         set_error("null argument");
         return PRAG_GPU_CONFIG;
@@ -928,38 +1017,49 @@ int prag_gpu_index_describe(const prag_gpu_index* ix, prag_gpu_index_desc* o) {
     o->shard_world = ix->shard_world;
     o->device_bytes = ix->device_bytes;
     o->code_layout = ix->dev.code_layout;
+    if (ix->is_group()) {  // the whole index, over shards.size() shards
+        o->shard_world = int32_t(ix->shards.size());
+        o->device_bytes = 0;
+        for (const prag_gpu_index* sh : ix->shards) o->device_bytes += sh->device_bytes;
+    }
     return PRAG_GPU_OK;
+    PG_API_END
 }
 
 uint32_t prag_gpu_index_nlist(const prag_gpu_index* ix) { return ix ? ix->dev.nlist : 0; }
 
 int prag_gpu_index_list_sizes(const prag_gpu_index* ix, uint64_t* out) {
+    PG_API_BEGIN
     if (!ix || !out) {
         set_error("null argument");
         return PRAG_GPU_CONFIG;
     }
     std::copy(ix->host_list_len.begin(), ix->host_list_len.end(), out);
     return PRAG_GPU_OK;
+    PG_API_END
 }
 
 int prag_gpu_search(prag_gpu_index* ix, const float* queries, uint32_t nq, uint32_t nprobe, uint32_t k,
                     uint64_t* out_ids, float* out_dist, uint32_t* out_count, uint64_t* out_scanned,
                     void* stream) {
+    PG_API_BEGIN
     if (!ix) {
         set_error("null index");
         return PRAG_GPU_CONFIG;
     }
     return do_search(ix, queries, nq, nprobe, k, out_ids, out_dist, out_count, out_scanned,
                      static_cast<cudaStream_t>(stream));
+    PG_API_END
 }
 
 int prag_gpu_index_store(const prag_gpu_index* ix, const char* path) {
+    PG_API_BEGIN
     if (!ix || !path) {
         set_error("null argument");
         return PRAG_GPU_CONFIG;
     }
     const DeviceIndex& d = ix->dev;
-    if (ix->shard_world > 1) {
+    if (ix->shard_world > 1 || ix->is_group()) {
         set_error("store: a shard holds only part of the lists; store the full index");
         return PRAG_GPU_CONFIG;
     }
@@ -1008,33 +1108,31 @@ int prag_gpu_index_store(const prag_gpu_index* ix, const char* path) {
         return PRAG_GPU_FORMAT;
     }
     return PRAG_GPU_OK;
+    PG_API_END
 }
 
 int prag_gpu_search_device(prag_gpu_index* ix, const float* queries, uint32_t nq, uint32_t nprobe, uint32_t k,
                            uint64_t* out_ids, float* out_dist, uint32_t* out_count, uint64_t* out_scanned,
                            void* stream) {
+    PG_API_BEGIN
     if (!ix) {
         set_error("null index");
         return PRAG_GPU_CONFIG;
     }
     return do_search(ix, queries, nq, nprobe, k, out_ids, out_dist, out_count, out_scanned,
                      static_cast<cudaStream_t>(stream), false, true);
+    PG_API_END
 }
 
 }  // extern "C"
 
-struct prag_gpu_plan {
-    prag_gpu_index* ix = nullptr;
-    pg::Workspace* w = nullptr;
-    cudaGraph_t graph = nullptr;
-    cudaGraphExec_t exec = nullptr;
-};
 
 extern "C" {
 
 int prag_gpu_plan_create(prag_gpu_index* ix, const float* queries, uint32_t nq, uint32_t nprobe, uint32_t k,
                          uint64_t* out_ids, float* out_dist, uint32_t* out_count, uint64_t* out_scanned,
                          void* stream, prag_gpu_plan** out) {
+    PG_API_BEGIN
     if (!ix || !out || !queries || !out_ids || !out_dist || !out_count || !out_scanned || nq == 0) {
         set_error("plan: null argument or empty batch");
         return PRAG_GPU_CONFIG;
@@ -1046,14 +1144,7 @@ int prag_gpu_plan_create(prag_gpu_index* ix, const float* queries, uint32_t nq, 
         set_error("plan: queries and outputs must be device memory");
         return PRAG_GPU_CONFIG;
     }
-    const DeviceIndex& d = ix->dev;
-    if (d.code_layout == 1 && k <= 32 && ix->scan_path == 0) {
-        const uint64_t img_q = uint64_t(nprobe) * skew_lut_bytes(d.nsq);
-        if (uint64_t(nq) * img_q > (1ull << 30)) {
-            set_error("plan: batch too large for one pass (split it)");
-            return PRAG_GPU_CONFIG;
-        }
-    } else if (uint64_t(nq) * std::max<uint64_t>(1, ix->top_prefix[nprobe]) > (192ull << 20)) {
+    if (pass_chunk(ix, nq, nprobe, k, false) < nq) {
         set_error("plan: batch too large for one pass (split it)");
         return PRAG_GPU_CONFIG;
     }
@@ -1061,6 +1152,12 @@ int prag_gpu_plan_create(prag_gpu_index* ix, const float* queries, uint32_t nq, 
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     auto plan = std::make_unique<prag_gpu_plan>();
     plan->ix = ix;
+    if (ix->is_group()) {  // per-shard graphs on their own devices + the root merge
+        PG_TRY(group_plan_create(ix, queries, nq, nprobe, k, out_ids, out_dist, out_count, out_scanned, s,
+                                 &plan->group));
+        *out = plan.release();
+        return PRAG_GPU_OK;
+    }
     plan->w = new Workspace();
     plan->w->device = ix->device;
     PG_CUDA(cudaEventCreateWithFlags(&plan->w->done, cudaEventDisableTiming));
@@ -1070,22 +1167,29 @@ int prag_gpu_plan_create(prag_gpu_index* ix, const float* queries, uint32_t nq, 
             if (!p) return;
             if (p->exec) cudaGraphExecDestroy(p->exec);
             if (p->graph) cudaGraphDestroy(p->graph);
-            cudaFree(p->w->buf);
-            cudaFree(p->w->stage);
-            cudaEventDestroy(p->w->done);
-            delete p->w;
+            free_ws(p->w);
         }
     } cleanup{plan.get()};
     // one ordinary pass sizes the plan's own workspace, then the same pass is
-    // captured (no allocation or host synchronisation inside it)
-    PG_TRY(search_pass(ix, plan->w, queries, nq, nprobe, k, out_ids, out_dist, out_count, out_scanned, s, nullptr,
-                       false));
+    // captured (no allocation or host synchronisation inside it). On a
+    // distributed shard both passes are collective (every rank creates the
+    // plan) and the capture holds the NCCL all-gather.
+    PG_TRY(any_pass(ix, plan->w, queries, nq, nprobe, k, out_ids, out_dist, out_count, out_scanned, s, nullptr,
+                    false));
     PG_CUDA(cudaStreamSynchronize(s));
-    PG_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-    const int rc = search_pass(ix, plan->w, queries, nq, nprobe, k, out_ids, out_dist, out_count, out_scanned, s,
-                               nullptr, false);
+    // capture on a private stream: the caller's may be the legacy default
+    // stream, which cannot be captured (the graph launches on any stream)
+    cudaStream_t cap = nullptr;
+    PG_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+    struct CapStream {
+        cudaStream_t s;
+        ~CapStream() { cudaStreamDestroy(s); }
+    } cap_guard{cap};
+    PG_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+    const int rc = any_pass(ix, plan->w, queries, nq, nprobe, k, out_ids, out_dist, out_count, out_scanned, cap,
+                            nullptr, false);
     cudaGraph_t graph = nullptr;
-    const cudaError_t ce = cudaStreamEndCapture(s, &graph);
+    const cudaError_t ce = cudaStreamEndCapture(cap, &graph);
     if (rc != PRAG_GPU_OK) {
         if (graph) cudaGraphDestroy(graph);
         return rc;
@@ -1096,45 +1200,58 @@ int prag_gpu_plan_create(prag_gpu_index* ix, const float* queries, uint32_t nq, 
     cleanup.p = nullptr;
     *out = plan.release();
     return PRAG_GPU_OK;
+    PG_API_END
 }
 
 int prag_gpu_plan_launch(prag_gpu_plan* plan, void* stream) {
+    PG_API_BEGIN
+    if (plan && plan->group) return group_plan_launch(plan->ix, plan->group, static_cast<cudaStream_t>(stream));
     if (!plan || !plan->exec) {
         set_error("plan: null plan");
         return PRAG_GPU_CONFIG;
     }
     PG_CUDA(cudaGraphLaunch(plan->exec, static_cast<cudaStream_t>(stream)));
     return PRAG_GPU_OK;
+    PG_API_END
 }
 
 void prag_gpu_plan_free(prag_gpu_plan* plan) {
     if (!plan) return;
+    if (plan->group) {
+        group_plan_free(plan->ix, plan->group);
+        delete plan;
+        return;
+    }
     DeviceGuard g(plan->ix->device);
     cudaDeviceSynchronize();
     if (plan->exec) cudaGraphExecDestroy(plan->exec);
     if (plan->graph) cudaGraphDestroy(plan->graph);
-    cudaFree(plan->w->buf);
-    cudaFree(plan->w->stage);
-    cudaEventDestroy(plan->w->done);
-    delete plan->w;
+    free_ws(plan->w);
     delete plan;
 }
 
 int prag_gpu_search_rerank(prag_gpu_index* ix, const float* queries, uint32_t nq, uint32_t nprobe, uint32_t k,
                            uint64_t* out_ids, float* out_dist, uint32_t* out_count, uint64_t* out_scanned,
                            void* stream) {
+    PG_API_BEGIN
     if (!ix) {
         set_error("null index");
         return PRAG_GPU_CONFIG;
     }
     return do_search(ix, queries, nq, nprobe, k, out_ids, out_dist, out_count, out_scanned,
                      static_cast<cudaStream_t>(stream), true);
+    PG_API_END
 }
 
 int prag_gpu_index_set_embeddings(prag_gpu_index* ix, const float* emb, uint64_t n) {
+    PG_API_BEGIN
     if (!ix || (!emb && n)) {
         set_error("null argument");
         return PRAG_GPU_CONFIG;
+    }
+    if (ix->is_group()) {  // every shard reranks its own candidates
+        for (prag_gpu_index* sh : ix->shards) PG_TRY(prag_gpu_index_set_embeddings(sh, emb, n));
+        return PRAG_GPU_OK;
     }
     DeviceGuard g(ix->device);
     PG_CUDA(cudaDeviceSynchronize());
@@ -1162,10 +1279,12 @@ int prag_gpu_index_set_embeddings(prag_gpu_index* ix, const float* emb, uint64_t
     ix->emb = e;
     ix->emb_n = n;
     return PRAG_GPU_OK;
+    PG_API_END
 }
 
 int prag_gpu_brute_force(const float* vectors, uint64_t n, uint32_t d, const float* queries, uint32_t nq,
                          uint32_t k, int device, uint64_t* out_ids, float* out_dist, uint32_t* out_count) {
+    PG_API_BEGIN
     if (k < 1) {  // annindex.hpp:246
         set_error("brute_force_search: k must be >= 1");
         return PRAG_GPU_CONFIG;
@@ -1215,16 +1334,19 @@ int prag_gpu_brute_force(const float* vectors, uint64_t n, uint32_t d, const flo
         PG_CUDA(cudaMemcpy(out_count + q0, b.p[7], size_t(m) * 4, cudaMemcpyDefault));
     }
     return PRAG_GPU_OK;
+    PG_API_END
 }
 
 int prag_gpu_probe(prag_gpu_index* ix, const float* queries, uint32_t nq, uint32_t nprobe, uint32_t* out_lists,
                    float* out_dist, void* stream) {
+    PG_API_BEGIN
     if (!ix) {
         set_error("null index");
         return PRAG_GPU_CONFIG;
     }
     PG_TRY(validate(ix, nprobe, 1));
     if (nq == 0) return PRAG_GPU_OK;
+    if (ix->is_group()) ix = ix->shards[0];  // centroids are replicated: every shard has the probe order
     DeviceGuard g(ix->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const DeviceIndex& d = ix->dev;
@@ -1261,9 +1383,11 @@ int prag_gpu_probe(prag_gpu_index* ix, const float* queries, uint32_t nq, uint32
     if (out_dist) PG_CUDA(cudaMemcpyAsync(out_dist, pd, size_t(nq) * nprobe * 4, cudaMemcpyDefault, s));
     PG_CUDA(cudaStreamSynchronize(s));
     return PRAG_GPU_OK;
+    PG_API_END
 }
 
 int prag_gpu_plan_shards(const uint64_t* sizes, uint32_t nlist, uint32_t world, uint32_t* owner) {
+    PG_API_BEGIN
     if ((!sizes || !owner) && nlist) {
         set_error("null argument");
         return PRAG_GPU_CONFIG;
@@ -1274,11 +1398,13 @@ int prag_gpu_plan_shards(const uint64_t* sizes, uint32_t nlist, uint32_t world, 
     }
     plan_shards_lpt(sizes, nlist, world, owner);
     return PRAG_GPU_OK;
+    PG_API_END
 }
 
 int prag_gpu_merge_topk(const uint64_t* ids, const float* dist, const uint32_t* count, const uint64_t* scanned,
                         uint32_t nparts, uint32_t nq, uint32_t kin, uint32_t k, uint64_t* out_ids,
                         float* out_dist, uint32_t* out_count, uint64_t* out_scanned, int device, void* stream) {
+    PG_API_BEGIN
     if (k < 1) {
         set_error("merge: k must be >= 1");
         return PRAG_GPU_CONFIG;
@@ -1331,6 +1457,7 @@ int prag_gpu_merge_topk(const uint64_t* ids, const float* dist, const uint32_t* 
     if (!(is_device_ptr(out_ids) && is_device_ptr(out_dist) && is_device_ptr(out_count)))
         PG_CUDA(cudaStreamSynchronize(s));
     return PRAG_GPU_OK;
+    PG_API_END
 }
 
 // ---------------------------------------------------- performance model
@@ -1412,6 +1539,7 @@ static int calibrate_core(const std::function<int(uint32_t, double*)>& measure, 
 int prag_gpu_calibrate_retrieval(prag_gpu_index* ix, const float* queries, uint32_t nq, uint32_t k,
                                  const uint32_t* grid, uint32_t grid_len, int repeats, int warmups,
                                  prag_gpu_perf_model* out, double* out_lat) {
+    PG_API_BEGIN
     if (!ix || !queries || nq == 0) {
         set_error("calibrate: need an index and >= 1 query");
         return PRAG_GPU_CONFIG;
@@ -1433,10 +1561,12 @@ int prag_gpu_calibrate_retrieval(prag_gpu_index* ix, const float* queries, uint3
             return PRAG_GPU_CONFIG;
         }
     return calibrate_core(measure, grid, grid_len, repeats, warmups, out, out_lat);
+    PG_API_END
 }
 
 int prag_gpu_calibrate_with(prag_gpu_measure_fn fn, void* ctx, const uint32_t* grid, uint32_t grid_len,
                             int repeats, int warmups, prag_gpu_perf_model* out) {
+    PG_API_BEGIN
     if (!fn) {
         set_error("null measure function");
         return PRAG_GPU_CONFIG;
@@ -1446,6 +1576,7 @@ int prag_gpu_calibrate_with(prag_gpu_measure_fn fn, void* ctx, const uint32_t* g
         return PRAG_GPU_OK;
     };
     return calibrate_core(measure, grid, grid_len, repeats, warmups, out, nullptr);
+    PG_API_END
 }
 
 uint32_t prag_gpu_select_nprobe(const prag_gpu_perf_model* m, double budget_s, uint32_t nlist, double margin) {
@@ -1460,40 +1591,52 @@ uint32_t prag_gpu_select_nprobe(const prag_gpu_perf_model* m, double budget_s, u
 }
 
 int prag_gpu_set_scan_path(prag_gpu_index* ix, int path) {
+    PG_API_BEGIN
     if (!ix || path < 0 || path > 1) {
         set_error("scan path must be 0 (auto) or 1 (generic)");
         return PRAG_GPU_CONFIG;
     }
     ix->scan_path = path;
+    for (prag_gpu_index* sh : ix->shards) sh->scan_path = path;
     return PRAG_GPU_OK;
+    PG_API_END
 }
 
 int prag_gpu_set_coarse_path(prag_gpu_index* ix, int path) {
+    PG_API_BEGIN
     if (!ix || path < 0 || path > 1) {
         set_error("coarse path must be 0 (auto) or 1 (exact SIMT)");
         return PRAG_GPU_CONFIG;
     }
     ix->coarse_path = path;
+    for (prag_gpu_index* sh : ix->shards) sh->coarse_path = path;
     return PRAG_GPU_OK;
+    PG_API_END
 }
 
 int prag_gpu_set_profiling(prag_gpu_index* ix, int enabled) {
+    PG_API_BEGIN
     if (!ix) {
         set_error("null index");
         return PRAG_GPU_CONFIG;
     }
     ix->profiling = enabled != 0;
+    for (prag_gpu_index* sh : ix->shards) sh->profiling = enabled != 0;
     return PRAG_GPU_OK;
+    PG_API_END
 }
 
 int prag_gpu_last_timings(const prag_gpu_index* ix, prag_gpu_timings* out) {
+    PG_API_BEGIN
     if (!ix || !out) {
         set_error("null argument");
         return PRAG_GPU_CONFIG;
     }
+    if (ix->is_group()) ix = ix->shards[0];  // the root shard's passes
     std::lock_guard<std::mutex> lk(const_cast<prag_gpu_index*>(ix)->mu);
     *out = ix->last;
     return PRAG_GPU_OK;
+    PG_API_END
 }
 
 }  // extern "C"

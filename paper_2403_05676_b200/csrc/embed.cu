@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdint>
 #include <memory>
+#include <unordered_map>
 #include <vector>
 
 #include "internal.h"
@@ -25,6 +26,8 @@ struct prag_gpu_embedder {
     uint32_t* tok = nullptr; // staging for host token chunks
     float* out = nullptr;    // staging for host outputs
     size_t tok_cap = 0, out_cap = 0;
+    float* extra = nullptr;  // per-call rows for token ids >= vocab (host tokens)
+    size_t extra_cap = 0;    // floats
 };
 
 namespace pg {
@@ -78,7 +81,11 @@ constexpr int kEmbThreads = 128;
 // One CTA per chunk. Thread i accumulates dims i, i + 128, ... over the
 // chunk's tokens in order (tokendb.hpp:99-103); one thread folds the squared
 // norm sequentially over dims (:104-105); every thread divides (:110).
+// Token rows: ids < vocab from the resident table, ids in [vocab, vocab +
+// n_extra) from this call's extra rows (host-computed for ids the database
+// vocabulary did not cover; the staged tokens are remapped to them).
 __global__ void __launch_bounds__(kEmbThreads) embed_kernel(const float* __restrict__ table, uint32_t vocab, uint32_t d,
+                                                            const float* __restrict__ extra, uint32_t n_extra,
                                                             const uint32_t* __restrict__ tokens, uint32_t m,
                                                             float* __restrict__ out, uint32_t* __restrict__ bad) {
     extern __shared__ double acc_s[];  // [d]
@@ -90,6 +97,10 @@ __global__ void __launch_bounds__(kEmbThreads) embed_kernel(const float* __restr
         for (uint32_t t = 0; t < m; ++t) {
             const uint32_t tok = tk[t];
             if (tok == 0) continue;  // kPadToken (common.hpp:16)
+            if (tok - vocab < n_extra) {  // (unsigned: false for tok < vocab)
+                acc = __dadd_rn(acc, double(__ldg(extra + size_t(tok - vocab) * d + i)));
+                continue;
+            }
             if (tok >= vocab) {
                 if (i == 0) atomicExch(bad, 1u);
                 continue;
@@ -127,6 +138,7 @@ using namespace pg;
 extern "C" {
 
 int prag_gpu_embedder_create(uint32_t d, uint64_t seed, uint32_t vocab, int device, prag_gpu_embedder** out) {
+    PG_API_BEGIN
     if (!out) {
         set_error("null argument");
         return PRAG_GPU_CONFIG;
@@ -166,6 +178,7 @@ int prag_gpu_embedder_create(uint32_t d, uint64_t seed, uint32_t vocab, int devi
     }
     *out = e.release();
     return PRAG_GPU_OK;
+    PG_API_END
 }
 
 void prag_gpu_embedder_free(prag_gpu_embedder* e) {
@@ -177,12 +190,14 @@ void prag_gpu_embedder_free(prag_gpu_embedder* e) {
     cudaFree(e->table);
     cudaFree(e->tok);
     cudaFree(e->out);
+    cudaFree(e->extra);
     cudaSetDevice(prev);
     delete e;
 }
 
 int prag_gpu_embed(prag_gpu_embedder* e, const uint32_t* tokens, uint32_t nchunks, uint32_t m, float* out,
                    void* stream) {
+    PG_API_BEGIN
     if (!e || (!tokens && nchunks && m) || (!out && nchunks)) {
         set_error("null argument");
         return PRAG_GPU_CONFIG;
@@ -208,8 +223,43 @@ int prag_gpu_embed(prag_gpu_embedder* e, const uint32_t* tokens, uint32_t nchunk
     }
     uint32_t* bad = e->tok + tok_n;  // error flag after the staged tokens
     const uint32_t* dtok = tokens;
+    uint32_t n_extra = 0;
     if (!tok_dev) {
-        PG_CUDA(cudaMemcpyAsync(e->tok, tokens, tok_n * 4, cudaMemcpyHostToDevice, s));
+        // ChunkEmbedder::embed computes any token's vector on demand
+        // (tokendb.hpp:63-80, :99-103): ids beyond the resident table get
+        // their rows computed here for this call, so no id is out of range
+        // and one request never fails the others embedded with it.
+        std::unordered_map<uint32_t, uint32_t> slot;
+        std::vector<uint32_t> staged;
+        for (size_t i = 0; i < tok_n; ++i) {
+            const uint32_t t = tokens[i];
+            if (t < e->vocab) continue;
+            if (staged.empty()) staged.assign(tokens, tokens + tok_n);
+            auto it = slot.emplace(t, e->vocab + uint32_t(slot.size())).first;
+            staged[i] = it->second;
+        }
+        n_extra = uint32_t(slot.size());
+        if (n_extra) {
+            if (uint64_t(e->vocab) + n_extra > 0xffffffffull) {
+                set_error("embed: too many distinct token ids");
+                return PRAG_GPU_CONFIG;
+            }
+            std::vector<float> rows(size_t(n_extra) * e->d);
+            for (const auto& kv : slot) token_vector(kv.first, e->d, e->seed, rows.data() + size_t(kv.second - e->vocab) * e->d);
+            if (e->extra_cap < rows.size()) {
+                PG_CUDA(cudaStreamSynchronize(s));
+                cudaFree(e->extra);
+                e->extra = nullptr;
+                e->extra_cap = 0;
+                PG_CUDA(cudaMalloc(&e->extra, rows.size() * 4));
+                e->extra_cap = rows.size();
+            }
+            // pageable sources: both copies have consumed their host buffers on return
+            PG_CUDA(cudaMemcpyAsync(e->extra, rows.data(), rows.size() * 4, cudaMemcpyHostToDevice, s));
+            PG_CUDA(cudaMemcpyAsync(e->tok, staged.data(), tok_n * 4, cudaMemcpyHostToDevice, s));
+        } else {
+            PG_CUDA(cudaMemcpyAsync(e->tok, tokens, tok_n * 4, cudaMemcpyHostToDevice, s));
+        }
         dtok = e->tok;
     }
     float* dout = out;
@@ -225,7 +275,8 @@ int prag_gpu_embed(prag_gpu_embedder* e, const uint32_t* tokens, uint32_t nchunk
         dout = e->out;
     }
     PG_CUDA(cudaMemsetAsync(bad, 0, 4, s));
-    embed_kernel<<<nchunks, kEmbThreads, size_t(e->d) * 8, s>>>(e->table, e->vocab, e->d, dtok, m, dout, bad);
+    embed_kernel<<<nchunks, kEmbThreads, size_t(e->d) * 8, s>>>(e->table, e->vocab, e->d, e->extra, n_extra, dtok, m,
+                                                                 dout, bad);
     PG_CUDA(cudaGetLastError());
     if (!out_dev || !tok_dev) {
         uint32_t hbad = 0;
@@ -238,6 +289,7 @@ int prag_gpu_embed(prag_gpu_embedder* e, const uint32_t* tokens, uint32_t nchunk
         }
     }
     return PRAG_GPU_OK;
+    PG_API_END
 }
 
 }  // extern "C"

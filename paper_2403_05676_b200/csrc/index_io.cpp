@@ -70,6 +70,22 @@ int read_pragix01(const std::string& path, HostIndex& out, const std::vector<uin
         return PRAG_GPU_FORMAT;
     }
     out.sub_dim = out.d / out.nsq;
+    // Header fields are untrusted: never allocate more than the file can
+    // hold. A short file fails on the same row (and offset) the row-by-row
+    // read below would report, before any allocation.
+    {
+        const uint64_t row = uint64_t(out.d) * 4, avail = file_size > offset ? file_size - offset : 0;
+        if (row && uint64_t(out.nlist) > avail / row) {
+            set_error("truncated centroids at offset " + std::to_string(offset + (avail / row) * row));
+            return PRAG_GPU_FORMAT;
+        }
+        const uint64_t wrow = uint64_t(out.sub_dim) * 4, after = offset + uint64_t(out.nlist) * row;
+        const uint64_t wavail = file_size > after ? file_size - after : 0;
+        if (wrow && uint64_t(out.nsq) * 256 > wavail / wrow) {
+            set_error("truncated codebook at offset " + std::to_string(after + (wavail / wrow) * wrow));
+            return PRAG_GPU_FORMAT;
+        }
+    }
     out.centroids.resize(size_t(out.nlist) * out.d);
     for (uint32_t c = 0; c < out.nlist; ++c) {
         if (!r.read(out.centroids.data() + size_t(c) * out.d, size_t(out.d) * 4)) {

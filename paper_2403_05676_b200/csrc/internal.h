@@ -4,7 +4,10 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
 #include <mutex>
+#include <new>
+#include <stdexcept>
 #include <string>
 #include <utility>
 #include <vector>
@@ -59,6 +62,29 @@ struct Status {
             return _e == cudaErrorMemoryAllocation ? PRAG_GPU_OOM : PRAG_GPU_CUDA;         \
         }                                                                                  \
     } while (0)
+
+// Every extern "C" int entry point runs inside PG_API_BEGIN / PG_API_END:
+// no C++ exception (a host allocation sized from a corrupt header, a
+// std::vector growth) crosses the C ABI; it becomes a status code instead.
+#define PG_API_BEGIN try {
+#define PG_API_END                                                              \
+    }                                                                           \
+    catch (const std::bad_alloc&) {                                             \
+        ::pg::set_error("out of host memory");                                  \
+        return PRAG_GPU_OOM;                                                    \
+    }                                                                           \
+    catch (const std::length_error& e) {                                        \
+        ::pg::set_error(std::string("allocation too large: ") + e.what());      \
+        return PRAG_GPU_OOM;                                                    \
+    }                                                                           \
+    catch (const std::exception& e) {                                           \
+        ::pg::set_error(std::string("internal error: ") + e.what());            \
+        return PRAG_GPU_CONFIG;                                                 \
+    }                                                                           \
+    catch (...) {                                                               \
+        ::pg::set_error("internal error: unknown exception");                   \
+        return PRAG_GPU_CONFIG;                                                 \
+    }
 
 #define PG_TRY(expr)                      \
     do {                                  \
@@ -125,6 +151,16 @@ struct Workspace {
     // pinned host staging
     void* host = nullptr;
     size_t host_bytes = 0;
+    // the last async H2D out of `host` (pageable queries staged through it):
+    // the next write into `host` waits for it (a later chunk or call must not
+    // overwrite queries a queued copy has not read yet)
+    cudaEvent_t host_ev = nullptr;
+    bool host_pending = false;
+    // list sharding (shard.cu): the per-shard top-k block / gathered blocks,
+    // and two events for cross-stream (cross-device) hand-offs
+    void* xbuf = nullptr;
+    size_t xbuf_bytes = 0;
+    cudaEvent_t xev = nullptr, xev2 = nullptr;
     // profiling events
     cudaEvent_t ev[8] = {};
     unsigned long long* win_stat = nullptr;  // profiling: sum of K1b window sizes
@@ -154,6 +190,20 @@ struct prag_gpu_index {
     uint64_t emb_n = 0;
     std::mutex mu;                                // guards pool and `last`
     std::vector<pg::Workspace*> pool;
+    // prefix sums of the WHOLE index's list sizes sorted desc (== top_prefix
+    // unless this is a shard): pass sizes that every rank agrees on
+    std::vector<uint64_t> global_top_prefix;
+    // --- list sharding (shard.cu)
+    // group handle: a list-sharded index spanning these shards (owned; shard
+    // r holds rank r of world shards.size(), possibly on different devices).
+    // dev holds only the shape (no device arrays); `device` is the root.
+    std::vector<prag_gpu_index*> shards;
+    std::vector<cudaStream_t> shard_streams;      // one per shard, on its device
+    std::vector<uint8_t> peer_direct;             // root's merge reads shard r's memory directly
+    // multi-process: this shard is rank comm->rank of a distributed index;
+    // prag_gpu_search on it is collective (NCCL all-gather + merge)
+    prag_gpu_comm* comm = nullptr;
+    bool is_group() const { return !shards.empty(); }
 };
 
 namespace pg {
@@ -239,8 +289,103 @@ int launch_select_window(const DeviceIndex& ix, float* partial, const float* que
 constexpr uint32_t kTcMaxNprobe = 256;
 // device-built synthetic index (synth_index.cu)
 void synth_list_sizes(uint32_t nlist, uint64_t ntotal, uint64_t seed, double sigma, std::vector<uint64_t>& sizes);
-int launch_synth_codes(uint32_t m, const uint64_t* list_off, const uint64_t* skew_off, uint32_t nlist, uint64_t seed,
-                       uint8_t* out, uint64_t ntiles, uint64_t* ids, const uint64_t* pad_off, uint64_t npadded);
+// gbase[l]: global list-major position of list l's entry 0; rlen[l]: its
+// resident length (0 for lists another shard holds)
+int launch_synth_codes(uint32_t m, const uint64_t* gbase, const uint64_t* rlen, const uint64_t* skew_off, uint32_t nlist,
+                       uint64_t seed, uint8_t* out, uint64_t ntiles, uint64_t* ids, const uint64_t* pad_off,
+                       uint64_t npadded);
 size_t select_smem_bytes();
 
 }  // namespace pg
+
+namespace pg {
+
+// ------------------------------------------------- orchestration (capi.cu)
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+struct Carver {
+    char* base;
+    size_t off = 0;
+    template <typename T>
+    T* take(size_t n) {
+        off = (off + 255) & ~size_t(255);
+        T* p = reinterpret_cast<T*>(base + off);
+        off += std::max<size_t>(n * sizeof(T), 16);
+        return p;
+    }
+};
+
+int sm_count(int device);
+int require_device(int device);
+bool is_device_ptr(const void* p);
+bool is_pinned_host(const void* p);
+uint32_t pow2_at_least(uint64_t v);
+void free_device_index(DeviceIndex& d);
+int upload(prag_gpu_index* ix, const HostIndex& h);
+int finish_load(std::unique_ptr<prag_gpu_index>& ix, HostIndex& h, int device, prag_gpu_index** out);
+Workspace* acquire_ws(prag_gpu_index* ix, cudaStream_t s);
+void release_ws(prag_gpu_index* ix, Workspace* w, cudaStream_t s);
+int ws_reserve(Workspace* w, size_t bytes, cudaStream_t s);
+int ws_reserve_stage(Workspace* w, size_t bytes, cudaStream_t s);
+int ws_reserve_host(Workspace* w, size_t bytes);
+int validate(const prag_gpu_index* ix, uint32_t nprobe, uint32_t k);
+int run_coarse(const prag_gpu_index* ix, const float* dq, uint32_t nq, uint32_t nprobe, float* coarse,
+               uint32_t* probe, float* probe_dist, uint32_t* pkey, uint64_t* ptie, cudaStream_t s,
+               Workspace* prof_ws = nullptr);
+// One pass over nq device-resident queries into device outputs, on stream s.
+int search_pass(prag_gpu_index* ix, Workspace* w, const float* dq, uint32_t nq, uint32_t nprobe, uint32_t k,
+                uint64_t* o_ids, float* o_dist, uint32_t* o_count, uint64_t* o_scanned, cudaStream_t s,
+                prag_gpu_timings* tm, bool rerank);
+// Queries per pass: a pure function of the WHOLE index's list sizes and the
+// shape, so every rank of a distributed index makes the same passes.
+uint32_t pass_chunk(const prag_gpu_index* ix, uint32_t nq, uint32_t nprobe, uint32_t k, bool rerank);
+int do_search(prag_gpu_index* ix, const float* queries, uint32_t nq, uint32_t nprobe, uint32_t k,
+              uint64_t* out_ids, float* out_dist, uint32_t* out_count, uint64_t* out_scanned, cudaStream_t s,
+              bool rerank = false, bool all_device = false);
+bool uses_fast_path(const prag_gpu_index* ix, uint32_t k, bool rerank);
+std::vector<uint64_t> prefix_desc(const std::vector<uint64_t>& sizes);
+int ws_reserve_x(Workspace* w, size_t bytes, cudaStream_t s);
+void free_ws(Workspace* w);
+
+// ------------------------------------------------ list sharding (shard.cu)
+struct GroupPlan;
+// Group handle: every shard's pass on its own device/stream, then the fused
+// peer-memory gather + merge on the root stream s. With `plan` the shard
+// passes replay that plan's captured graphs and dedicated workspaces.
+int group_pass(prag_gpu_index* g, Workspace* wg, const float* dq, uint32_t nq, uint32_t nprobe, uint32_t k,
+               uint64_t* o_ids, float* o_dist, uint32_t* o_count, uint64_t* o_scanned, cudaStream_t s, bool rerank,
+               GroupPlan* plan);
+// Distributed shard (NCCL comm attached): local pass into the rank's top-k
+// block, ncclAllGather of the blocks on s, merge on every rank.
+int dist_pass(prag_gpu_index* ix, Workspace* w, const float* dq, uint32_t nq, uint32_t nprobe, uint32_t k,
+              uint64_t* o_ids, float* o_dist, uint32_t* o_count, uint64_t* o_scanned, cudaStream_t s,
+              prag_gpu_timings* tm, bool rerank);
+int group_plan_create(prag_gpu_index* g, const float* dq, uint32_t nq, uint32_t nprobe, uint32_t k, uint64_t* o_ids,
+                      float* o_dist, uint32_t* o_count, uint64_t* o_scanned, cudaStream_t s, GroupPlan** out);
+int group_plan_launch(prag_gpu_index* g, GroupPlan* p, cudaStream_t s);
+void group_plan_free(prag_gpu_index* g, GroupPlan* p);
+void free_group(prag_gpu_index* g);
+// synthetic index (capi.cu): rank `rank` of `world` (world 1: the whole index)
+int build_synthetic(uint32_t nlist, uint32_t d, uint32_t nsq, uint64_t ntotal, uint64_t seed, double sigma,
+                    const float* centroids, const float* codewords, int rank, int world, int device,
+                    prag_gpu_index** out);
+
+}  // namespace pg
+
+struct prag_gpu_plan {
+    prag_gpu_index* ix = nullptr;
+    pg::Workspace* w = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    pg::GroupPlan* group = nullptr;  // group handle: per-shard graphs + the root merge
+};

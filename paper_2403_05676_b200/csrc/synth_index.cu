@@ -5,6 +5,8 @@
 // because a 1B-entry PRAGIX01 file (~72 GB) and the reference's AoS in-memory
 // index (~115 GB) cannot be staged through host memory here.
 //
+// A shard (prag_gpu_index_synthetic_shard) holds only its lists, each entry
+// at its global position g, so its codes and chunk ids equal the full index's.
 // Given centroids [nlist][d] and codewords [nsq][256][d/nsq] (the caller's,
 // e.g. trained elsewhere), list sizes follow a log-normal skew drawn from
 // SplitMix64 on the host; entry g (global, list-major) has chunk id g and
@@ -37,7 +39,8 @@ __device__ __forceinline__ uint32_t code_byte(uint64_t seed, uint64_t g, uint32_
 // One thread per (tile, lane): the lane's m bytes of the tile in fold-step
 // order (scan_skew.cu build_skew_layout, on the device).
 template <int M>
-__global__ void synth_skew_kernel(const uint64_t* __restrict__ list_off, const uint64_t* __restrict__ skew_off,
+__global__ void synth_skew_kernel(const uint64_t* __restrict__ gbase, const uint64_t* __restrict__ rlen,
+                                  const uint64_t* __restrict__ skew_off,
                                   uint32_t nlist, uint64_t seed, uint8_t* __restrict__ out, uint64_t ntiles) {
     const uint64_t gt = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const uint64_t tile = gt >> 5;
@@ -51,7 +54,7 @@ __global__ void synth_skew_kernel(const uint64_t* __restrict__ list_off, const u
     }
     const uint32_t l = lo;
     const uint64_t j = tile - skew_off[l];
-    const uint64_t base = list_off[l], len = list_off[l + 1] - base;
+    const uint64_t base = gbase[l], len = rlen[l];  // global position of entry 0, resident length
     uint8_t* dst = out + tile * (32ull * M);
 #pragma unroll 4
     for (uint32_t s = 0; s < uint32_t(M); ++s) {
@@ -72,7 +75,8 @@ __global__ void synth_skew_kernel(const uint64_t* __restrict__ list_off, const u
 }
 
 // ids of the padded list-major slots: chunk id g for real entries, ~0 pads
-__global__ void synth_ids_kernel(const uint64_t* __restrict__ list_off, const uint64_t* __restrict__ pad_off,
+__global__ void synth_ids_kernel(const uint64_t* __restrict__ gbase, const uint64_t* __restrict__ rlen,
+                                 const uint64_t* __restrict__ pad_off,
                                  uint32_t nlist, uint64_t* __restrict__ ids, uint64_t npadded) {
     const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= npadded) return;
@@ -82,8 +86,7 @@ __global__ void synth_ids_kernel(const uint64_t* __restrict__ list_off, const ui
         if (pad_off[mid] <= i) lo = mid; else hi = mid;
     }
     const uint64_t e = i - pad_off[lo];
-    const uint64_t len = list_off[lo + 1] - list_off[lo];
-    ids[i] = e < len ? list_off[lo] + e : ~0ull;
+    ids[i] = e < rlen[lo] ? gbase[lo] + e : ~0ull;
 }
 
 }  // namespace
@@ -114,16 +117,17 @@ void synth_list_sizes(uint32_t nlist, uint64_t ntotal, uint64_t seed, double sig
     for (uint64_t i = 0; used < ntotal; ++i, ++used) ++sizes[rem[i % nlist].second];
 }
 
-int launch_synth_codes(uint32_t m, const uint64_t* list_off, const uint64_t* skew_off, uint32_t nlist, uint64_t seed,
-                       uint8_t* out, uint64_t ntiles, uint64_t* ids, const uint64_t* pad_off, uint64_t npadded) {
+int launch_synth_codes(uint32_t m, const uint64_t* gbase, const uint64_t* rlen, const uint64_t* skew_off, uint32_t nlist,
+                       uint64_t seed, uint8_t* out, uint64_t ntiles, uint64_t* ids, const uint64_t* pad_off,
+                       uint64_t npadded) {
     const uint64_t threads = ntiles * 32;
     const uint32_t blocks = uint32_t((threads + 255) / 256);
     if (m == 32)
-        synth_skew_kernel<32><<<blocks, 256>>>(list_off, skew_off, nlist, seed, out, ntiles);
+        synth_skew_kernel<32><<<blocks, 256>>>(gbase, rlen, skew_off, nlist, seed, out, ntiles);
     else
-        synth_skew_kernel<64><<<blocks, 256>>>(list_off, skew_off, nlist, seed, out, ntiles);
+        synth_skew_kernel<64><<<blocks, 256>>>(gbase, rlen, skew_off, nlist, seed, out, ntiles);
     PG_CUDA(cudaGetLastError());
-    synth_ids_kernel<<<uint32_t((npadded + 255) / 256), 256>>>(list_off, pad_off, nlist, ids, npadded);
+    synth_ids_kernel<<<uint32_t((npadded + 255) / 256), 256>>>(gbase, rlen, pad_off, nlist, ids, npadded);
     PG_CUDA(cudaGetLastError());
     PG_CUDA(cudaDeviceSynchronize());
     return PRAG_GPU_OK;

@@ -596,6 +596,7 @@ extern "C" {
 int prag_gpu_train_index(const float* vectors, uint64_t n, uint32_t d, const prag_gpu_train_params* params,
                          int device, float* centroids, float* codewords, uint64_t* list_off, uint64_t* ids,
                          uint8_t* codes) {
+    PG_API_BEGIN
     if (!params || (!vectors && n)) {
         set_error("null argument");
         return PRAG_GPU_CONFIG;
@@ -773,6 +774,7 @@ int prag_gpu_train_index(const float* vectors, uint64_t n, uint32_t d, const pra
     if (!codes_dev) PG_CUDA(cudaMemcpyAsync(codes, codes_out, n * nsq, kind, s));
     PG_CUDA(cudaStreamSynchronize(s));
     return PRAG_GPU_OK;
+    PG_API_END
 }
 
 }  // extern "C"

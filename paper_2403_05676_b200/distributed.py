@@ -9,9 +9,12 @@ top-k of the union of per-shard top-k lists, ordered by (distance, chunk_id)
      bytes) assigns it, plus replicated centroids and codebooks, so every rank
      computes the identical probe set (annindex.hpp:277-281);
   2. each rank searches its shard (K1-K4) -> per-shard top-k;
-  3. one all-gather of a packed [nq, 2k+2] int64 record per rank (ids,
-     distance bits, count, scanned_vectors) over NCCL / NVLink;
-  4. rank 0 runs the exact merge kernel (K5) and holds the batch result.
+  3. one ncclAllGather of each rank's top-k block, issued by libprag_gpu on
+     the search stream (prag_gpu_index_attach_comm; graph-capturable);
+  4. every rank runs the exact merge kernel over the gathered blocks.
+
+ShardedIndex is that path. gather_merge below is the same exchange written
+with torch.distributed, kept for the CPU (gloo) tests of the host logic.
 
 The reference has no multi-GPU path (it is a single-process scalar library);
 this module is the B200 extension the north star asks for. The gather/merge
@@ -79,22 +82,69 @@ def gather_merge(local: BatchResult, k: int, merge: Optional[Callable] = None, g
     return merge(ids, dd, cnt, sc, k)
 
 
-class ShardedIndex:
-    """One rank's shard of a PRAGIX01 index on its own GPU."""
+def exchange_unique_id(group=None, src: int = 0) -> bytes:
+    """The NCCL unique id (prag_gpu_comm_unique_id on rank `src`), broadcast
+    over the torch.distributed group (gloo or nccl): every rank returns the
+    same 128 bytes."""
+    from .ivfpq import Comm
+    obj = [Comm.unique_id() if dist.get_rank(group) == src else None]
+    dist.broadcast_object_list(obj, src=src, group=group)
+    uid = obj[0]
+    if not isinstance(uid, (bytes, bytearray)) or len(uid) != 128:
+        raise RuntimeError("bad NCCL unique id from the broadcast")
+    return bytes(uid)
 
-    def __init__(self, path: str, device: Optional[int] = None, group=None):
+
+def make_comm(device: int, group=None):
+    """prag_gpu_comm of this rank over the group's ranks (collective)."""
+    from .ivfpq import Comm
+    uid = exchange_unique_id(group)
+    return Comm(uid, dist.get_world_size(group), dist.get_rank(group), device)
+
+
+class ShardedIndex:
+    """One rank's shard of a list-sharded index on its own GPU, searched
+    collectively through the C ABI: K1-K4 on the rank's lists, one
+    ncclAllGather of the per-shard top-k blocks issued by libprag_gpu on the
+    search stream, and the exact merge kernel -- every rank gets the merged
+    result (prag_gpu_index_attach_comm)."""
+
+    def __init__(self, index: GpuIndex, device: int, group=None):
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
-        self.device = torch.cuda.current_device() if device is None else device
-        self.index = GpuIndex.load_shard(path, self.rank, self.world, self.device)
-        self.nlist = self.index.nlist
+        self.device = device
+        self.index = index
+        self.comm = make_comm(device, group)
+        index.attach_comm(self.comm)
+        self.nlist = index.nlist
+
+    @classmethod
+    def load(cls, path: str, device: Optional[int] = None, group=None) -> "ShardedIndex":
+        device = torch.cuda.current_device() if device is None else device
+        return cls(GpuIndex.load_shard(path, dist.get_rank(group), dist.get_world_size(group), device), device,
+                   group)
+
+    @classmethod
+    def synthetic(cls, centroids, codewords, ntotal: int, seed: int = 1, sigma: float = 1.0,
+                  device: Optional[int] = None, group=None) -> "ShardedIndex":
+        device = torch.cuda.current_device() if device is None else device
+        ix = GpuIndex.synthetic_shard(centroids, codewords, ntotal, dist.get_rank(group), dist.get_world_size(group),
+                                      seed=seed, sigma=sigma, device=device)
+        return cls(ix, device, group)
 
     def search_batch(self, queries, k: int, nprobe: int, stream=None):
-        """queries: CUDA tensor [nq, d] (identical on every rank). Returns the
-        merged result on rank 0 and None on the other ranks."""
-        local = self.index.search_batch(queries, k, nprobe, stream=stream)
-        return gather_merge(local, k, group=self.group)
+        """queries identical on every rank (collective); the merged result."""
+        return self.index.search_batch(queries, k, nprobe, stream=stream)
+
+    def plan(self, queries, k: int, nprobe: int, out, stream=None):
+        """Captured collective search (graph with the NCCL all-gather)."""
+        return self.index.plan(queries, k, nprobe, out, stream=stream)
+
+    def close(self) -> None:
+        self.index.attach_comm(None)
+        self.index.close()
+        self.comm.close()
 
 
 # ------------------------------------------------------------ shard files

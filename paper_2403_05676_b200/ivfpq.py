@@ -146,6 +146,47 @@ class GpuIndex:
                                              device, C.byref(h)))
         return cls(h)
 
+    @classmethod
+    def synthetic_shard(cls, centroids, codewords, ntotal: int, rank: int, world: int, seed: int = 1,
+                        sigma: float = 1.0, device: int = 0) -> "GpuIndex":
+        """Rank `rank` of `world` of the synthetic index (same entries, ids and
+        codes as GpuIndex.synthetic with the same arguments)."""
+        centroids = np.ascontiguousarray(centroids, dtype=np.float32)
+        codewords = np.ascontiguousarray(codewords, dtype=np.float32)
+        nlist, d = centroids.shape
+        nsq = codewords.shape[0]
+        h = C.c_void_p()
+        check(lib().prag_gpu_index_synthetic_shard(nlist, d, nsq, ntotal, seed, sigma, _ptr(centroids),
+                                                   _ptr(codewords), rank, world, device, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def load_sharded(cls, path: str, devices: Sequence[int]) -> "GpuIndex":
+        """One process, several GPUs: the index's lists spread over `devices`
+        (LPT on bytes; devices may repeat). Searches run every shard on its own
+        device and merge on devices[0] reading the shards over NVLink."""
+        dv = np.ascontiguousarray(devices, dtype=np.int32)
+        h = C.c_void_p()
+        check(lib().prag_gpu_index_load_sharded(str(path).encode(), _ptr(dv), len(dv), C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def group(cls, shards: Sequence["GpuIndex"]) -> "GpuIndex":
+        """Group handle over shard handles (ranks 0..n-1 of world n); takes
+        ownership of them."""
+        arr = (C.c_void_p * len(shards))(*[s._h for s in shards])
+        h = C.c_void_p()
+        check(lib().prag_gpu_index_group(arr, len(shards), C.byref(h)))
+        for s in shards:
+            s._h = None  # owned by the group now
+        return cls(h)
+
+    def attach_comm(self, comm: Optional["Comm"]) -> None:
+        """Makes searches on this shard collective over `comm` (NCCL):
+        every rank passes the same queries and gets the merged result."""
+        check(lib().prag_gpu_index_attach_comm(self._h, comm._h if comm is not None else None))
+        self._comm = comm
+
     def store(self, path: str) -> None:
         """prag::store_index (annindex.hpp:335-359) of the resident index."""
         check(lib().prag_gpu_index_store(self._h, str(path).encode()))
@@ -194,6 +235,7 @@ class GpuIndex:
             q = queries.contiguous()
             if q.dtype != torch.float32:
                 raise ConfigError("queries must be float32")
+            self._check_dev_queries(q)
             nq = q.shape[0] if q.dim() == 2 else 1
             if out is None:
                 out = BatchResult(torch.empty((nq, k), dtype=torch.int64, device=q.device),
@@ -222,11 +264,20 @@ class GpuIndex:
                  _ptr(out.scanned), _stream_ptr(stream)))
         return out
 
+    def _check_dev_queries(self, q) -> None:
+        # the C ABI takes no d: a device tensor of the wrong width would be
+        # read as nq x d floats out of bounds
+        if q.dim() not in (1, 2) or q.shape[-1] != self.d:
+            raise ConfigError(f"queries must be [nq, {self.d}] (or [{self.d}]), got {tuple(q.shape)}")
+
     def plan(self, queries, k: int, nprobe: int, out: BatchResult, stream=None) -> "SearchPlan":
         """A captured search (prag_gpu_plan_create) over fixed CUDA buffers:
         write new queries into `queries`, then SearchPlan.launch()."""
         if not (torch is not None and isinstance(queries, torch.Tensor) and queries.is_cuda):
             raise ConfigError("plan: queries must be a CUDA tensor")
+        if queries.dtype != torch.float32 or not queries.is_contiguous():
+            raise ConfigError("plan: queries must be a contiguous float32 tensor")
+        self._check_dev_queries(queries)
         h = C.c_void_p()
         nq = queries.shape[0] if queries.dim() == 2 else 1
         check(lib().prag_gpu_plan_create(self._h, _ptr(queries), nq, nprobe, k, _ptr(out.ids), _ptr(out.dist),
@@ -257,6 +308,36 @@ class GpuIndex:
         t = Timings()
         check(lib().prag_gpu_last_timings(self._h, C.byref(t)))
         return {f: getattr(t, f) for f, _ in Timings._fields_}
+
+
+class Comm:
+    """NCCL communicator of one rank (prag_gpu_comm_*): the exchange step of
+    a distributed list-sharded index."""
+
+    def __init__(self, unique_id: bytes, world: int, rank: int, device: int):
+        if len(unique_id) != 128:
+            raise ConfigError("unique id must be 128 bytes")
+        buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        h = C.c_void_p()
+        check(lib().prag_gpu_comm_init(buf, world, rank, device, C.byref(h)))
+        self._h, self.world, self.rank, self.device = h, world, rank, device
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        check(lib().prag_gpu_comm_unique_id(buf))
+        return bytes(buf)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib().prag_gpu_comm_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class SearchPlan:

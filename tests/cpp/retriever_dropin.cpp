@@ -56,10 +56,16 @@ bool same_outcome(const RetrievalOutcome& a, const RetrievalOutcome& b) {
     return a.nprobe_used == b.nprobe_used && a.neighbors == b.neighbors;
 }
 
-void dropin_parity(const Fixture& fx, const std::string& tag) {
+// devices: {} = one GPU; several entries = the index list-sharded over them
+// (repeated ordinals put several shards on one GPU)
+void dropin_parity(const Fixture& fx, const std::string& tag, const std::vector<int>& devices = {}) {
     RetrievalPerfModel perf{2e-5, 1e-4, 0.0, false};
     LocalRetriever local(fx.db, fx.index, fx.codebook, 7, perf);
-    gpu::GpuRetriever gpu_r(fx.db, fx.index, fx.codebook, 7, perf);
+    gpu::GpuRetriever gpu_r = devices.empty() ? gpu::GpuRetriever(fx.db, fx.index, fx.codebook, 7, perf)
+                                              : gpu::GpuRetriever(fx.db, fx.index, fx.codebook, 7, perf, 0.10, devices);
+    if (!devices.empty())
+        report(gpu_r.index().describe().shard_world == int(devices.size()),
+               tag + ": the retriever's index spans " + std::to_string(devices.size()) + " shards");
     report(gpu_r.nlist() == local.nlist(), tag + ": nlist()");
     SplitMix64 rng(202);
     int bad = 0, total = 0;
@@ -213,6 +219,13 @@ int main() {
     {
         Fixture fx(60, 384, 32, 32);  // d=384, m=32: lane-skewed fast path
         dropin_parity(fx, "d384/m32");
+        // list-sharded GpuRetriever: 3 shards (each on GPU 0 here; on an
+        // 8-GPU box pass {0, 1, 2, ...}) merged by the peer-memory kernel
+        dropin_parity(fx, "d384/m32 sharded x3", {0, 0, 0});
+    }
+    {
+        Fixture fx(60, 32, 32, 0);
+        dropin_parity(fx, "d32/m8 sharded x2", {0, 0});
     }
     std::printf("%s (%d failures)\n", g_fail ? "FAILED" : "ALL PASS", g_fail);
     return g_fail ? 1 : 0;

@@ -51,9 +51,24 @@ def test_gpu_embed_device_pointers_and_vocab_check(tmp_path):
     dev = emb.embed(torch.from_numpy(tok.view(np.int32)).cuda())
     torch.cuda.synchronize()
     assert (dev.cpu().numpy().view(np.uint32) == host.view(np.uint32)).all()
-    bad = tok.copy()
-    bad[3, 5] = 300
-    with pytest.raises(pg.ConfigError):
-        emb.embed(bad)
     with pytest.raises(pg.ConfigError):
         pg.GpuChunkEmbedder(1, 7)
+
+
+def test_gpu_embed_ids_beyond_vocab(tmp_path):
+    """ChunkEmbedder::embed computes any id's vector on demand
+    (tokendb.hpp:63-80): host token ids past the resident table embed
+    bit-identically to the reference, mixed with in-table ids in one batch."""
+    if not O.ref_available():
+        pytest.skip("oracle/_ref/ref_tool not built")
+    import paper_2403_05676_b200 as pg
+    emb = pg.GpuChunkEmbedder(384, 7, vocab=257)
+    tok = np.random.default_rng(2).integers(0, 257, (6, 32)).astype(np.uint32)
+    tok[1, 5] = 300
+    tok[2, :4] = [70000, 70000, 1 << 20, 258]  # (the reference's cache resize overflows at 2^32-1)
+    tok[4, 31] = 300
+    got = emb.embed(tok)
+    ref = _ref_embed(tmp_path, tok, 384, 7)
+    assert (got.view(np.uint32) == ref.view(np.uint32)).all()
+    again = emb.embed(tok[:1])  # a later in-table call is unaffected
+    assert (again.view(np.uint32) == ref[:1].view(np.uint32)).all()

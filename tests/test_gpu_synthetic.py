@@ -56,4 +56,12 @@ def test_config_d_1b_sampled_parity():
     ix = pg.GpuIndex.synthetic(cents, words, 1_000_000_000, seed=seed, sigma=1.0)
     rng = np.random.default_rng(2)
     q = (cents[rng.integers(0, 16384, 2)] + rng.standard_normal((2, 384)).astype(np.float32) * 0.5).astype(np.float32)
-    _check(ix, cents, words, seed, q, 16, 10)
+    sizes = ix.list_sizes()
+    print(f"\nconfig D: ntotal={ix.ntotal} nlist={ix.nlist} m={ix.nsq} device_bytes={ix.desc.device_bytes} "
+          f"list p50={int(np.median(sizes))} max={int(sizes.max())}")
+    for nprobe, k in [(16, 10), (64, 32)]:
+        _check(ix, cents, words, seed, q, nprobe, k)
+        r = ix.search_batch(q, k, nprobe)
+        for i in range(q.shape[0]):
+            print(f"  nprobe={nprobe} k={k} q{i}: scanned_vectors={int(r.scanned[i])} "
+                  f"ids[:5]={r.ids[i, :5].tolist()} == host restatement (ids, distance bits, scanned)")

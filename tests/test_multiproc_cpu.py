@@ -130,3 +130,36 @@ def test_pack_unpack_roundtrip():
     ids, dd, cnt, sc = D.unpack_results(g, k)
     assert torch.equal(ids[0], r.ids) and torch.equal(cnt[0], r.count) and torch.equal(sc[0], r.scanned)
     assert torch.equal(dd[0].view(torch.int32), r.dist.view(torch.int32))
+
+
+def _uid_worker(rank, world, port, out_dir):
+    import torch.distributed as dist
+
+    import paper_2403_05676_b200 as pg
+    from paper_2403_05676_b200 import distributed as D
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        uid = D.exchange_unique_id()
+        with open(os.path.join(out_dir, f"uid{rank}.bin"), "wb") as f:
+            f.write(uid)
+        # no GPU here: the communicator itself must refuse, not fall back
+        if pg.device_count() == 0:
+            try:
+                pg.Comm(uid, world, rank, 0)
+                raise AssertionError("comm_init without a device must fail")
+            except pg.NoDeviceError:
+                pass
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_nccl_unique_id_rendezvous(tmp_path):
+    """The host side of the distributed shard (ShardedIndex / bench.py
+    --gpus N): rank 0's prag_gpu_comm_unique_id reaches every rank intact
+    over a world-2 gloo group."""
+    import torch.multiprocessing as mp
+    port = _free_port()
+    mp.start_processes(_uid_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True, start_method="spawn")
+    a = open(tmp_path / "uid0.bin", "rb").read()
+    b = open(tmp_path / "uid1.bin", "rb").read()
+    assert len(a) == 128 and a == b and any(a)
