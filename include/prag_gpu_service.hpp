@@ -22,10 +22,15 @@
 
 #include <prag/service.hpp>
 
+#include <poll.h>
+#include <sys/eventfd.h>
+
+#include <cerrno>
 #include <condition_variable>
 #include <deque>
 #include <future>
 #include <map>
+#include <set>
 
 #include "prag_gpu.hpp"
 
@@ -128,9 +133,49 @@ private:
     std::thread worker_;
 };
 
+// Client connections of a GpuRetrievalService: one handler thread per
+// socket. shut() wakes every handler blocked in a read (the socket stays
+// open until its handler closes it); join() waits for all of them.
+class ConnectionRegistry {
+public:
+    template <class Handler>
+    void spawn(int fd, Handler handler) {
+        std::lock_guard<std::mutex> lk(mu_);
+        open_.insert(fd);
+        threads_.emplace_back([this, fd, handler] {
+            handler(fd);
+            {
+                std::lock_guard<std::mutex> g(mu_);
+                open_.erase(fd);
+            }
+            ::close(fd);
+        });
+    }
+    void shut() {
+        std::lock_guard<std::mutex> lk(mu_);
+        for (int fd : open_) ::shutdown(fd, SHUT_RDWR);
+    }
+    void join() {
+        std::vector<std::thread> ts;
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            ts.swap(threads_);
+        }
+        for (auto& t : ts) t.join();
+    }
+
+private:
+    std::mutex mu_;
+    std::set<int> open_;
+    std::vector<std::thread> threads_;
+};
+
 // Drop-in for prag::RetrievalService (service.hpp:243-362): same constructor
-// arguments (plus the CUDA device and the batch cap), same start/port/stop,
-// same frames and error behaviour, GPU batched retrieval behind it.
+// arguments (plus the CUDA device and the batch cap), same start/port/stop
+// contract and bind errors, same frames and error behaviour; GPU batched
+// retrieval behind it. The acceptor polls the listening socket together with
+// an eventfd, so stop() wakes it by writing the eventfd rather than by
+// tearing the listening socket down under a blocked accept().
 class GpuRetrievalService {
 public:
     GpuRetrievalService(const ::prag::Database& db, const ::prag::IvfIndex& index,
@@ -143,9 +188,15 @@ public:
 
     // Listens on address:port (0 = ephemeral); returns the bound port.
     std::uint16_t start(const std::string& address = "127.0.0.1", std::uint16_t port = 0) {
-        listen_fd_ = open_listener(address, port, &port_);
-        running_ = true;
-        acceptor_ = std::thread([this] { accept_connections(); });
+        const Listener l = bind_listener(address, port);
+        wake_fd_ = ::eventfd(0, EFD_CLOEXEC);
+        if (wake_fd_ < 0) {
+            ::close(l.fd);
+            throw ConfigError("service: eventfd() failed");
+        }
+        listen_fd_ = l.fd;
+        port_ = l.port;
+        acceptor_ = std::thread([this] { acceptor_main(); });
         return port_;
     }
 
@@ -153,59 +204,66 @@ public:
     GpuRetriever& retriever() { return gpu_; }
     BatchingRetriever::Stats batch_stats() const { return batcher_.stats(); }
 
+    // Idempotent: wakes and joins the acceptor, then ends every connection.
     void stop() {
-        if (!running_.exchange(false)) return;
-        ::shutdown(listen_fd_, SHUT_RDWR);
+        if (!acceptor_.joinable()) return;
+        const std::uint64_t one = 1;
+        (void)!::write(wake_fd_, &one, sizeof one);
+        acceptor_.join();
         ::close(listen_fd_);
-        {
-            std::lock_guard<std::mutex> lk(conn_mu_);
-            for (int fd : conns_) ::shutdown(fd, SHUT_RDWR);
-        }
-        if (acceptor_.joinable()) acceptor_.join();
-        for (auto& t : workers_)
-            if (t.joinable()) t.join();
-        workers_.clear();
+        ::close(wake_fd_);
+        listen_fd_ = wake_fd_ = -1;
+        conns_.shut();
+        conns_.join();
     }
 
 private:
-    static int open_listener(const std::string& address, std::uint16_t port, std::uint16_t* bound) {
-        sockaddr_in sa{};
-        sa.sin_family = AF_INET;
-        sa.sin_port = htons(port);
-        if (::inet_pton(AF_INET, address.c_str(), &sa.sin_addr) != 1)
+    struct Listener {
+        int fd;
+        std::uint16_t port;
+    };
+
+    // socket/bind/listen with the reference's ConfigError texts
+    // (service.hpp:254-268 behaviour).
+    static Listener bind_listener(const std::string& address, std::uint16_t port) {
+        in_addr ip{};
+        if (::inet_pton(AF_INET, address.c_str(), &ip) != 1)
             throw ConfigError("service: invalid bind address " + address);
-        const int fd = ::socket(AF_INET, SOCK_STREAM, 0);
+        const int fd = ::socket(AF_INET, SOCK_STREAM | SOCK_CLOEXEC, 0);
         if (fd < 0) throw ConfigError("service: socket() failed");
-        const int reuse = 1;
-        ::setsockopt(fd, SOL_SOCKET, SO_REUSEADDR, &reuse, sizeof reuse);
-        if (::bind(fd, reinterpret_cast<const sockaddr*>(&sa), sizeof sa) != 0) {
+        auto fail = [fd](const std::string& what) {
             ::close(fd);
-            throw ConfigError("service: bind failed on " + address + ":" + std::to_string(port));
-        }
-        if (::listen(fd, 64) != 0) {
-            ::close(fd);
-            throw ConfigError("service: listen failed");
-        }
-        socklen_t sl = sizeof sa;
-        ::getsockname(fd, reinterpret_cast<sockaddr*>(&sa), &sl);
-        *bound = ntohs(sa.sin_port);
-        return fd;
+            throw ConfigError(what);
+        };
+        const int on = 1;
+        ::setsockopt(fd, SOL_SOCKET, SO_REUSEADDR, &on, sizeof on);
+        sockaddr_in want{};
+        want.sin_family = AF_INET;
+        want.sin_addr = ip;
+        want.sin_port = htons(port);
+        if (::bind(fd, reinterpret_cast<const sockaddr*>(&want), sizeof want) != 0)
+            fail("service: bind failed on " + address + ":" + std::to_string(port));
+        if (::listen(fd, SOMAXCONN) != 0) fail("service: listen failed");
+        sockaddr_in got{};
+        socklen_t n = sizeof got;
+        ::getsockname(fd, reinterpret_cast<sockaddr*>(&got), &n);
+        return {fd, ntohs(got.sin_port)};
     }
 
-    void accept_connections() {
-        for (;;) {
-            const int fd = running_ ? ::accept(listen_fd_, nullptr, nullptr) : -1;
-            if (fd < 0) return;
-            const int nodelay = 1;
-            ::setsockopt(fd, IPPROTO_TCP, TCP_NODELAY, &nodelay, sizeof nodelay);
-            std::lock_guard<std::mutex> lk(conn_mu_);
-            conns_.insert(fd);
-            workers_.emplace_back([this, fd] {
-                serve(fd);
-                ::close(fd);
-                std::lock_guard<std::mutex> g(conn_mu_);
-                conns_.erase(fd);
-            });
+    void acceptor_main() {
+        pollfd pf[2] = {{listen_fd_, POLLIN, 0}, {wake_fd_, POLLIN, 0}};
+        while (true) {
+            if (::poll(pf, 2, -1) < 0) {
+                if (errno == EINTR) continue;
+                return;
+            }
+            if (pf[1].revents) return;  // stop()
+            if (!(pf[0].revents & POLLIN)) continue;
+            const int fd = ::accept4(listen_fd_, nullptr, nullptr, SOCK_CLOEXEC);
+            if (fd < 0) continue;  // the peer went away before accept
+            const int on = 1;
+            ::setsockopt(fd, IPPROTO_TCP, TCP_NODELAY, &on, sizeof on);
+            conns_.spawn(fd, [this](int c) { serve(c); });
         }
     }
 
@@ -275,13 +333,10 @@ private:
 
     GpuRetriever gpu_;
     BatchingRetriever batcher_;
-    int listen_fd_ = -1;
+    int listen_fd_ = -1, wake_fd_ = -1;
     std::uint16_t port_ = 0;
-    std::atomic<bool> running_{false};
     std::thread acceptor_;
-    std::vector<std::thread> workers_;
-    std::mutex conn_mu_;
-    std::set<int> conns_;
+    ConnectionRegistry conns_;
 };
 
 }  // namespace gpu

@@ -16,7 +16,10 @@ want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "lts__t_bytes.sum", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
         "sm__memory_throughput.avg.pct_of_peak_sustained_elapsed", "launch__occupancy_limit_shared_mem",
         "launch__occupancy_limit_registers", "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
-        "smsp__inst_executed_pipe_lsu.sum", "smsp__inst_executed_op_shared_ld.sum"]
+        "smsp__inst_executed_pipe_lsu.sum", "smsp__inst_executed_op_shared_ld.sum",
+        "dram__bytes_read.sum.per_second", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+        "lts__t_sector_hit_rate.pct", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_uniform.avg.pct_of_peak_sustained_active"]
 out = {}
 for i, name in enumerate(h):
     if name in want:
