@@ -457,25 +457,26 @@ template <int M>
 struct SkewCfg;
 template <>
 struct SkewCfg<32> {
-    // consumer warps; + 1 producer + kExp expander warps, 1 CTA per SM. 12 + 3
-    // measured best (config B K3: 13 + 2 138.6 us, 12 + 3 132.1, 11 + 4 140.1,
-    // 13 + 3 164 -- register spills): with two expanders the consumers waited
-    // on the next item's image ~13% of the time.
+    // consumer warps; + 1 producer + kExp expander warps, 1 CTA per SM
+    // (12 + 3 measured best with the SMEM code ring: 13 + 2 138.6 us, 12 + 3
+    // 132.1, 11 + 4 140.1 at config B)
     static constexpr int kWarps = 12;
     static constexpr int kExp = 3;
-    static constexpr int kDepth = 4;   // cp.async ring slots per consumer warp
-    static constexpr int kBufs = 2;    // SMEM images: item i+1's is built while item i is scanned
+    static constexpr int kPrefetch = 8;  // tiles a warp keeps requested into L2 ahead of its loads
 };
 template <>
 struct SkewCfg<64> {
-    static constexpr int kWarps = 12;  // 11 + 3 measured no better for m = 64 (single-buffered image)
+    // (more than 12 warps put 4 on some SM sub-partition, which caps a
+    // thread at 128 registers: ptxas then rematerialises part of the 64
+    // step-mask registers inside the fold -- still cheaper than spilling)
+    static constexpr int kWarps = 12;
     static constexpr int kExp = 2;
-    static constexpr int kDepth = 2;
-    static constexpr int kBufs = 1;    // 128 KiB image: single-buffered
+    static constexpr int kPrefetch = 4;
 };
 
 constexpr uint32_t kEndItem = 0xffffffffu;
 constexpr uint32_t kMinWarpTiles = 4;  // a warp re-reads one tail tile per range: keep ranges >= 4 tiles
+constexpr uint32_t kHeadTiles = 4;     // first tiles of each warp range the producer requests into L2
 
 struct ItemSlot {
     uint32_t pair, tb, te, len, q;
@@ -485,28 +486,41 @@ struct ItemSlot {
     uint64_t lbase;          // list_off[list]: padded entry slot of the list's entry 0
 };
 
-// SMEM plan of K3 (runtime: it depends on where the dynamic window starts).
-// The LUT images sit at a 64 KiB-aligned shared address, so a gather address
-// is exactly PRMT(code byte -> bits 8..15, lane column -> bits 0..7, image
-// base -> bits 16..31) plus a compile-time offset: LDS [R + imm], no add.
-// The alignment pad in front of the images holds as many of the consumer
-// warps' TMA rings as fit; the staging buffer, the remaining rings, the
-// mbarriers and the item slots follow the images.
+// SMEM plan of K3: two LUT images (item i+1's is built while item i is
+// scanned), the staging buffer the producer bulk-copies compact tables into,
+// then barriers, item slots and the merge stashes. Image 0 starts at a
+// 64 KiB-aligned shared address and image 1 a fixed stride above it, so a
+// gather address is PRMT(code byte -> bits 8..15, lane column -> bits 0..7,
+// image page -> bits 16..31) plus a compile-time offset: one PRMT and one
+// LDS [R + imm] per code byte. The staging buffer and the tail go into the
+// alignment pad below image 0 when they fit there, else above the images.
+//  * m = 32: image [256 codes][64 columns] fp32, column c = T[c mod 32] (the
+//    wrap-around duplicated), lane t at step s reads column 32 + s - t.
+//  * m = 64: image [256][64], column c = T[c] (no duplicate), lane t at step
+//    s reads column (s - t) mod 64. The wrap (s < t: the tail of the previous
+//    entry) is folded into the code byte: the ingest stores those bytes as
+//    (code + 1) mod 256, so row code + 1 minus 4(t - s) bytes lands on column
+//    64 + s - t of row `code`. Code 255 wraps to row 0 and reads just below
+//    the image: a 128-byte guard holding row 255's upper half.
+// Code tiles are not staged in SMEM at all: each lane loads the 16-byte
+// chunks it folds straight into registers, one tile ahead, and lane 0 keeps
+// the warp's next kPrefetch tiles requested into L2 (bulk prefetch).
 template <int M>
 struct SkewSmem {
-    static constexpr int W = SkewCfg<M>::kWarps, D = SkewCfg<M>::kDepth, NB = SkewCfg<M>::kBufs;
-    static constexpr uint32_t kImg = image_floats<M>() * 4;  // R x 64 KiB
-    static constexpr uint32_t kStage = 32768;                // 32 subquantizers of T[sq][256] fp32
-    static constexpr uint32_t kTile = 32u * M;
-    static constexpr uint32_t kRing = uint32_t(D) * kTile;  // per consumer warp
-    // img_full[NB], img_empty[NB], stg_full, stg_empty
-    static constexpr uint32_t nbars = 2 * NB + 2;
+    static constexpr int W = SkewCfg<M>::kWarps, NB = 2;
+    static constexpr uint32_t kGuard = M == 64 ? 128u : 0u;
+    static constexpr uint32_t kImg = 65536;
+    static constexpr uint32_t kImgStride = kGuard + kImg;
+    static constexpr uint32_t kStage = 32768;  // 32 subquantizers of T[sq][256] fp32
+    // img_full[NB], stg_full
+    static constexpr uint32_t nbars = NB + 1;
     // + cta_thr[NB] + merge counters[NB] + per-(buffer, warp) list stash {key[32], pos[32]}
     static constexpr uint32_t kTail = 8 * nbars + (NB + 1) * uint32_t(sizeof(ItemSlot)) + 4 * NB + 4 * NB +
                                       uint32_t(NB) * W * 64 * 4;
-    static constexpr uint32_t bytes = 232448;                // 227 KiB: the opt-in maximum
-    // worst case: a pad just below one ring (nothing fits in it)
-    static constexpr uint32_t worst = (kRing - 16) + NB * kImg + kStage + W * kRing + kTail;
+    static constexpr uint32_t kImgSpan = kImgStride + kImg;  // image 0 start .. image 1 end
+    static constexpr uint32_t bytes = 232448;                 // 227 KiB: the opt-in maximum
+    // worst case: a pad just too small for the staging buffer and the tail
+    static constexpr uint32_t worst = (kGuard + kStage + kTail - 16) + kImgSpan + kStage + kTail;
     static constexpr int threads = (W + 1 + SkewCfg<M>::kExp) * 32;
 };
 
@@ -514,19 +528,11 @@ template <int M>
 constexpr size_t skew_smem_bytes() {
     return SkewSmem<M>::bytes;
 }
-static_assert(SkewSmem<32>::worst <= 232448 && SkewSmem<64>::worst <= 232448, "K3 SMEM exceeds 227 KiB");
+static_assert(SkewSmem<32>::worst <= SkewSmem<32>::bytes && SkewSmem<64>::worst <= SkewSmem<64>::bytes,
+              "K3 SMEM exceeds 227 KiB");
 
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-// LUT gather: 32-bit shared::cta address (uniform base folded by ptxas into
-// LDS [R + UR + imm]) plus a compile-time offset.
+// LUT gather: 32-bit shared::cta address (the PRMT result) plus a
+// compile-time offset.
 template <int IMM>
 __device__ __forceinline__ float lds_lut(uint32_t addr) {
     float v;
@@ -534,24 +540,34 @@ __device__ __forceinline__ float lds_lut(uint32_t addr) {
     return v;
 }
 
-__device__ __forceinline__ uint4 lds_u4(uint32_t addr) {
-    uint4 v;
-    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
-    return v;
-}
-
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// Streaming 16-byte load of code bytes: read once per search, kept out of L1.
+__device__ __forceinline__ uint4 ldg_codes(const unsigned char* p) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
+
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 // One step of the skewed fold: lane's code byte S -> table column, gather,
 // and the masked {cur, prev} update (steps >= 32 always belong to `cur`).
-template <int M, int S>
-__device__ __forceinline__ void skew_step(const uint32_t* w, uint32_t bt, float& cur, float& prev, const float* mk,
+template <int M, int BUF, int S>
+__device__ __forceinline__ void skew_step(const uint4* v, uint32_t bt, float& cur, float& prev, const float* mk,
                                           const float* nk) {
-    constexpr int r = S >> 5;
-    const uint32_t addr = __byte_perm(w[S >> 2], bt, 0x7604u | (uint32_t(S & 3) << 4));
-    const float t = lds_lut<r * 65536 + (S - 32 * r) * 4>(addr);
+    constexpr int IMM = (M == 32 ? 4 * (S + 1) : 4 * (S - 31)) + BUF * int(SkewSmem<M>::kImgStride);
+    const uint4 c = v[S >> 4];
+    const uint32_t w = ((S >> 2) & 3) == 0 ? c.x : ((S >> 2) & 3) == 1 ? c.y : ((S >> 2) & 3) == 2 ? c.z : c.w;
+    // bytes: 0 = lane column (bt byte 0), 1 = code byte S & 3, 2-3 = image page (bt bytes 2-3)
+    const uint32_t addr = __byte_perm(w, bt, 0x7604u | (uint32_t(S & 3) << 4));
+    const float t = lds_lut<IMM>(addr);
     if constexpr (S < 32) {
         fma2_bcast(cur, prev, t, mk[S], nk[S]);
     } else {
@@ -559,10 +575,10 @@ __device__ __forceinline__ void skew_step(const uint32_t* w, uint32_t bt, float&
     }
 }
 
-template <int M, int... S>
-__device__ __forceinline__ void skew_round(const uint32_t* w, uint32_t bt, float& cur, float& prev, const float* mk,
+template <int M, int BUF, int... S>
+__device__ __forceinline__ void skew_round(const uint4* v, uint32_t bt, float& cur, float& prev, const float* mk,
                                            const float* nk, std::integer_sequence<int, S...>) {
-    (skew_step<M, S>(w, bt, cur, prev, mk, nk), ...);
+    (skew_step<M, BUF, S>(v, bt, cur, prev, mk, nk), ...);
 }
 
 __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
@@ -571,13 +587,9 @@ __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
     return v;
 }
 
-// One consumer warp's share [a, e_end] of an item: stream the tiles through
-// the warp's TMA ring, fold them against the SMEM image at byte offset IMG
-// (compile-time, so the gather is LDS [R + UR + imm]), keep the warp top-k and
-// publish it to the query's candidate pool.
 struct ScanCtx {
     uint32_t* cta_thr;  // this item's CTA-wide threshold (SMEM)
-    uint32_t ring_s, lane, bt, k;  // bt: column offset | image page (see SkewSmem)
+    uint32_t lane, bt, k;  // bt: lane column byte | image 0 page
     const uint8_t* skew_codes;
     const uint64_t* ids;
     uint32_t* gthr;
@@ -597,12 +609,10 @@ struct WarpTopK {
     uint32_t key, pos, thr, g;
 };
 
-__device__ __forceinline__ void topk_offer(WarpTopK& t, uint32_t key, bool valid, uint32_t mypos, uint32_t lane,
-                                           uint32_t k, const uint64_t* __restrict__ ids, uint32_t* gthr_q,
-                                           uint32_t* cta_thr) {
-    const bool pass = valid && key <= min(t.thr, t.g);
+// Inserts the lanes' candidates that pass (rare after the first tiles).
+__device__ __forceinline__ void topk_insert(WarpTopK& t, uint32_t key, bool pass, uint32_t mypos, uint32_t lane,
+                                            uint32_t k, const uint64_t* __restrict__ ids) {
     unsigned bal = __ballot_sync(0xffffffffu, pass);
-    if (!bal) return;
     while (bal) {
         const int src = __ffs(bal) - 1;
         bal &= bal - 1;
@@ -630,6 +640,19 @@ __device__ __forceinline__ void topk_offer(WarpTopK& t, uint32_t key, bool valid
             t.thr = __shfl_sync(0xffffffffu, t.key, k - 1);
         }
     }
+}
+
+// Offers the completed entries of two consecutive tiles at once: one
+// threshold refresh and one vote per pair of tiles.
+__device__ __forceinline__ void topk_offer2(WarpTopK& t, uint32_t ka, bool va, uint32_t pa, uint32_t kb, bool vb,
+                                            uint32_t pb, uint32_t lane, uint32_t k, const uint64_t* __restrict__ ids,
+                                            uint32_t* gthr_q, uint32_t* cta_thr) {
+    t.g = min(t.g, *reinterpret_cast<volatile uint32_t*>(cta_thr));  // other warps of this item
+    const uint32_t lim = min(t.thr, t.g);
+    const bool passa = va && ka <= lim, passb = vb && kb <= lim;
+    if (!__any_sync(0xffffffffu, passa || passb)) return;
+    topk_insert(t, ka, passa, pa, lane, k, ids);
+    topk_insert(t, kb, passb && kb <= t.thr, pb, lane, k, ids);
     if (t.thr < t.g) {
         if (lane == 0) {
             atomicMin(gthr_q, t.thr);
@@ -637,30 +660,6 @@ __device__ __forceinline__ void topk_offer(WarpTopK& t, uint32_t key, bool valid
         }
         t.g = t.thr;
     }
-}
-
-// The next item a warp will scan (buffer b^1), known once its image is
-// published; lets the tail of one range prefetch the head of the next.
-struct NextRange {
-    const ItemSlot* slot;  // slots[b^1]
-    uint64_t* full;        // img_full[b^1]
-    uint32_t phase;        // parity of that item's img_full phase
-    uint32_t warp;
-    bool enabled;          // double-buffered images only
-};
-
-__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t phase) {
-    uint32_t done;
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-        "selp.u32 %0, 1, 0, p;\n"
-        "}\n"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(phase)
-        : "memory");
-    return done != 0;
 }
 
 // This warp's tile range [a, e_end) of an item (empty when a >= e_end).
@@ -683,100 +682,72 @@ __device__ __forceinline__ uint32_t warp_count(const ItemSlot& sl) {
 }
 
 template <int M>
-__device__ __forceinline__ bool scan_range(const ScanCtx& cx, const ItemSlot& sl, uint32_t a, uint32_t e_end,
-                                           uint32_t& consumed, const float* mk, const float* nk,
-                                           bool prefetched, const NextRange& nx) {
-    constexpr int W = SkewCfg<M>::kWarps, D = SkewCfg<M>::kDepth;
-    constexpr int kChunks = M / 16;
+__device__ __forceinline__ void load_tile(uint4 (&v)[M / 16], const unsigned char* src_lane, uint32_t j) {
+#pragma unroll
+    for (int c = 0; c < M / 16; ++c) v[c] = ldg_codes(src_lane + size_t(j) * (32u * M) + c * 512);
+}
+
+
+// One consumer warp's share [a, e_end] of an item: tiles a..e_end inclusive
+// (tile e_end holds the tails of the range's last entries) are loaded into
+// registers one tile ahead (A, B alternate) and folded against the SMEM
+// image; lane 0 keeps the next kPrefetch tiles requested into L2 (the
+// producer requested each range's first tiles when it fetched the item).
+// Completed entries of each pair of tiles are
+// offered to the warp's exact top-k, which is finally merged with the item's
+// other warps and published to the query's candidate pool.
+// BUF: the image buffer (compile-time: its offset from image 0 is part of
+// every gather's immediate).
+template <int M, int BUF>
+__device__ __forceinline__ void scan_range(const ScanCtx& cx, const ItemSlot& sl, uint32_t a, uint32_t e_end,
+                                           const float* mk, const float* nk) {
+    constexpr int W = SkewCfg<M>::kWarps, P = SkewCfg<M>::kPrefetch;
     constexpr uint32_t kTileBytes = 32u * M;
-    const uint32_t lane = cx.lane, bt = cx.bt, k = cx.k, ring_s = cx.ring_s;
+    const uint32_t lane = cx.lane, bt = cx.bt, k = cx.k;
     const uint64_t* __restrict__ ids = cx.ids;
-    uint32_t* gthr = cx.gthr;
-    const uint8_t* skew_codes = cx.skew_codes;
-    uint32_t* pool_key = cx.pool_key;
-    uint64_t* pool_id = cx.pool_id;
-    const uint32_t q = sl.q;
-    const unsigned char* tiles = skew_codes + sl.tile_byte_off;
-    // this warp streams tiles a..e_end inclusive (tile e_end holds the tails
-    // of the range's last entries) through a D-deep ring. Each lane copies
-    // exactly the 16-byte chunks it will read itself (cp.async, one commit
-    // group per tile), so a lane only ever waits on its own copies: no
-    // barrier, no cross-lane synchronisation.
-    // the query's shared threshold (other CTAs' k-th distances), read once per
-    // range (an in-loop refresh would put a global load on every tile) and
-    // issued before the ring prologue so its latency overlaps the copies; the
-    // producer's snapshot from item fetch time bounds it meanwhile
-    WarpTopK t{0xffffffffu, 0xffffffffu, 0xffffffffu, min(sl.thr, ld_relaxed(gthr + q))};
+    uint32_t* gthr_q = cx.gthr + sl.q;
+    const unsigned char* tiles = cx.skew_codes + sl.tile_byte_off;
     const unsigned char* src_lane = tiles + lane * 16;
-    const uint32_t dst_lane = ring_s + lane * 16;
-    if (!prefetched) {
-#pragma unroll
-        for (uint32_t t = 0; t < uint32_t(D); ++t) {
-            if (a + t <= e_end) {
-                const uint32_t slot = (consumed + t) % D;
-#pragma unroll
-                for (int c = 0; c < kChunks; ++c)
-                    cp_async16(dst_lane + slot * kTileBytes + c * 512, src_lane + size_t(a + t) * kTileBytes + c * 512);
-            }
-            cp_async_commit();
-        }
-    }
-    // cross-range prefetch: once the last D tiles of this range are in
-    // flight, the freed ring slots take the first tiles of this warp's range
-    // in the next item (if that item is already published), so the next range
-    // starts without a memory round trip. Only for ranges of >= D tiles, so
-    // the prefetch covers exactly the next range's first D ring slots.
-    bool nx_tried = !nx.enabled || e_end - a + 1 < uint32_t(D);
-    bool nx_ok = false;
-    uint32_t nx_a = 0, nx_e = 0;
-    const unsigned char* nx_src = nullptr;
+    // the query's shared threshold (other CTAs' k-th distances), read once
+    // per range; the producer's snapshot from item fetch time bounds it too
+    WarpTopK t{0xffffffffu, 0xffffffffu, 0xffffffffu, min(sl.thr, ld_relaxed(gthr_q))};
+    uint4 A[M / 16], B[M / 16];
+    load_tile<M>(A, src_lane, a);
+    load_tile<M>(B, src_lane, a + 1);  // ranges have >= 2 tiles
+    // L2 window: tiles [a + 2, pf) requested so far (the producer requested
+    // [a, a + kHeadTiles) at item fetch)
+    uint32_t pf = min(a + uint32_t(kHeadTiles), e_end + 1);
+    const uint32_t lbase = uint32_t(sl.lbase), len = sl.len;
     float cur = 0.0f, prev = 0.0f;
-    for (uint32_t j = a; j <= e_end; ++j, ++consumed) {
-        const uint32_t slot = consumed % D;
-        cp_async_wait<D - 1>();  // this lane's chunks of tile j have landed
-        uint32_t wd[M / 4];
-#pragma unroll
-        for (int c = 0; c < kChunks; ++c) {
-            const uint4 v = lds_u4(dst_lane + slot * kTileBytes + c * 512);
-            wd[4 * c] = v.x;
-            wd[4 * c + 1] = v.y;
-            wd[4 * c + 2] = v.z;
-            wd[4 * c + 3] = v.w;
-        }
-        skew_round<M>(wd, bt, cur, prev, mk, nk, std::make_integer_sequence<int, M>{});
-        // the fold consumed every byte of the slot: refill it with tile j + D
-        // of this range, or with the next range's head
-        if (j + D <= e_end) {
-#pragma unroll
-            for (int c = 0; c < kChunks; ++c)
-                cp_async16(dst_lane + slot * kTileBytes + c * 512, src_lane + size_t(j + D) * kTileBytes + c * 512);
-        } else {
-            if (!nx_tried) {
-                nx_tried = true;
-                if (mbar_test(nx.full, nx.phase)) {
-                    const ItemSlot ns = *nx.slot;
-                    if (ns.pair != kEndItem) {
-                        warp_range<W>(ns, nx.warp, nx_a, nx_e);
-                        nx_ok = nx_a < nx_e;
-                        nx_src = skew_codes + ns.tile_byte_off + lane * 16;
-                    }
-                }
-            }
-            const uint32_t t = j + D - e_end - 1;  // next range's tile index this slot will hold
-            if (nx_ok && nx_a + t <= nx_e) {
-#pragma unroll
-                for (int c = 0; c < kChunks; ++c)
-                    cp_async16(dst_lane + slot * kTileBytes + c * 512, nx_src + size_t(nx_a + t) * kTileBytes + c * 512);
-            }
-        }
-        cp_async_commit();
-        t.g = min(t.g, *reinterpret_cast<volatile uint32_t*>(cx.cta_thr));  // other warps of this item
-        // entry 32(j-1)+lane is complete in `prev`
-        const uint32_t e = (j - 1) * kTileEntries + lane;
-        const uint32_t key = __float_as_uint(prev);
+    for (uint32_t j = a;; j += 2) {
+        // ---- tile j (registers A)
+        skew_round<M, BUF>(A, bt, cur, prev, mk, nk, std::make_integer_sequence<int, M>{});
+        if (j + 2 <= e_end) load_tile<M>(A, src_lane, j + 2);
+        const uint32_t ea = (j - 1) * kTileEntries + lane;  // entry completed in `prev`
+        const uint32_t ka = __float_as_uint(prev);
+        const bool va = j > a && ea < len;
         prev = cur;
         cur = 0.0f;
-        topk_offer(t, key, j > a && e < sl.len, uint32_t(sl.lbase) + e, lane, k, ids, gthr + q, cx.cta_thr);
+        if (j + 1 > e_end) {
+            topk_offer2(t, ka, va, lbase + ea, 0xffffffffu, false, 0u, lane, k, ids, gthr_q, cx.cta_thr);
+            break;
+        }
+        // ---- tile j + 1 (registers B)
+        skew_round<M, BUF>(B, bt, cur, prev, mk, nk, std::make_integer_sequence<int, M>{});
+        if (j + 3 <= e_end) load_tile<M>(B, src_lane, j + 3);
+        const uint32_t eb = j * kTileEntries + lane;
+        const uint32_t kb = __float_as_uint(prev);
+        const bool vb = eb < len;
+        prev = cur;
+        cur = 0.0f;
+        // slide the L2 window two tiles (kPrefetch ahead of the loads)
+        if (pf <= e_end && pf < j + 4 + uint32_t(P)) {
+            const uint32_t pe = min(pf + 2, e_end + 1);
+            if (lane == 0) prefetch_l2(tiles + size_t(pf) * kTileBytes, (pe - pf) * kTileBytes);
+            pf = pe;
+        }
+        topk_offer2(t, ka, va, lbase + ea, kb, vb, lbase + eb, lane, k, ids, gthr_q, cx.cta_thr);
+        if (j + 2 > e_end) break;
     }
     // Stash this warp's list; the item's last warp merges the stashed lists
     // into the CTA's exact top-k of the item and publishes only that (k
@@ -790,7 +761,7 @@ __device__ __forceinline__ bool scan_range(const ScanCtx& cx, const ItemSlot& sl
         arrived = atomicAdd(cx.mcount, 1u);
     }
     arrived = __shfl_sync(0xffffffffu, arrived, 0);
-    if (arrived + 1 < cx.nact) return nx_ok;
+    if (arrived + 1 < cx.nact) return;
     __threadfence_block();
     if (lane == 0) *cx.mcount = 0;  // the buffer's next item starts from zero
     // k rounds of "smallest (key, id) among the list heads" (lane w < nact
@@ -828,34 +799,34 @@ __device__ __forceinline__ bool scan_range(const ScanCtx& cx, const ItemSlot& sl
     }
     if (cnt == k) {
         const uint32_t kth = __shfl_sync(0xffffffffu, rk, k - 1);
-        if (lane == 0) atomicMin(gthr + q, kth);
+        if (lane == 0) atomicMin(gthr_q, kth);
     }
     // the item's fixed pool slot: k entries, unfilled ones as +inf sentinels
     if (lane < k) {
         const size_t o = size_t(sl.pslot) * k + lane;
-        pool_key[o] = lane < cnt ? ord_key(__uint_as_float(rk)) : 0xffffffffu;
-        pool_id[o] = lane < cnt ? ids[rp] : ~0ull;
+        cx.pool_key[o] = lane < cnt ? ord_key(__uint_as_float(rk)) : 0xffffffffu;
+        cx.pool_id[o] = lane < cnt ? ids[rp] : ~0ull;
     }
-    return nx_ok;
 }
 
 // Persistent, one CTA per SM, warp-specialised:
 //  * producer warp (one lane): pulls work items {pair, tile_begin,
-//    tile_end} (largest first), resolves the list's metadata and TMA-copies
-//    the pair's compact table T[m][256] into a staging buffer;
-//  * kExpWarps expander warps: transpose the staged table into the
-//    conflict-free image (4x4 register transposes walked diagonally, so every
-//    LDS.128 / STS.128 is conflict-free) in one of kBufs image buffers --
-//    item i+1's image is built while item i is scanned;
-//  * kWarps consumer warps: each scans a contiguous tile range of the item,
-//    its code tiles streamed through a per-warp ring of kDepth TMA bulk
-//    copies (one elected lane, one mbarrier per slot), keeps an exact top-k
-//    (k <= 32) in registers by (distance, chunk_id), prunes with a per-query
-//    threshold shared through global memory (atomicMin on the k-th distance),
-//    and publishes its list into the query's candidate pool.
-// Stages hand off through full/empty mbarrier pairs; no CTA-wide barrier
-// after setup. Candidates are held as (distance bits, entry slot); chunk ids
-// are loaded only on an exact distance tie and when a list is published.
+//    tile_end} (largest first), resolves the list's metadata and bulk-copies
+//    the pair's compact table T[m][256] into the staging buffer (32
+//    subquantizers per round);
+//  * kExp expander warps: transpose the staged table into the conflict-free
+//    image (4x4 register transposes walked diagonally, so every LDS.128 /
+//    STS.128 is conflict-free) in one of two image buffers -- item i+1's
+//    image is built while item i is scanned;
+//  * kWarps consumer warps: each scans a contiguous tile range of the item
+//    (scan_range), keeps an exact top-k (k <= 32) in registers by (distance,
+//    chunk_id), prunes with a per-query threshold shared through global
+//    memory (atomicMin on the k-th distance), and the item's last warp merges
+//    the warps' lists into the item's pool slot.
+// "Data ready" hand-offs are mbarriers; "slot free" hand-offs are named
+// barriers (a waiting warp is descheduled, arriving warps do not wait).
+// Candidates are held as (distance bits, entry slot); chunk ids are loaded
+// only on an exact distance tie and when a list is published.
 template <int M>
 __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
     scan_skew_kernel(const uint4* __restrict__ items, const uint32_t* __restrict__ num_items,
@@ -868,28 +839,21 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
     using L = SkewSmem<M>;
     constexpr int W = L::W, NB = L::NB;
     constexpr int kExpWarps = SkewCfg<M>::kExp;
-    constexpr uint32_t kImgBytes = L::kImg;
     constexpr uint32_t kStageBytes = L::kStage;
     constexpr uint32_t kHalves = M / 32;  // staging rounds per item (32 subquantizers each)
     extern __shared__ __align__(1024) unsigned char smem[];
     const uint32_t base = smem_u32(smem);
-    const uint32_t pad = ((base + 0xffffu) & ~0xffffu) - base;  // images start 64 KiB-aligned
-    const uint32_t img_off = pad;
-    const uint32_t stage_off = img_off + NB * kImgBytes;
-    const uint32_t rings_in_pad = min(uint32_t(W), pad / L::kRing);
-    const uint32_t after_off = stage_off + kStageBytes;  // rings not in the pad, then the tail
-    // the tail goes into what the rings leave of the pad when it fits there
-    const uint32_t pad_tail = (rings_in_pad * L::kRing + 15u) & ~15u;
-    const uint32_t tail_off = pad_tail + L::kTail <= pad ? pad_tail : after_off + (W - rings_in_pad) * L::kRing;
-    if (tail_off + L::kTail > L::bytes || after_off + (W - rings_in_pad) * L::kRing > L::bytes) __trap();
+    const uint32_t img_off = ((base + L::kGuard + 0xffffu) & ~0xffffu) - base;  // image 0, 64 KiB-aligned
+    const bool in_pad = img_off >= L::kGuard + L::kStage + L::kTail;
+    const uint32_t stage_off = in_pad ? 0u : img_off + L::kImgSpan;
+    const uint32_t tail_off = stage_off + L::kStage;
+    if ((in_pad ? img_off + L::kImgSpan : tail_off + L::kTail) > L::bytes) __trap();
     float* stage = reinterpret_cast<float*>(smem + stage_off);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + tail_off);
     uint64_t* img_full = bars;
-    uint64_t* img_empty = bars + NB;
-    uint64_t* stg_full = bars + 2 * NB;
-    uint64_t* stg_empty = bars + 2 * NB + 1;
+    uint64_t* stg_full = bars + NB;
     ItemSlot* slots = reinterpret_cast<ItemSlot*>(smem + tail_off + 8 * L::nbars);  // [NB] image slots
-    ItemSlot* stg_slot = slots + NB;                                                 // staging slot
+    ItemSlot* stg_slot = slots + NB;                                                  // staging slot
     uint32_t* cta_thr = reinterpret_cast<uint32_t*>(stg_slot + 1);  // [NB]: the CTA's k-th distance per item
     uint32_t* mcount = cta_thr + NB;                                  // [NB]: merge arrivals per item
     uint32_t* mstash = mcount + NB;                                   // [NB][W][64]: warp lists of an item
@@ -898,23 +862,18 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
     if (threadIdx.x == 0) {
         for (int i = 0; i < NB; ++i) {
             mbar_init(img_full + i, kExpWarps);
-            mbar_init(img_empty + i, W);
+            mcount[i] = 0;
         }
         mbar_init(stg_full, 1);
-        mbar_init(stg_empty, kExpWarps);
-        for (int i = 0; i < NB; ++i) mcount[i] = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     pdl_wait();  // items, LUTs and thresholds come from the previous kernels
     const uint32_t total = *num_items;
 
-    // hand-offs in the "slot is free" direction are named barriers: a waiting
-    // warp is descheduled until the last arrival (no polling), and arriving
-    // warps do not wait. Barrier 1 + b: consumers arrive when done with image
-    // buffer b, expanders sync before overwriting it; barrier 1 + NB:
-    // expanders arrive when done with the staging buffer, the producer syncs
-    // before refilling it. The "data is ready" direction stays on mbarriers.
+    // Barrier 1 + b: consumers arrive when done with image buffer b,
+    // expanders sync before overwriting it. Barrier 1 + NB: expanders arrive
+    // when done with the staging buffer, the producer syncs before refilling.
     constexpr uint32_t kImgEmptyCount = uint32_t(W + kExpWarps) * 32;
     constexpr uint32_t kStgEmptyCount = uint32_t(kExpWarps + 1) * 32;
     constexpr uint32_t kStgBar = 1 + NB;
@@ -934,7 +893,7 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
                 sl.te = w4.z;
                 sl.len = list_len[list];
                 sl.q = w4.x / nprobe;
-                sl.tile_byte_off = skew_off[list] * L::kTile;
+                sl.tile_byte_off = skew_off[list] * (32u * M);
                 sl.lbase = list_off[list];
                 sl.thr = ld_relaxed(gthr + sl.q);
                 sl.pslot = w4.w;
@@ -949,6 +908,17 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
                     mbar_arrive(stg_full);
                 }
                 break;
+            }
+            {  // request the head of every consumer warp's range into L2 now, an
+               // item or two before the consumers reach it
+                ItemSlot r{};
+                r.tb = __shfl_sync(0xffffffffu, sl.tb, 0);
+                r.te = __shfl_sync(0xffffffffu, sl.te, 0);
+                const uint64_t tbo = __shfl_sync(0xffffffffu, sl.tile_byte_off, 0);
+                uint32_t wa, we;
+                warp_range<W>(r, lane, wa, we);
+                if (lane < uint32_t(W) && wa < we)
+                    prefetch_l2(skew_codes + tbo + size_t(wa) * (32u * M), min(we - wa + 1, kHeadTiles) * (32u * M));
             }
             const unsigned char* src = reinterpret_cast<const unsigned char*>(luts) + size_t(pair) * M * 1024;
             for (uint32_t h = 0; h < kHalves; ++h, ++round) {
@@ -968,7 +938,7 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
         const uint32_t ew = warp - W - 1;
         uint32_t round = 0;
         for (uint32_t i = 0;; ++i) {
-            const uint32_t b = NB == 1 ? 0u : i % NB;
+            const uint32_t b = i % NB;
             mbar_wait(stg_full, round & 1u);
             const ItemSlot sl = *stg_slot;
             if (i >= uint32_t(NB)) named_sync(1 + b, kImgEmptyCount);  // consumers done with item i - NB
@@ -983,40 +953,37 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
                 }
                 break;
             }
-            float* img = reinterpret_cast<float*>(smem + img_off + b * kImgBytes);
+            float* img = reinterpret_cast<float*>(smem + img_off + b * L::kImgStride);
             for (uint32_t h = 0; h < kHalves; ++h, ++round) {
                 if (h > 0) mbar_wait(stg_full, round & 1u);
                 // 4x4 register transposes: lane L owns codes cb + 4L .. +3 and
                 // walks the 8 groups of 4 subquantizers diagonally (group
                 // (g + L) mod 8), so every LDS.128 (4 codes of one staged row)
-                // and STS.128 (4 columns of one image row) is conflict-free
+                // and STS.128 (4 columns of one image row) is conflict-free;
                 // units (code block of 128, subquantizer group step): 2 x 8,
                 // dealt round-robin to the expander warps
 #pragma unroll 2
                 for (uint32_t u = ew; u < 16; u += kExpWarps) {
                     const uint32_t c4 = (u >> 3) * 128 + 4 * lane;
-                    {
-                        const uint32_t g = u & 7u;
-                        const uint32_t sq0 = 4 * ((g + lane) & 7u);  // local subquantizer group
-                        float4 v[4];
+                    const uint32_t g = u & 7u;
+                    const uint32_t sq0 = 4 * ((g + lane) & 7u);  // local subquantizer group
+                    float4 v[4];
 #pragma unroll
-                        for (int r = 0; r < 4; ++r)
-                            v[r] = *reinterpret_cast<const float4*>(stage + (sq0 + r) * 256 + c4);
-                        const float4 col[4] = {make_float4(v[0].x, v[1].x, v[2].x, v[3].x),
-                                               make_float4(v[0].y, v[1].y, v[2].y, v[3].y),
-                                               make_float4(v[0].z, v[1].z, v[2].z, v[3].z),
-                                               make_float4(v[0].w, v[1].w, v[2].w, v[3].w)};
-                        const uint32_t sq = 32 * h + sq0;
+                    for (int r = 0; r < 4; ++r) v[r] = *reinterpret_cast<const float4*>(stage + (sq0 + r) * 256 + c4);
+                    const float4 col[4] = {make_float4(v[0].x, v[1].x, v[2].x, v[3].x),
+                                           make_float4(v[0].y, v[1].y, v[2].y, v[3].y),
+                                           make_float4(v[0].z, v[1].z, v[2].z, v[3].z),
+                                           make_float4(v[0].w, v[1].w, v[2].w, v[3].w)};
+                    const uint32_t sq = 32 * h + sq0;
 #pragma unroll
-                        for (int i = 0; i < 4; ++i) {
-                            float* row = img + (c4 + i) * 64;
-                            if (M == 32) {  // image 0, column c = T[c mod 32]: columns sq and sq + 32
-                                *reinterpret_cast<float4*>(row + sq) = col[i];
-                                *reinterpret_cast<float4*>(row + sq + 32) = col[i];
-                            } else {        // image 0 at (sq + 32) mod 64, image 1 at sq
-                                *reinterpret_cast<float4*>(row + ((sq + 32) & (M - 1))) = col[i];
-                                *reinterpret_cast<float4*>(row + 16384 + sq) = col[i];
-                            }
+                    for (int i = 0; i < 4; ++i) {
+                        float* row = img + (c4 + i) * 64;
+                        if (M == 32) {  // column c = T[c mod 32]: columns sq and sq + 32
+                            *reinterpret_cast<float4*>(row + sq) = col[i];
+                            *reinterpret_cast<float4*>(row + sq + 32) = col[i];
+                        } else {        // column c = T[c]; row 255's upper half also in the guard
+                            *reinterpret_cast<float4*>(row + sq) = col[i];
+                            if (c4 + i == 255 && h == 1) *reinterpret_cast<float4*>(img - 64 + sq) = col[i];
                         }
                     }
                 }
@@ -1035,11 +1002,9 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
     }
 
     // -------------------------------------------------------- consumers
-    // lane's column offset (bytes) in byte 0, the image's 64 KiB page in bytes 2-3
-    const uint32_t bt0 = (32u - lane) * 4u | ((base + img_off) & 0xffff0000u);
-    unsigned char* wring = smem + (warp < rings_in_pad ? warp * L::kRing : after_off + (warp - rings_in_pad) * L::kRing);
-    const uint32_t ring_s = smem_u32(wring);
-    uint32_t consumed = 0;  // tiles this warp has taken from its ring (slot/parity bookkeeping)
+    // lane's column byte 4 (31 - lane) (the step's column offset is in the
+    // gather's immediate) and image 0's 64 KiB page in bytes 2-3
+    const uint32_t bt = (31u - lane) * 4u | ((base + img_off) & 0xffff0000u);
     // step masks: {1, 0} where step s >= lane (the starting entry), {0, 1}
     // before (the finishing entry); one FFMA2 updates {cur, prev}.
     float mk[32], nk[32];
@@ -1049,23 +1014,21 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
         nk[s] = (uint32_t(s) >= lane) ? 0.0f : 1.0f;
     }
 
-    bool pref = false;  // the first ring slots of this item's range are already in flight
     for (uint32_t i = 0;; ++i) {
-        const uint32_t b = NB == 1 ? 0u : i % NB;
-        mbar_wait(img_full + b, (NB == 1 ? i : i / NB) & 1u);
+        const uint32_t b = i % NB;
+        mbar_wait(img_full + b, (i / NB) & 1u);
         const ItemSlot sl = slots[b];
         if (sl.pair == kEndItem) break;
         uint32_t a, e_end;
         warp_range<W>(sl, warp, a, e_end);
         if (a < e_end) {
             uint32_t* mb = mstash + b * (W * 64);
-            const ScanCtx cx{cta_thr + b, ring_s, lane, bt0 + b * (kImgBytes & 0xffff0000u), k, skew_codes, ids, gthr,
-                             pool_key, pool_id, mb + warp * 64, mb, mcount + b, warp_count<W>(sl)};
-            const uint32_t bn = NB == 1 ? 0u : (i + 1) % NB;
-            const NextRange nx{slots + bn, img_full + bn, (NB == 1 ? i + 1 : (i + 1) / NB) & 1u, warp, NB > 1};
-            pref = scan_range<M>(cx, sl, a, e_end, consumed, mk, nk, pref, nx);
-        } else {
-            pref = false;
+            const ScanCtx cx{cta_thr + b, lane, bt, k, skew_codes, ids, gthr, pool_key, pool_id, mb + warp * 64,
+                             mb, mcount + b, warp_count<W>(sl)};
+            if (b == 0)
+                scan_range<M, 0>(cx, sl, a, e_end, mk, nk);
+            else
+                scan_range<M, 1>(cx, sl, a, e_end, mk, nk);
         }
         __syncwarp();
         named_arrive(1 + b, kImgEmptyCount);  // image buffer b is free
@@ -1077,11 +1040,9 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
 uint32_t skew_item_tiles(uint64_t est_tiles, uint32_t grid) {
     // enough items for ~per_cta per CTA, within [kMinItemTiles, kMaxItemTiles]
     // (PRAG_GPU_ITEMS_PER_CTA overrides the default of 1, best in tools/sweep_items.sh; tuning knob)
-    static const uint64_t per_cta = [] {
-        const char* e = getenv("PRAG_GPU_ITEMS_PER_CTA");
-        const long v = e ? atol(e) : 0;
-        return uint64_t(v > 0 ? v : 1);
-    }();
+    const char* e = getenv("PRAG_GPU_ITEMS_PER_CTA");
+    const long v = e ? atol(e) : 0;
+    const uint64_t per_cta = uint64_t(v > 0 ? v : 1);
     uint64_t want = est_tiles / (uint64_t(grid) * per_cta + 1);
     uint32_t it = kMinItemTiles;
     while (it < kMaxItemTiles && uint64_t(it) * 2 <= want) it *= 2;
@@ -1207,8 +1168,10 @@ void build_skew_layout(const HostIndex& h, uint32_t m, std::vector<uint64_t>& sk
                         byte = s - t + m;
                         ok = ok && e < len;
                     }
-                    // lane t's byte s lives in 16-byte chunk s/16 at chunk*512 + t*16 + s%16
-                    tile[(s / 16) * 512 + t * 16 + (s % 16)] = ok ? codes[e * m + byte] : 0;
+                    // lane t's byte s lives in 16-byte chunk s/16 at chunk*512 + t*16 + s%16;
+                    // m = 64 stores a tail byte (s < t) as code + 1 (see SkewSmem)
+                    const uint8_t c = ok ? codes[e * m + byte] : 0;
+                    tile[(s / 16) * 512 + t * 16 + (s % 16)] = (m == 64 && s < t) ? uint8_t(c + 1) : c;
                 }
             }
         }

@@ -70,7 +70,9 @@ __global__ void synth_skew_kernel(const uint64_t* __restrict__ gbase, const uint
             byte = s - t + M;
             ok = j >= 1 && e < len;
         }
-        dst[(s / 16) * 512 + t * 16 + (s % 16)] = ok ? uint8_t(code_byte(seed, base + e, byte)) : uint8_t(0);
+        const uint8_t c = ok ? uint8_t(code_byte(seed, base + e, byte)) : uint8_t(0);
+        // m = 64: a tail byte (s < t) is stored as code + 1 (scan_skew.cu SkewSmem)
+        dst[(s / 16) * 512 + t * 16 + (s % 16)] = (M == 64 && s < t) ? uint8_t(c + 1) : c;
     }
 }
 

@@ -23,15 +23,18 @@ ap.add_argument("--nq", type=int, default=64)
 ap.add_argument("--k", type=int, default=10)
 ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--generic", action="store_true")
+ap.add_argument("--seed", type=int, default=1)
 a = ap.parse_args()
 if a.small:
     a.n, a.nlist = 1_000_000, 1024
-path, q, meta = F.ensure_fixture(a.n, 384, a.nlist, a.m, 1, nq=64, log=lambda *x: print(*x, file=sys.stderr))
+path, q, meta = F.ensure_fixture(a.n, 384, a.nlist, a.m, a.seed, nq=64, log=lambda *x: print(*x, file=sys.stderr))
 ix = pg.GpuIndex.load(path, 0)
 if a.generic:
     ix.set_scan_path(1)
 qd = torch.from_numpy(q[:a.nq]).cuda()
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 for _ in range(a.iters):
+    flush.zero_()  # L2 flushed before each search, as in the timed runs
     r = ix.search_batch(qd, a.k, a.nprobe)
 torch.cuda.synchronize()
 print("done", meta)
