@@ -462,7 +462,7 @@ struct SkewCfg<32> {
     // 132.1, 11 + 4 140.1 at config B)
     static constexpr int kWarps = 12;
     static constexpr int kExp = 3;
-    static constexpr int kPrefetch = 8;  // tiles a warp keeps requested into L2 ahead of its loads
+    static constexpr int kPrefetch = 2;  // tiles a warp keeps requested into L2 ahead of its loads (2-16 measured within 2%)
 };
 template <>
 struct SkewCfg<64> {
@@ -471,7 +471,7 @@ struct SkewCfg<64> {
     // step-mask registers inside the fold -- still cheaper than spilling)
     static constexpr int kWarps = 12;
     static constexpr int kExp = 2;
-    static constexpr int kPrefetch = 4;
+    static constexpr int kPrefetch = 2;
 };
 
 constexpr uint32_t kEndItem = 0xffffffffu;
@@ -700,8 +700,7 @@ __device__ __forceinline__ void load_tile(uint4 (&v)[M / 16], const unsigned cha
 // every gather's immediate).
 template <int M, int BUF>
 __device__ __forceinline__ void scan_range(const ScanCtx& cx, const ItemSlot& sl, uint32_t a, uint32_t e_end,
-                                           const float* mk, const float* nk) {
-    constexpr int W = SkewCfg<M>::kWarps, P = SkewCfg<M>::kPrefetch;
+                                           const float* mk, const float* nk, uint32_t P) {
     constexpr uint32_t kTileBytes = 32u * M;
     const uint32_t lane = cx.lane, bt = cx.bt, k = cx.k;
     const uint64_t* __restrict__ ids = cx.ids;
@@ -716,7 +715,7 @@ __device__ __forceinline__ void scan_range(const ScanCtx& cx, const ItemSlot& sl
     load_tile<M>(B, src_lane, a + 1);  // ranges have >= 2 tiles
     // L2 window: tiles [a + 2, pf) requested so far (the producer requested
     // [a, a + kHeadTiles) at item fetch)
-    uint32_t pf = min(a + uint32_t(kHeadTiles), e_end + 1);
+    uint32_t pf = P ? min(a + uint32_t(kHeadTiles), e_end + 1) : e_end + 1;
     const uint32_t lbase = uint32_t(sl.lbase), len = sl.len;
     float cur = 0.0f, prev = 0.0f;
     for (uint32_t j = a;; j += 2) {
@@ -741,7 +740,7 @@ __device__ __forceinline__ void scan_range(const ScanCtx& cx, const ItemSlot& sl
         prev = cur;
         cur = 0.0f;
         // slide the L2 window two tiles (kPrefetch ahead of the loads)
-        if (pf <= e_end && pf < j + 4 + uint32_t(P)) {
+        if (pf <= e_end && pf < j + 4 + P) {
             const uint32_t pe = min(pf + 2, e_end + 1);
             if (lane == 0) prefetch_l2(tiles + size_t(pf) * kTileBytes, (pe - pf) * kTileBytes);
             pf = pe;
@@ -835,7 +834,7 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
                      const uint8_t* __restrict__ skew_codes, const uint64_t* __restrict__ list_off,
                      const uint64_t* __restrict__ ids, const float* __restrict__ luts, uint32_t nprobe,
                      uint32_t k, uint32_t* __restrict__ gthr, uint32_t* __restrict__ pool_key,
-                     uint64_t* __restrict__ pool_id) {
+                     uint64_t* __restrict__ pool_id, uint32_t l2_prefetch) {
     using L = SkewSmem<M>;
     constexpr int W = L::W, NB = L::NB;
     constexpr int kExpWarps = SkewCfg<M>::kExp;
@@ -917,7 +916,7 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
                 const uint64_t tbo = __shfl_sync(0xffffffffu, sl.tile_byte_off, 0);
                 uint32_t wa, we;
                 warp_range<W>(r, lane, wa, we);
-                if (lane < uint32_t(W) && wa < we)
+                if (l2_prefetch && lane < uint32_t(W) && wa < we)
                     prefetch_l2(skew_codes + tbo + size_t(wa) * (32u * M), min(we - wa + 1, kHeadTiles) * (32u * M));
             }
             const unsigned char* src = reinterpret_cast<const unsigned char*>(luts) + size_t(pair) * M * 1024;
@@ -1026,9 +1025,9 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
             const ScanCtx cx{cta_thr + b, lane, bt, k, skew_codes, ids, gthr, pool_key, pool_id, mb + warp * 64,
                              mb, mcount + b, warp_count<W>(sl)};
             if (b == 0)
-                scan_range<M, 0>(cx, sl, a, e_end, mk, nk);
+                scan_range<M, 0>(cx, sl, a, e_end, mk, nk, l2_prefetch);
             else
-                scan_range<M, 1>(cx, sl, a, e_end, mk, nk);
+                scan_range<M, 1>(cx, sl, a, e_end, mk, nk, l2_prefetch);
         }
         __syncwarp();
         named_arrive(1 + b, kImgEmptyCount);  // image buffer b is free
@@ -1117,18 +1116,21 @@ int launch_lut_images(const DeviceIndex& ix, const float* queries, const uint32_
 int launch_scan_skew(const DeviceIndex& ix, const uint4* items, const uint32_t* num_items, uint32_t* cursor,
                      const uint32_t* probe, const float* luts, uint32_t nprobe, uint32_t k, uint32_t* gthr,
                      uint32_t* pool_key, uint64_t* pool_id, int grid, cudaStream_t s) {
+    // L2 prefetch distance in tiles (0: off); PRAG_GPU_L2_PREFETCH overrides (tuning knob)
+    const char* pe = getenv("PRAG_GPU_L2_PREFETCH");
+    const uint32_t l2pf = pe ? uint32_t(atoi(pe)) : uint32_t(ix.nsq == 32 ? SkewCfg<32>::kPrefetch : SkewCfg<64>::kPrefetch);
     if (ix.nsq == 32) {
         const size_t smem = skew_smem_bytes<32>();
         PG_CUDA(ensure_smem(reinterpret_cast<const void*>(scan_skew_kernel<32>), int(smem)));
         PG_CUDA(launch_pdl(scan_skew_kernel<32>, dim3(grid), dim3(SkewSmem<32>::threads), smem, s, items, num_items,
                            cursor, probe, ix.list_len, ix.skew_off, ix.skew_codes, ix.list_off, ix.ids, luts, nprobe, k,
-                           gthr, pool_key, pool_id));
+                           gthr, pool_key, pool_id, l2pf));
     } else {
         const size_t smem = skew_smem_bytes<64>();
         PG_CUDA(ensure_smem(reinterpret_cast<const void*>(scan_skew_kernel<64>), int(smem)));
         PG_CUDA(launch_pdl(scan_skew_kernel<64>, dim3(grid), dim3(SkewSmem<64>::threads), smem, s, items, num_items,
                            cursor, probe, ix.list_len, ix.skew_off, ix.skew_codes, ix.list_off, ix.ids, luts, nprobe, k,
-                           gthr, pool_key, pool_id));
+                           gthr, pool_key, pool_id, l2pf));
     }
     return check("scan_skew");
 }

@@ -13,6 +13,7 @@ ap.add_argument("--seed", type=int, default=3)
 ap.add_argument("--rows", default="1:64,1:128,8:64,64:16")
 ap.add_argument("--per", default="1,2,4,8")
 ap.add_argument("--reps", type=int, default=7)
+ap.add_argument("--env", default="PRAG_GPU_ITEMS_PER_CTA")
 a = ap.parse_args()
 path, q, meta = F.ensure_fixture(a.n, 384, a.nlist, a.m, a.seed, nq=64, log=lambda *x: None)
 ix = pg.GpuIndex.load(path, 0)
@@ -23,7 +24,7 @@ for spec in a.rows.split(","):
     nq, nprobe = (int(x) for x in spec.split(":"))
     qd = torch.from_numpy(q[:nq]).cuda()
     for per in a.per.split(","):
-        os.environ["PRAG_GPU_ITEMS_PER_CTA"] = per
+        os.environ[a.env] = per
         for _ in range(2):
             ix.search_batch(qd, 10, nprobe, stream=s)
         ix.set_profiling(True)
@@ -38,6 +39,7 @@ for spec in a.rows.split(","):
         ix.set_profiling(False)
         scan = statistics.median(t["scan_ms"] for t in ts)
         balg = statistics.median(t["scanned_bytes"] for t in ts)
-        print(json.dumps({"nq": nq, "nprobe": nprobe, "per_cta": int(per), "scan_ms": round(scan, 4),
+        print(json.dumps({"nq": nq, "nprobe": nprobe, a.env: int(per), "scan_ms": round(scan, 4),
                           "work_items": statistics.median(t["work_items"] for t in ts),
                           "alg_frac": round(balg / (scan / 1e3) / 1e9 / hbm, 3)}), flush=True)
+    os.environ.pop(a.env, None)

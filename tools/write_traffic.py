@@ -23,7 +23,12 @@ def to_bytes(name):
     return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit[name], 1)
 
 
-out = {"workload": "ivfpq search: 10M x 384 fp32 DB, nlist=4096, PQ m=32x8b, nq=64, nprobe=16, k=10",
+import hashlib
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+k3 = hashlib.sha1(open(os.path.join(REPO, "paper_2403_05676_b200", "csrc", "scan_skew.cu"), "rb").read()).hexdigest()
+out = {"workload": sys.argv[2] if len(sys.argv) > 2 else
+       "config B: ivfpq search, 10M x 384 fp32 DB, nlist=4096, PQ m=32x8b, nq=64, nprobe=16, k=10",
+       "k3_source_sha1": k3,
        "kernel": row["Kernel Name"][:80],
        "dram_bytes_read_per_launch": int(to_bytes("dram__bytes_read.sum")),
        "dram_bytes_write_per_launch": int(to_bytes("dram__bytes_write.sum")),
