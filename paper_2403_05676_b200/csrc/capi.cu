@@ -249,6 +249,9 @@ Workspace* acquire_ws(prag_gpu_index* ix, cudaStream_t s) {
     cudaEventCreateWithFlags(&w->xev, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&w->xev2, cudaEventDisableTiming);
     for (auto& e : w->ev) cudaEventCreate(&e);
+    if (cudaMalloc(&w->sync, 64) == cudaSuccess) cudaMemset(w->sync, 0, 64);
+    else w->sync = nullptr;
+    cudaGetLastError();
     w->busy = true;
     ix->pool.push_back(w);
     return w;
@@ -298,6 +301,7 @@ void free_ws(Workspace* w) {
     cudaFree(w->stage);
     cudaFree(w->xbuf);
     cudaFree(w->win_stat);
+    cudaFree(w->sync);
     if (w->host) cudaFreeHost(w->host);
     if (w->done) cudaEventDestroy(w->done);
     if (w->host_ev) cudaEventDestroy(w->host_ev);
@@ -395,6 +399,24 @@ int search_pass_skew(prag_gpu_index* ix, Workspace* w, const float* dq, uint32_t
     const DeviceIndex& d = ix->dev;
     const int sms = sm_count(ix->device);
     const int grid = sms;  // persistent: one CTA per SM
+    if (w->sync && search1_eligible(d, nq, nprobe, k, sms)) {
+        // one query: the whole search in one launch (batch1.cu)
+        PG_TRY(ws_reserve(w, search1_scratch_bytes(d, nprobe, grid), s));
+        if (tm) cudaEventRecord(w->ev[0], s);
+        PG_TRY(launch_search1(d, dq, nprobe, k, o_ids, o_dist, o_count, o_scanned, w->buf, w->sync, grid, s));
+        if (tm) {
+            cudaEventRecord(w->ev[5], s);
+            PG_CUDA(cudaEventSynchronize(w->ev[5]));
+            float tot;
+            cudaEventElapsedTime(&tot, w->ev[0], w->ev[5]);
+            tm->scan_ms += tot;  // one kernel: coarse, tables, scan and merge
+            tm->total_ms += tot;
+            uint64_t sc = 0;
+            PG_CUDA(cudaMemcpy(&sc, o_scanned, 8, cudaMemcpyDeviceToHost));
+            tm->scanned_bytes += sc * d.nsq;
+        }
+        return PRAG_GPU_OK;
+    }
     // item size from the worst-case tile count of this shape (host-side, so a
     // given (nq, nprobe) always plans the same way)
     const uint64_t max_tiles_q = (ix->top_prefix[nprobe] + 31) / 32 + nprobe;

@@ -161,6 +161,8 @@ struct Workspace {
     void* xbuf = nullptr;
     size_t xbuf_bytes = 0;
     cudaEvent_t xev = nullptr, xev2 = nullptr;
+    // batch-1 kernel (batch1.cu): grid-barrier and finish-ticket counters
+    unsigned* sync = nullptr;
     // profiling events
     cudaEvent_t ev[8] = {};
     unsigned long long* win_stat = nullptr;  // profiling: sum of K1b window sizes
@@ -326,6 +328,12 @@ struct Carver {
 };
 
 int sm_count(int device);
+// batch-1 single-launch search (batch1.cu)
+bool search1_eligible(const DeviceIndex& d, uint32_t nq, uint32_t nprobe, uint32_t k, int sms);
+size_t search1_scratch_bytes(const DeviceIndex& d, uint32_t nprobe, int grid);
+int launch_search1(const DeviceIndex& d, const float* dq, uint32_t nprobe, uint32_t k, uint64_t* o_ids,
+                   float* o_dist, uint32_t* o_count, uint64_t* o_scanned, void* scratch, unsigned* sync, int grid,
+                   cudaStream_t s);
 int require_device(int device);
 bool is_device_ptr(const void* p);
 bool is_pinned_host(const void* p);

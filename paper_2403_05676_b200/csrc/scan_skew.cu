@@ -30,76 +30,14 @@
 #include <utility>
 
 #include "internal.h"
+#include "skew_common.cuh"
 
 namespace pg {
 namespace {
 
-constexpr uint32_t kTileEntries = 32;
+using namespace skew;
 constexpr uint32_t kMaxItemTiles = 512;  // tiles per scan work item (16384 entries) at most
 constexpr uint32_t kMinItemTiles = 32;   // and at least (small batches: more, smaller items)
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-
-// Blocking wait: try_wait with a suspend-time hint, so a waiting warp is
-// descheduled until the phase completes instead of spinning on issue slots.
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "LAB_WAIT:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
-        "@!p bra LAB_WAIT;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(phase), "r"(0x989680u)
-        : "memory");
-}
-
-
-__device__ __forceinline__ void named_sync(uint32_t id, uint32_t count) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
-__device__ __forceinline__ void named_arrive(uint32_t id, uint32_t count) {
-    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-
-// {c0, c1} = {a*b0 + c0, a*b1 + c1}: two independent IEEE fp32 FMAs (rn) in
-// one FFMA2 with a scalar-broadcast first operand.
-__device__ __forceinline__ void fma2_bcast(float& c0, float& c1, float a, float b0, float b1) {
-    unsigned long long r;
-    asm("{.reg .b64 A, B, C;\n"
-        " mov.b64 A, {%1, %1};\n"
-        " mov.b64 B, {%2, %3};\n"
-        " mov.b64 C, {%4, %5};\n"
-        " fma.rn.f32x2 %0, A, B, C;}"
-        : "=l"(r)
-        : "f"(a), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
-    c0 = __uint_as_float(uint32_t(r));
-    c1 = __uint_as_float(uint32_t(r >> 32));
-}
-
-__device__ __forceinline__ uint32_t ord_key(float f) {
-    uint32_t u = __float_as_uint(f);
-    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-}
 
 // ----------------------------------------------------------- LUT images
 // {(r0 - w)^2, (r1 - w)^2}: one FADD2 then one FMUL2, each lane a single
@@ -531,62 +469,6 @@ constexpr size_t skew_smem_bytes() {
 static_assert(SkewSmem<32>::worst <= SkewSmem<32>::bytes && SkewSmem<64>::worst <= SkewSmem<64>::bytes,
               "K3 SMEM exceeds 227 KiB");
 
-// LUT gather: 32-bit shared::cta address (the PRMT result) plus a
-// compile-time offset.
-template <int IMM>
-__device__ __forceinline__ float lds_lut(uint32_t addr) {
-    float v;
-    asm("ld.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(addr), "n"(IMM));
-    return v;
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-// Streaming 16-byte load of code bytes: read once per search, kept out of L1.
-__device__ __forceinline__ uint4 ldg_codes(const unsigned char* p) {
-    uint4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                 : "l"(p));
-    return v;
-}
-
-__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
-
-// One step of the skewed fold: lane's code byte S -> table column, gather,
-// and the masked {cur, prev} update (steps >= 32 always belong to `cur`).
-template <int M, int BUF, int S>
-__device__ __forceinline__ void skew_step(const uint4* v, uint32_t bt, float& cur, float& prev, const float* mk,
-                                          const float* nk) {
-    constexpr int IMM = (M == 32 ? 4 * (S + 1) : 4 * (S - 31)) + BUF * int(SkewSmem<M>::kImgStride);
-    const uint4 c = v[S >> 4];
-    const uint32_t w = ((S >> 2) & 3) == 0 ? c.x : ((S >> 2) & 3) == 1 ? c.y : ((S >> 2) & 3) == 2 ? c.z : c.w;
-    // bytes: 0 = lane column (bt byte 0), 1 = code byte S & 3, 2-3 = image page (bt bytes 2-3)
-    const uint32_t addr = __byte_perm(w, bt, 0x7604u | (uint32_t(S & 3) << 4));
-    const float t = lds_lut<IMM>(addr);
-    if constexpr (S < 32) {
-        fma2_bcast(cur, prev, t, mk[S], nk[S]);
-    } else {
-        cur = __fadd_rn(cur, t);
-    }
-}
-
-template <int M, int BUF, int... S>
-__device__ __forceinline__ void skew_round(const uint4* v, uint32_t bt, float& cur, float& prev, const float* mk,
-                                           const float* nk, std::integer_sequence<int, S...>) {
-    (skew_step<M, BUF, S>(v, bt, cur, prev, mk, nk), ...);
-}
-
-__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
-    uint32_t v;
-    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
-    return v;
-}
-
 struct ScanCtx {
     uint32_t* cta_thr;  // this item's CTA-wide threshold (SMEM)
     uint32_t lane, bt, k;  // bt: lane column byte | image 0 page
@@ -600,47 +482,6 @@ struct ScanCtx {
     uint32_t* mcount;  // warps of the item done so far
     uint32_t nact;     // warps with a non-empty range in the item
 };
-
-// Exact warp top-k (k <= 32): lane i holds the i-th (distance bits, entry
-// slot) by (distance, chunk_id) (annindex.hpp:55-58); `thr` is the k-th key
-// (0xffffffff until the list is full) and `g` the warp's view of the query's
-// shared threshold. Chunk ids are read only on an exact distance tie.
-struct WarpTopK {
-    uint32_t key, pos, thr, g;
-};
-
-// Inserts the lanes' candidates that pass (rare after the first tiles).
-__device__ __forceinline__ void topk_insert(WarpTopK& t, uint32_t key, bool pass, uint32_t mypos, uint32_t lane,
-                                            uint32_t k, const uint64_t* __restrict__ ids) {
-    unsigned bal = __ballot_sync(0xffffffffu, pass);
-    while (bal) {
-        const int src = __ffs(bal) - 1;
-        bal &= bal - 1;
-        const uint32_t ck = __shfl_sync(0xffffffffu, key, src);
-        const uint32_t cp = __shfl_sync(0xffffffffu, mypos, src);
-        if (ck > t.thr) continue;  // threshold tightened by an earlier insertion
-        bool gt = t.key > ck;      // lanes whose element sorts after the candidate
-        if (__any_sync(0xffffffffu, t.key == ck)) {  // exact distance tie: compare ids
-            const uint64_t cid = ids[cp];
-            const uint64_t mid = t.key == ck ? ids[t.pos] : 0ull;
-            gt = gt || (t.key == ck && mid > cid);
-        }
-        const unsigned gm = __ballot_sync(0xffffffffu, gt);
-        const int pos = gm ? __ffs(gm) - 1 : 32;
-        if (pos < int(k)) {
-            const uint32_t uk = __shfl_up_sync(0xffffffffu, t.key, 1);
-            const uint32_t up = __shfl_up_sync(0xffffffffu, t.pos, 1);
-            if (int(lane) > pos) {
-                t.key = uk;
-                t.pos = up;
-            } else if (int(lane) == pos) {
-                t.key = ck;
-                t.pos = cp;
-            }
-            t.thr = __shfl_sync(0xffffffffu, t.key, k - 1);
-        }
-    }
-}
 
 // Offers the completed entries of two consecutive tiles at once: one
 // threshold refresh and one vote per pair of tiles.
@@ -681,13 +522,6 @@ __device__ __forceinline__ uint32_t warp_count(const ItemSlot& sl) {
     return min(nw, (ntile + per - 1) / per);
 }
 
-template <int M>
-__device__ __forceinline__ void load_tile(uint4 (&v)[M / 16], const unsigned char* src_lane, uint32_t j) {
-#pragma unroll
-    for (int c = 0; c < M / 16; ++c) v[c] = ldg_codes(src_lane + size_t(j) * (32u * M) + c * 512);
-}
-
-
 // One consumer warp's share [a, e_end] of an item: tiles a..e_end inclusive
 // (tile e_end holds the tails of the range's last entries) are loaded into
 // registers one tile ahead (A, B alternate) and folded against the SMEM
@@ -720,7 +554,7 @@ __device__ __forceinline__ void scan_range(const ScanCtx& cx, const ItemSlot& sl
     float cur = 0.0f, prev = 0.0f;
     for (uint32_t j = a;; j += 2) {
         // ---- tile j (registers A)
-        skew_round<M, BUF>(A, bt, cur, prev, mk, nk, std::make_integer_sequence<int, M>{});
+        skew_round<M, BUF * int(SkewSmem<M>::kImgStride)>(A, bt, cur, prev, mk, nk, std::make_integer_sequence<int, M>{});
         if (j + 2 <= e_end) load_tile<M>(A, src_lane, j + 2);
         const uint32_t ea = (j - 1) * kTileEntries + lane;  // entry completed in `prev`
         const uint32_t ka = __float_as_uint(prev);
@@ -732,7 +566,7 @@ __device__ __forceinline__ void scan_range(const ScanCtx& cx, const ItemSlot& sl
             break;
         }
         // ---- tile j + 1 (registers B)
-        skew_round<M, BUF>(B, bt, cur, prev, mk, nk, std::make_integer_sequence<int, M>{});
+        skew_round<M, BUF * int(SkewSmem<M>::kImgStride)>(B, bt, cur, prev, mk, nk, std::make_integer_sequence<int, M>{});
         if (j + 3 <= e_end) load_tile<M>(B, src_lane, j + 3);
         const uint32_t eb = j * kTileEntries + lane;
         const uint32_t kb = __float_as_uint(prev);
