@@ -318,6 +318,10 @@ uint32_t prag_gpu_select_nprobe(const prag_gpu_perf_model* model, double budget_
 /* Scan-path selection: 0 = automatic (lane-skewed fused fast path for
  * m = 32 / 64 and k <= 32, generic otherwise), 1 = always the generic path
  * (used by the parity suite to check both paths against each other). */
+/* SM budget of the persistent search kernels (the list scan's grid, the
+ * batch-1 kernel): searches size their grids to min(sms, device SMs) so
+ * they run beside work pinned to the other SMs (config E). 0 = every SM. */
+int prag_gpu_set_sm_budget(prag_gpu_index* index, int sms);
 int prag_gpu_set_scan_path(prag_gpu_index* index, int path);
 /* Coarse-quantizer selection: 0 = automatic (tcgen05 tensor-core pre-filter
  * + exact rescoring of the boundary window when nlist % 128 == 0,
@@ -354,6 +358,10 @@ int prag_gpu_embed(prag_gpu_embedder* embedder, const uint32_t* tokens, uint32_t
  * in position. Not part of the retrieval path. y must hold rows + 1 floats. */
 int prag_gpu_synthetic_decode(const float* weights, uint64_t rows, uint32_t cols, const float* x, float* y,
                               const float* kv, uint64_t kv_floats, void* stream);
+/* The same decode step on exactly `sms` SMs (one 1024-thread CTA per SM),
+ * leaving the other SMs free for retrieval on a side stream (config E). */
+int prag_gpu_synthetic_decode_sms(const float* weights, uint64_t rows, uint32_t cols, const float* x, float* y,
+                                  const float* kv, uint64_t kv_floats, uint32_t sms, void* stream);
 
 #ifdef __cplusplus
 }

@@ -108,10 +108,12 @@ SYMBOLS = [
      [MEASURE_FN, P, P, C.c_uint32, C.c_int, C.c_int, C.POINTER(PerfModelC)]),
     ("prag_gpu_select_nprobe", C.c_uint32, [C.POINTER(PerfModelC), C.c_double, C.c_uint32, C.c_double]),
     ("prag_gpu_set_scan_path", C.c_int, [P, C.c_int]),
+    ("prag_gpu_set_sm_budget", C.c_int, [P, C.c_int]),
     ("prag_gpu_set_coarse_path", C.c_int, [P, C.c_int]),
     ("prag_gpu_set_profiling", C.c_int, [P, C.c_int]),
     ("prag_gpu_last_timings", C.c_int, [P, C.POINTER(Timings)]),
     ("prag_gpu_synthetic_decode", C.c_int, [P, C.c_uint64, C.c_uint32, P, P, P, C.c_uint64, P]),
+    ("prag_gpu_synthetic_decode_sms", C.c_int, [P, C.c_uint64, C.c_uint32, P, P, P, C.c_uint64, C.c_uint32, P]),
     ("prag_gpu_embedder_create", C.c_int, [C.c_uint32, C.c_uint64, C.c_uint32, C.c_int, C.POINTER(P)]),
     ("prag_gpu_embedder_free", None, [P]),
     ("prag_gpu_embed", C.c_int, [P, P, C.c_uint32, C.c_uint32, P, P]),

@@ -38,6 +38,14 @@ int require_device(int device) {
 }
 
 
+// SMs the persistent search kernels size their grids to: the device's, or
+// the index's budget (prag_gpu_set_sm_budget) when retrieval shares the GPU
+// with other work pinned to the remaining SMs (config E).
+int search_sms(const prag_gpu_index* ix) {
+    const int all = sm_count(ix->device);
+    return ix->sm_budget > 0 ? std::min(all, ix->sm_budget) : all;
+}
+
 int sm_count(int device) {
     static std::atomic<int> cache[64];
     if (device < 0 || device >= 64) {
@@ -397,8 +405,8 @@ int search_pass_skew(prag_gpu_index* ix, Workspace* w, const float* dq, uint32_t
                      uint64_t* o_ids, float* o_dist, uint32_t* o_count, uint64_t* o_scanned, cudaStream_t s,
                      prag_gpu_timings* tm) {
     const DeviceIndex& d = ix->dev;
-    const int sms = sm_count(ix->device);
-    const int grid = sms;  // persistent: one CTA per SM
+    const int sms = search_sms(ix);
+    const int grid = sms;  // persistent: one CTA per SM (of the search's SM budget)
     if (w->sync && search1_eligible(d, nq, nprobe, k, sms)) {
         // one query: the whole search in one launch (batch1.cu)
         PG_TRY(ws_reserve(w, search1_scratch_bytes(d, nprobe, grid), s));
@@ -515,7 +523,7 @@ int search_pass(prag_gpu_index* ix, Workspace* w, const float* dq, uint32_t nq, 
     const uint64_t item_cap = uint64_t(nq) * (nprobe + (max_cand_q + C - 1) / C) + 1;
     const uint32_t pw_p = pow2_at_least(nprobe);
     const uint32_t pw_f = pow2_at_least(std::max<uint64_t>(1, std::min<uint64_t>(k, max_cand_q)));
-    const int sms = sm_count(ix->device);
+    const int sms = search_sms(ix);
     const int per_sm = blocks_per_sm_scan(ix);
     const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>(item_cap, uint64_t(sms) * per_sm)));
     const size_t lut_bytes = size_t(d.nsq) * 1024 + ((d.d + 3) & ~3u) * 4;
@@ -1610,6 +1618,18 @@ uint32_t prag_gpu_select_nprobe(const prag_gpu_perf_model* m, double budget_s, u
     const double max_n = (limit - m->intercept_s) / m->slope_s;
     if (max_n >= double(nlist)) return nlist;
     return uint32_t(std::max(1.0, std::floor(max_n + 1e-9)));
+}
+
+int prag_gpu_set_sm_budget(prag_gpu_index* ix, int sms) {
+    PG_API_BEGIN
+    if (!ix || sms < 0) {
+        set_error("sm budget must be >= 0 (0: every SM)");
+        return PRAG_GPU_CONFIG;
+    }
+    ix->sm_budget = sms;
+    for (prag_gpu_index* sh : ix->shards) sh->sm_budget = sms;
+    return PRAG_GPU_OK;
+    PG_API_END
 }
 
 int prag_gpu_set_scan_path(prag_gpu_index* ix, int path) {

@@ -187,6 +187,7 @@ struct prag_gpu_index {
     bool profiling = false;
     int scan_path = 0;                            // 0 auto, 1 force generic
     int coarse_path = 0;                          // 0 auto (tensor cores when eligible), 1 force exact SIMT
+    int sm_budget = 0;                            // persistent search grids: 0 = every SM
     prag_gpu_timings last{};
     float* emb = nullptr;                         // raw embeddings [emb_n][d] for exact rerank (annindex.hpp:307-312)
     uint64_t emb_n = 0;
@@ -328,6 +329,7 @@ struct Carver {
 };
 
 int sm_count(int device);
+int search_sms(const prag_gpu_index* ix);
 // batch-1 single-launch search (batch1.cu)
 bool search1_eligible(const DeviceIndex& d, uint32_t nq, uint32_t nprobe, uint32_t k, int sms);
 size_t search1_scratch_bytes(const DeviceIndex& d, uint32_t nprobe, int grid);

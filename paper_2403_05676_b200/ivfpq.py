@@ -292,6 +292,11 @@ class GpuIndex:
         check(lib().prag_gpu_probe(self._h, _ptr(q), q.shape[0], nprobe, _ptr(lists), _ptr(dist), None))
         return lists, dist
 
+    def set_sm_budget(self, sms: int) -> None:
+        """Persistent search grids on at most `sms` SMs (0 = all): retrieval
+        beside work pinned to the other SMs (prag_gpu_set_sm_budget)."""
+        check(lib().prag_gpu_set_sm_budget(self._h, int(sms)))
+
     def set_scan_path(self, path: int) -> None:
         """0 = automatic (fast lane-skewed path when eligible), 1 = generic."""
         check(lib().prag_gpu_set_scan_path(self._h, path))

@@ -8,16 +8,26 @@ and a mutex/condition-variable mailbox (pipeline.hpp:471-554, mailbox
                   (prag_gpu_synthetic_decode: the model's fp32 weights plus
                   the KV cache of earlier positions streamed per token),
                   standing in for SyntheticGenerator (generator.hpp:220-252);
-  * retrieval  -- a high-priority side stream runs the IVF-PQ search of the
-                  next chunk (prag_gpu_search, device pointers, async);
+  * retrieval  -- a high-priority side stream runs the query embedding
+                  (prag_gpu_embed, ChunkEmbedder::embed bit-identical) and
+                  the IVF-PQ search of the next chunk (prag_gpu_search,
+                  device pointers, async);
   * mailbox    -- a CUDA event per chunk: ready(j) = cudaEventQuery,
                   take(j) = cudaStreamWaitEvent on the main stream; the stall
-                  is the device time the main stream spends blocked on it.
+                  is the device time the main stream spends blocked on it;
+  * SMs        -- with `retrieval_sms` = R, the piperag decode runs on the
+                  other S - R SMs (prag_gpu_synthetic_decode_sms: one CTA per
+                  SM) and the search sizes its persistent grids to R SMs
+                  (prag_gpu_set_sm_budget), so the side stream has SMs of its
+                  own instead of waiting for decode kernels to drain.
 
 Modes and their schedule follow PipelineEngine::run_impl (pipeline.hpp
 :414-452): "retro" retrieves (blocking) before every chunk, "piperag" launches
-chunk j+1's retrieval before generating chunk j (staleness 0 here: the query
-is fixed per chunk, query embedding is out of scope).
+chunk j+1's retrieval before generating chunk j. The query of chunk j is the
+window of m tokens ending `staleness` tokens before chunk j starts
+(make_query_window, pipeline.hpp:122-144; staleness = interval for piperag
+and 0 for retro, pipeline.hpp:70-76), embedded on the GPU; without a token
+sequence the engine falls back to fixed query rows.
 With the auto nprobe policy, nprobe = select_nprobe(retrieval model,
 predict_chunk_budget(inference model, position)) (pipeline.hpp:414-420,
 perfmodel.hpp:148-183). All timestamps are CUDA events on the device clock.
@@ -102,7 +112,7 @@ class SyntheticDecoder:
     plus `kv_bytes_per_token` of KV cache per earlier position."""
 
     def __init__(self, params: int = 582_000_000, cols: int = 4096, kv_bytes_per_token: int = 2 * 24 * 1024 * 4,
-                 max_positions: int = 4096, device: int = 0, stream=None):
+                 max_positions: int = 4096, device: int = 0, stream=None, sms: Optional[int] = None):
         assert torch is not None
         self.dev = torch.device("cuda", device)
         self.cols = cols
@@ -114,6 +124,7 @@ class SyntheticDecoder:
         self.kv = torch.randn(self.kv_per_tok * max_positions, device=self.dev, dtype=torch.float32)
         self.max_positions = max_positions
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.dev)
+        self.sms = sms  # None: every SM (grid of 4 CTAs per SM); else one CTA on each of `sms` SMs
 
     def bytes_per_token(self, position: int) -> int:
         return self.rows * self.cols * 4 + min(position, self.max_positions) * self.kv_per_tok * 4
@@ -121,9 +132,12 @@ class SyntheticDecoder:
     def step(self, position: int, stream=None) -> None:
         s = stream if stream is not None else self.stream
         kvf = min(position, self.max_positions) * self.kv_per_tok
-        check(lib().prag_gpu_synthetic_decode(C.c_void_p(self.w.data_ptr()), self.rows, self.cols,
-                                              C.c_void_p(self.x.data_ptr()), C.c_void_p(self.y.data_ptr()),
-                                              C.c_void_p(self.kv.data_ptr()), kvf, C.c_void_p(s.cuda_stream)))
+        args = (C.c_void_p(self.w.data_ptr()), self.rows, self.cols, C.c_void_p(self.x.data_ptr()),
+                C.c_void_p(self.y.data_ptr()), C.c_void_p(self.kv.data_ptr()), kvf)
+        if self.sms:
+            check(lib().prag_gpu_synthetic_decode_sms(*args, int(self.sms), C.c_void_p(s.cuda_stream)))
+        else:
+            check(lib().prag_gpu_synthetic_decode(*args, C.c_void_p(s.cuda_stream)))
 
     def generate_chunk(self, position: int, m_prime: int, stream=None) -> None:
         for o in range(m_prime):
@@ -158,6 +172,7 @@ class GenerationTrace:
     stall_count: int = 0
     nprobe_used: List[int] = field(default_factory=list)
     results: List[BatchResult] = field(default_factory=list)
+    queries: List[object] = field(default_factory=list)  # the embedded query of each retrieval
 
     def durations(self, start_kind: str):
         end = {"gen_chunk_start": "gen_chunk_end", "ret_start": "ret_end"}.get(start_kind, "stall_end")
@@ -176,12 +191,18 @@ class PipelineEngine:
 
     STALL_EPS_S = 2e-6  # a wait shorter than this is an already-delivered context
 
-    def __init__(self, decoder: SyntheticDecoder, index: GpuIndex, queries, k: int = 2,
+    def __init__(self, decoder: SyntheticDecoder, index: GpuIndex, queries=None, k: int = 2,
                  retrieval_model: Optional[RetrievalPerfModel] = None,
-                 inference_model: Optional[InferencePerfModel] = None, safety_margin: float = 0.10):
+                 inference_model: Optional[InferencePerfModel] = None, safety_margin: float = 0.10,
+                 embedder=None, tokens=None, retrieval_sms: Optional[int] = None):
         self.dec = decoder
         self.ix = index
-        self.q = queries  # CUDA tensor [n_queries, d]; chunk j uses row (j-1) % n
+        self.q = queries  # fallback: CUDA tensor [n_queries, d]; chunk j uses row (j-1) % n
+        # the token sequence (CUDA int32 [>= m + total_tokens]: prompt chunk,
+        # then the generated tokens) and the GPU ChunkEmbedder for query windows
+        self.embedder = embedder
+        self.tokens = tokens
+        self.retrieval_sms = retrieval_sms
         self.k = k
         self.rmodel = retrieval_model
         self.imodel = inference_model
@@ -197,10 +218,26 @@ class PipelineEngine:
         budget, _ = predict_chunk_budget(self.imodel, m + (j - 1) * mp)
         return select_nprobe(self.rmodel, budget, self.ix.nlist, self.margin)
 
+    def query_window(self, j: int, m: int, mp: int, s: int):
+        """make_query_window (pipeline.hpp:122-144) over the token sequence:
+        the m tokens ending s before chunk j starts (j == 1: non-stale),
+        pad token 0 before position 0; a [1, m] view or padded copy."""
+        s_eff = 0 if j == 1 else s
+        begin = m + (j - 1) * mp - s_eff - m
+        if begin + m > self.tokens.shape[0]:
+            raise ValueError("make_query_window: window extends past generated tokens")
+        if begin >= 0:
+            return self.tokens[begin:begin + m].view(1, m)
+        w = torch.zeros((1, m), dtype=self.tokens.dtype, device=self.tokens.device)
+        w[0, -begin:] = self.tokens[:begin + m]
+        return w
+
     def run(self, mode: str, total_tokens: int, interval: int, query_window: int = 64,
             nprobe: Optional[int] = 16) -> GenerationTrace:
         if mode not in ("retro", "piperag"):
             raise ValueError("mode must be retro or piperag")
+        if self.tokens is None and self.q is None:
+            raise ValueError("PipelineEngine needs a token sequence (+ embedder) or fixed query rows")
         if nprobe is None and (self.rmodel is None or self.imodel is None):
             raise ValueError("auto nprobe needs retrieval and inference perf models")
         mp, m = interval, query_window
@@ -214,16 +251,31 @@ class PipelineEngine:
             ev.append((kind, j, e))
             return e
 
+        staleness = mp if mode == "piperag" else 0  # pipeline.hpp:70-76
+
         def retrieve(j, stream):
             npb = self._nprobe(j, m, mp, nprobe)
             rec("ret_start", j, stream)
-            qi = (j - 1) % self.q.shape[0]
-            r = self.ix.search_batch(self.q[qi:qi + 1], self.k, npb, stream=stream)
+            if self.tokens is not None:
+                qv = self.embedder.embed(self.query_window(j, m, mp, staleness), stream=stream)
+            else:
+                qi = (j - 1) % self.q.shape[0]
+                qv = self.q[qi:qi + 1]
+            r = self.ix.search_batch(qv, self.k, npb, stream=stream)
             done = rec("ret_end", j, stream)
             tr.nprobe_used.append(npb)
             tr.retrieval_count += 1
             tr.results.append(r)
+            tr.queries.append(qv)
             return done
+
+        # SM partition for the overlapped mode: decode on S - R SMs, search on R
+        part = mode == "piperag" and self.retrieval_sms
+        saved = self.dec.sms
+        if part:
+            total = torch.cuda.get_device_properties(self.dec.dev).multi_processor_count
+            self.dec.sms = max(1, total - int(self.retrieval_sms))
+            self.ix.set_sm_budget(int(self.retrieval_sms))
 
         t0 = torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize(self.dec.dev)
@@ -259,6 +311,9 @@ class PipelineEngine:
         t1 = rec("end", 0, self.main)
         self.main.wait_stream(self.side)
         torch.cuda.synchronize(self.dec.dev)
+        if part:
+            self.dec.sms = saved
+            self.ix.set_sm_budget(0)
         stalled = set()
         for j, s0, s1 in stalls:
             dt = s0.elapsed_time(s1) / 1e3
