@@ -163,7 +163,11 @@ int upload(prag_gpu_index* ix, const HostIndex& h) {
     PG_TRY(dmalloc(&d.list_off, size_t(nl) + 1, acct));
     PG_TRY(dmalloc(&d.list_len, nl, acct));
     PG_TRY(dmalloc(&d.ids, d.npadded, acct));
-    PG_TRY(dmalloc(&d.codes, d.npadded * h.nsq, acct));
+    // m = 32 / 64: the lane-skewed tiles are the only copy of the codes in
+    // HBM (the generic path gathers from them too); other m: plain [slot][m]
+    const bool skew_only = (h.nsq == 32 || h.nsq == 64) && h.sub_dim <= 16;
+    if (!skew_only) PG_TRY(dmalloc(&d.codes, d.npadded * h.nsq, acct));
+    d.plain_codes = !skew_only;
 
     PG_CUDA(cudaMemcpy(d.centroids, h.centroids.data(), h.centroids.size() * 4, cudaMemcpyHostToDevice));
     {
@@ -192,19 +196,19 @@ int upload(prag_gpu_index* ix, const HostIndex& h) {
     {
         // padded ids (pad = ~0) and codes (pad = 0), uploaded list by list group
         std::vector<uint64_t> pid(d.npadded, ~0ull);
-        std::vector<uint8_t> pcode(d.npadded * h.nsq, 0);
+        std::vector<uint8_t> pcode(d.codes ? d.npadded * h.nsq : 0, 0);
         for (uint32_t l = 0; l < nl; ++l) {
             const uint64_t src = h.list_off[l], n = len[l];
             std::memcpy(&pid[off[l]], &h.ids[src], n * 8);
-            std::memcpy(&pcode[off[l] * h.nsq], &h.codes[src * h.nsq], n * h.nsq);
+            if (d.codes) std::memcpy(&pcode[off[l] * h.nsq], &h.codes[src * h.nsq], n * h.nsq);
         }
         PG_CUDA(cudaMemcpy(d.ids, pid.data(), pid.size() * 8, cudaMemcpyHostToDevice));
-        PG_CUDA(cudaMemcpy(d.codes, pcode.data(), pcode.size(), cudaMemcpyHostToDevice));
+        if (d.codes) PG_CUDA(cudaMemcpy(d.codes, pcode.data(), pcode.size(), cudaMemcpyHostToDevice));
     }
     d.code_layout = 0;
     PG_TRY(dmalloc(&d.codewords, h.codewords.size(), acct));
     PG_CUDA(cudaMemcpy(d.codewords, h.codewords.data(), h.codewords.size() * 4, cudaMemcpyHostToDevice));
-    if ((h.nsq == 32 || h.nsq == 64) && h.sub_dim <= 16) {
+    if (skew_only) {
         std::vector<uint64_t> soff;
         std::vector<uint8_t> scodes;
         build_skew_layout(h, h.nsq, soff, scodes);
@@ -613,10 +617,6 @@ int search_pass(prag_gpu_index* ix, Workspace* w, const float* dq, uint32_t nq, 
 }
 
 int validate(const prag_gpu_index* ix, uint32_t nprobe, uint32_t k) {
-    if (!ix->dev.plain_codes && (k > 32 || ix->scan_path != 0)) {
-        set_error("search: this index keeps only the lane-skewed code layout (synthetic index): k must be <= 32");
-        return PRAG_GPU_CONFIG;
-    }
     if (k < 1) {  // annindex.hpp:265
         set_error("search: k must be >= 1");
         return PRAG_GPU_CONFIG;
@@ -666,10 +666,6 @@ int do_search(prag_gpu_index* ix, const float* queries, uint32_t nq, uint32_t np
     const bool has_emb = ix->is_group() ? ix->shards[0]->emb != nullptr : ix->emb != nullptr;
     if (rerank && !has_emb) {  // annindex.hpp:269-271
         set_error("search: exact_rerank requires raw embeddings");
-        return PRAG_GPU_CONFIG;
-    }
-    if (rerank && !ix->dev.plain_codes) {
-        set_error("search: exact_rerank needs the plain code layout (not a device-built synthetic index)");
         return PRAG_GPU_CONFIG;
     }
     if (nq == 0) return PRAG_GPU_OK;
@@ -1093,22 +1089,48 @@ int prag_gpu_index_store(const prag_gpu_index* ix, const char* path) {
         set_error("store: a shard holds only part of the lists; store the full index");
         return PRAG_GPU_CONFIG;
     }
-    if (!d.plain_codes) {
-        set_error("store: this index has no plain code copy (device-built synthetic index)");
-        return PRAG_GPU_CONFIG;
-    }
     DeviceGuard g(ix->device);
     const uint32_t nl = d.nlist, sub = d.d / d.nsq;
     std::vector<float> cent(size_t(nl) * d.d), words(size_t(d.nsq) * 256 * sub);
     std::vector<uint64_t> off(size_t(nl) + 1), ids(d.npadded);
     std::vector<uint32_t> len(nl);
     std::vector<uint8_t> codes(d.npadded * d.nsq);
+    if (d.codes) {
+        PG_CUDA(cudaMemcpy(codes.data(), d.codes, codes.size(), cudaMemcpyDeviceToHost));
+    } else {  // only the lane-skewed tiles are resident: undo the skew (scan_skew.cu)
+        std::vector<uint64_t> soff(size_t(nl) + 1), off2(size_t(nl) + 1);
+        std::vector<uint32_t> len2(nl);
+        PG_CUDA(cudaMemcpy(soff.data(), d.skew_off, soff.size() * 8, cudaMemcpyDeviceToHost));
+        PG_CUDA(cudaMemcpy(off2.data(), d.list_off, off2.size() * 8, cudaMemcpyDeviceToHost));
+        PG_CUDA(cudaMemcpy(len2.data(), d.list_len, len2.size() * 4, cudaMemcpyDeviceToHost));
+        const uint32_t m = d.nsq;
+        std::vector<uint8_t> tiles;
+        for (uint32_t l = 0; l < nl; ++l) {
+            const uint64_t nt = soff[l + 1] - soff[l];
+            if (!nt) continue;
+            tiles.resize(nt * 32 * m);
+            PG_CUDA(cudaMemcpy(tiles.data(), d.skew_codes + soff[l] * 32 * m, tiles.size(), cudaMemcpyDeviceToHost));
+            for (uint32_t e = 0; e < len2[l]; ++e) {
+                const uint32_t t = e & 31u;
+                for (uint32_t b = 0; b < m; ++b) {
+                    uint32_t tile = e >> 5, s = b + t;
+                    bool tail = false;
+                    if (s >= m) {
+                        s -= m;
+                        ++tile;
+                        tail = true;
+                    }
+                    const uint8_t v = tiles[size_t(tile) * 32 * m + (s >> 4) * 512 + t * 16 + (s & 15u)];
+                    codes[(off2[l] + e) * m + b] = (tail && m == 64) ? uint8_t(v - 1) : v;
+                }
+            }
+        }
+    }
     PG_CUDA(cudaMemcpy(cent.data(), d.centroids, cent.size() * 4, cudaMemcpyDeviceToHost));
     PG_CUDA(cudaMemcpy(words.data(), d.codewords, words.size() * 4, cudaMemcpyDeviceToHost));
     PG_CUDA(cudaMemcpy(off.data(), d.list_off, off.size() * 8, cudaMemcpyDeviceToHost));
     PG_CUDA(cudaMemcpy(len.data(), d.list_len, len.size() * 4, cudaMemcpyDeviceToHost));
     PG_CUDA(cudaMemcpy(ids.data(), d.ids, ids.size() * 8, cudaMemcpyDeviceToHost));
-    PG_CUDA(cudaMemcpy(codes.data(), d.codes, codes.size(), cudaMemcpyDeviceToHost));
     // annindex.hpp:335-359 layout, written to a temporary then renamed
     const std::string tmp = std::string(path) + ".tmp";
     FILE* f = fopen(tmp.c_str(), "wb");

@@ -451,14 +451,34 @@ __global__ void __launch_bounds__(1024) plan_kernel(const uint32_t* __restrict__
 // T[sq][code] = squared_l2(r_sq, w[sq][code], sub_dim) (:293-299) are built
 // in SMEM; then each thread folds one entry at a time:
 // dist = ((0 + T[0][c0]) + T[1][c1]) + ... (:300-302).
-template <bool kSmemLut>
+// Code byte b of entry e of a list in the lane-skewed tile layout K3 reads
+// (scan_skew.cu): lane t = e mod 32 of tile e / 32 folds it at step b + t;
+// steps past m continue in the next tile, whose tail bytes m = 64 stores as
+// code + 1 (scan_skew.cu SkewSmem).
+__device__ __forceinline__ uint32_t skew_code(const uint8_t* __restrict__ tiles, uint32_t nsq, uint32_t e,
+                                              uint32_t b) {
+    const uint32_t t = e & 31u;
+    uint32_t tile = e >> 5, s = b + t;
+    bool tail = false;
+    if (s >= nsq) {
+        s -= nsq;
+        ++tile;
+        tail = true;
+    }
+    const uint32_t v = tiles[size_t(tile) * 32 * nsq + (s >> 4) * 512 + t * 16 + (s & 15u)];
+    return (tail && nsq == 64) ? ((v - 1) & 255u) : v;
+}
+
+// kSkew: the index keeps only the lane-skewed code tiles (m = 32 / 64); the
+// entry's code bytes are gathered from them instead of the plain array.
+template <bool kSmemLut, bool kSkew>
 __global__ void __launch_bounds__(256) scan_kernel(
     const float* __restrict__ queries, const float* __restrict__ centroids,
     const float* __restrict__ codewordsT, const uint64_t* __restrict__ list_off,
-    const uint32_t* __restrict__ list_len, const uint8_t* __restrict__ codes, uint32_t d, uint32_t nsq,
-    uint32_t sub_dim, const uint4* __restrict__ items, const uint32_t* __restrict__ num_items,
-    uint32_t* __restrict__ cursor, float* __restrict__ cand_dist, uint32_t* __restrict__ cand_entry,
-    float* __restrict__ glut) {
+    const uint32_t* __restrict__ list_len, const uint8_t* __restrict__ codes, const uint64_t* __restrict__ skew_off,
+    uint32_t d, uint32_t nsq, uint32_t sub_dim, const uint4* __restrict__ items,
+    const uint32_t* __restrict__ num_items, uint32_t* __restrict__ cursor, float* __restrict__ cand_dist,
+    uint32_t* __restrict__ cand_entry, float* __restrict__ glut) {
     extern __shared__ __align__(16) float smf[];
     float* resid = smf;                                   // [d]
     float* lut = kSmemLut ? smf + ((d + 3) & ~3u) : glut + size_t(blockIdx.x) * nsq * 256;
@@ -499,7 +519,10 @@ __global__ void __launch_bounds__(256) scan_kernel(
             const uint64_t slot = lbase + e;
             const uint8_t* c = codes + slot * nsq;
             float dist = 0.0f;
-            if ((nsq & 3u) == 0) {
+            if (kSkew) {
+                const uint8_t* tiles = codes + skew_off[list] * 32 * nsq;
+                for (uint32_t s = 0; s < nsq; ++s) dist = __fadd_rn(dist, lut[s * 256 + skew_code(tiles, nsq, e, s)]);
+            } else if ((nsq & 3u) == 0) {
                 for (uint32_t s4 = 0; s4 < nsq; s4 += 4) {
                     const uint32_t wd = *reinterpret_cast<const uint32_t*>(c + s4);
                     dist = __fadd_rn(dist, lut[(s4 + 0) * 256 + (wd & 255u)]);
@@ -741,19 +764,31 @@ int launch_scan(const DeviceIndex& ix, const SearchBuffers& b, cudaStream_t s, i
     const size_t lut_bytes = size_t(ix.nsq) * 256 * sizeof(float);
     const size_t res_bytes = ((ix.d + 3) & ~3u) * sizeof(float);
     const bool smem_lut = lut_bytes + res_bytes <= 200 * 1024;
+    // no plain code array: read the lane-skewed tiles (m = 32 / 64)
+    const bool skew = ix.codes == nullptr;
+    const uint8_t* codes = skew ? ix.skew_codes : ix.codes;
+#define PG_SCAN(SM, SK, SMEM, GL)                                                                               \
+    do {                                                                                                       \
+        PG_CUDA(ensure_smem(reinterpret_cast<const void*>(scan_kernel<SM, SK>), int(SMEM)));                  \
+        scan_kernel<SM, SK><<<grid, 256, SMEM, s>>>(b.queries, ix.centroids, ix.codewordsT, ix.list_off,       \
+                                                    ix.list_len, codes, ix.skew_off, ix.d, ix.nsq, ix.sub_dim, \
+                                                    b.items, b.num_items, b.item_cursor, b.cand_dist,          \
+                                                    b.cand_entry, GL);                                         \
+    } while (0)
     if (smem_lut) {
         const size_t smem = lut_bytes + res_bytes;
-        PG_CUDA(ensure_smem(reinterpret_cast<const void*>(scan_kernel<true>), int(smem)));
-        scan_kernel<true><<<grid, 256, smem, s>>>(b.queries, ix.centroids, ix.codewordsT, ix.list_off, ix.list_len,
-                                                  ix.codes, ix.d, ix.nsq, ix.sub_dim, b.items, b.num_items,
-                                                  b.item_cursor, b.cand_dist, b.cand_entry, nullptr);
+        if (skew)
+            PG_SCAN(true, true, smem, nullptr);
+        else
+            PG_SCAN(true, false, smem, nullptr);
     } else {
         const size_t smem = res_bytes;
-        PG_CUDA(ensure_smem(reinterpret_cast<const void*>(scan_kernel<false>), int(smem)));
-        scan_kernel<false><<<grid, 256, smem, s>>>(b.queries, ix.centroids, ix.codewordsT, ix.list_off,
-                                                   ix.list_len, ix.codes, ix.d, ix.nsq, ix.sub_dim, b.items,
-                                                   b.num_items, b.item_cursor, b.cand_dist, b.cand_entry, glut);
+        if (skew)
+            PG_SCAN(false, true, smem, glut);
+        else
+            PG_SCAN(false, false, smem, glut);
     }
+#undef PG_SCAN
     return check_launch("scan");
 }
 

@@ -404,11 +404,13 @@ struct SkewCfg<32> {
 };
 template <>
 struct SkewCfg<64> {
-    // (more than 12 warps put 4 on some SM sub-partition, which caps a
-    // thread at 128 registers: ptxas then rematerialises part of the 64
-    // step-mask registers inside the fold -- still cheaper than spilling)
-    static constexpr int kWarps = 12;
-    static constexpr int kExp = 2;
+    // 10 consumers + producer + 1 expander = 12 warps, 3 per SM
+    // sub-partition: up to 168 registers a thread, so both code tiles in
+    // flight (32 registers) and the 64 step-mask registers stay resident
+    // (with 15 warps the 128-register cap made ptxas rematerialise the masks
+    // inside the fold, ~35 extra instructions per 2 KiB tile)
+    static constexpr int kWarps = 10;
+    static constexpr int kExp = 1;
     static constexpr int kPrefetch = 2;
 };
 

@@ -44,8 +44,12 @@ def test_synthetic_index_matches_host_restatement(m):
     q = (cents[rng.integers(0, 256, 6)] + rng.standard_normal((6, 384)).astype(np.float32) * 0.5).astype(np.float32)
     for nprobe, k in [(1, 10), (16, 10), (5, 32)]:
         _check(ix, cents, words, seed, q, nprobe, k)
-    with pytest.raises(pg.ConfigError):  # no plain code copy: fast path only
-        ix.search_batch(q, 33, 4)
+    # k > 32 takes the generic path, which gathers from the lane-skewed tiles
+    # (the only code copy in HBM)
+    _check(ix, cents, words, seed, q, 4, 33)
+    ix.set_scan_path(1)
+    _check(ix, cents, words, seed, q, 16, 10)
+    ix.set_scan_path(0)
 
 
 @pytest.mark.skipif(os.environ.get("PRAG_CONFIG_D") != "1", reason="set PRAG_CONFIG_D=1 (1B entries, 72 GB HBM)")
@@ -65,3 +69,30 @@ def test_config_d_1b_sampled_parity():
         for i in range(q.shape[0]):
             print(f"  nprobe={nprobe} k={k} q{i}: scanned_vectors={int(r.scanned[i])} "
                   f"ids[:5]={r.ids[i, :5].tolist()} == host restatement (ids, distance bits, scanned)")
+
+
+@pytest.mark.parametrize("m", [32, 64])
+def test_synthetic_store_roundtrip_through_oracle(tmp_path, m):
+    """prag_gpu_index_store rebuilds the plain codes from the lane-skewed
+    tiles (the only copy in HBM; m = 64 tail bytes are stored + 1): the
+    written PRAGIX01 searched by the CPU oracle equals the GPU search and the
+    restatement."""
+    import _oracle as O
+    import paper_2403_05676_b200 as pg
+    cents, words = _model(128, 384, m, 8)
+    seed = 700 + m
+    ix = pg.GpuIndex.synthetic(cents, words, 60_000, seed=seed, sigma=1.0)
+    p = str(tmp_path / f"synth{m}.pragix")
+    ix.store(p)
+    oi = O.OracleIndex(p)
+    rng = np.random.default_rng(4)
+    q = (cents[rng.integers(0, 128, 5)] + rng.standard_normal((5, 384)).astype(np.float32) * 0.5).astype(np.float32)
+    for nprobe, k in [(1, 10), (8, 40), (128, 5)]:
+        r = ix.search_batch(q, k, nprobe)
+        o_ids, o_dist, o_cnt, o_sc = oi.search(q, nprobe, k)
+        assert (r.count == o_cnt).all() and (r.scanned == o_sc).all()
+        for i in range(q.shape[0]):
+            c = int(o_cnt[i])
+            assert (r.ids[i, :c] == o_ids[i, :c]).all()
+            assert (r.dist[i, :c].view(np.uint32) == o_dist[i, :c].view(np.uint32)).all()
+    _check(ix, cents, words, seed, q, 8, 40)
