@@ -403,6 +403,13 @@ int run_coarse(const prag_gpu_index* ix, const float* dq, uint32_t nq, uint32_t 
     return launch_select_probe(d, coarse, nq, nprobe, probe, probe_dist, pkey, ptie, s);
 }
 
+// PRAG_GPU_SPLIT_ITEMS (tuning knob, scan_skew.cu launch_lut_images): extra
+// work-item capacity when it asks for more split items than the default.
+static uint64_t split_items_override() {
+    const char* e = getenv("PRAG_GPU_SPLIT_ITEMS");
+    return e ? 3ull * uint64_t(std::max(0, atoi(e))) : 0ull;
+}
+
 // Fast path (m = 32 / 64, k <= 32): coarse -> top-nprobe -> plan -> LUT
 // images -> fused conflict-free scan + warp top-k -> pool select.
 int search_pass_skew(prag_gpu_index* ix, Workspace* w, const float* dq, uint32_t nq, uint32_t nprobe, uint32_t k,
@@ -433,7 +440,8 @@ int search_pass_skew(prag_gpu_index* ix, Workspace* w, const float* dq, uint32_t
     // given (nq, nprobe) always plans the same way)
     const uint64_t max_tiles_q = (ix->top_prefix[nprobe] + 31) / 32 + nprobe;
     const uint32_t IT = skew_item_tiles(uint64_t(nq) * max_tiles_q, uint32_t(grid));
-    const uint64_t item_cap = uint64_t(nq) * (nprobe + max_tiles_q / IT + 1) + 1;
+    // + the tail items the planner may split (kSplit - 1 = 3 extra per split item)
+    const uint64_t item_cap = uint64_t(nq) * (nprobe + max_tiles_q / IT + 1) + 1 + split_items_override();
     const uint64_t pool_cap = item_cap * k;  // k entries per work item
     const uint32_t pw_p = pow2_at_least(nprobe);
     const uint32_t pw_f = pow2_at_least(std::max<uint64_t>(1, std::min<uint64_t>(k, pool_cap)));
@@ -481,7 +489,7 @@ int search_pass_skew(prag_gpu_index* ix, Workspace* w, const float* dq, uint32_t
     PG_TRY(run_coarse(ix, dq, nq, nprobe, coarse, probe, probe_dist, pkey, ptie, s, prof ? w : nullptr));
     if (prof) cudaEventRecord(w->ev[2], s);
     PG_TRY(launch_lut_images(d, dq, probe, nq, nprobe, images, IT, o_scanned, items, ctr, ctr + 1, q_item_off, gthr,
-                             pair_off, item_cap, s));
+                             pair_off, item_cap, uint32_t(grid), s));
     if (prof) cudaEventRecord(w->ev[3], s);
     PG_TRY(launch_scan_skew(d, items, ctr, ctr + 1, probe, images, nprobe, k, gthr, pool_key, pool_id, grid, s));
     if (prof) cudaEventRecord(w->ev[4], s);

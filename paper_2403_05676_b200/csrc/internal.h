@@ -263,7 +263,7 @@ uint32_t scan_chunk();
 int launch_lut_images(const DeviceIndex& ix, const float* queries, const uint32_t* probe, uint32_t nq,
                       uint32_t nprobe, float* luts, uint32_t it_tiles, uint64_t* scanned, uint4* items,
                       uint32_t* num_items, uint32_t* cursor, uint32_t* q_item_off, uint32_t* gthr,
-                      uint32_t* pair_off, uint64_t item_cap, cudaStream_t s);
+                      uint32_t* pair_off, uint64_t item_cap, uint32_t scan_grid, cudaStream_t s);
 int launch_scan_skew(const DeviceIndex& ix, const uint4* items, const uint32_t* num_items, uint32_t* cursor,
                      const uint32_t* probe, const float* images, uint32_t nprobe, uint32_t k, uint32_t* gthr,
                      uint32_t* pool_key, uint64_t* pool_id, int grid, cudaStream_t s);

@@ -24,6 +24,7 @@
 //    (distance, chunk_id); a per-query threshold shared through global
 //    memory (atomicMin on the k-th distance) prunes candidates; ids are
 //    loaded only for candidates that pass.
+#include <algorithm>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -78,6 +79,7 @@ constexpr uint32_t image_floats() {
 // writes scanned_vectors (annindex.hpp:305: the sum of probed list sizes).
 struct PlanArgs {
     uint32_t it_tiles;
+    uint32_t split_items;  // full items cut into kSplit smaller ones (scheduled last): the queue's tail
     uint64_t* scanned;
     uint4* items;
     uint32_t* num_items;
@@ -87,6 +89,13 @@ struct PlanArgs {
     uint32_t* pair_off;  // [nq * nprobe] pool item index of each pair's first item
     uint64_t item_cap;
 };
+
+// The scan's work queue is consumed largest item first, so the kernel's tail
+// is the last items: with ~4 items per CTA of up to kMaxItemTiles each (config
+// C/D at batch 1) a CTA can finish a whole item after the others. The planner
+// therefore cuts `split_items` of the full items into kSplit pieces that land
+// in a smaller size bucket, i.e. at the end of the queue ("guided" tail).
+constexpr uint32_t kSplit = 4;
 
 // plan_items for up to R pairs per thread (P <= R * blockDim.x): thread t
 // owns pairs [t*R, t*R + R), so every probe[] / list_len[] load is issued up
@@ -116,19 +125,58 @@ __device__ __noinline__ void plan_items_regs(const uint32_t* __restrict__ probe,
         const uint32_t i = tid * R + r;
         len[r] = i < P ? list_len[len[r]] : 0u;
     }
-    __syncthreads();  // scanned[] zeroed, bucket_cnt ready
-    uint32_t mine = 0;
+    // full items of this thread's pairs, and their exclusive prefix over the
+    // block (pair order): full item number g < split is cut into kSplit pieces
+    uint32_t fmine = 0;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-        const uint32_t i = tid * R + r;
-        if (len[r]) atomicAdd(reinterpret_cast<unsigned long long*>(pa.scanned + i / nprobe), (unsigned long long)len[r]);
         const uint32_t tiles = (len[r] + kTileEntries - 1) / kTileEntries;
         const uint32_t nit = (tiles + it_tiles - 1) / it_tiles;
-        if (nit) {  // nit - 1 full items, then the remainder
-            if (nit > 1) atomicAdd(&bucket_cnt[31 - __clz(it_tiles)], nit - 1);
-            atomicAdd(&bucket_cnt[31 - __clz(tiles - (nit - 1) * it_tiles)], 1u);
+        fmine += nit ? nit - 1 : 0u;
+    }
+    const uint32_t split = it_tiles >= kSplit * kMinItemTiles ? pa.split_items : 0u;
+    uint32_t fincl = fmine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, fincl, o);
+        if (lane >= uint32_t(o)) fincl += t;
+    }
+    if (lane == 31) wsum[w] = fincl;
+    __syncthreads();  // scanned[] zeroed, bucket_cnt ready, full-item warp sums
+    if (w == 0) {
+        const uint32_t nw = blockDim.x >> 5;
+        const uint32_t x = lane < nw ? wsum[lane] : 0u;
+        uint32_t xi = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, xi, o);
+            if (lane >= uint32_t(o)) xi += t;
         }
-        mine += nit;
+        if (lane < nw) wsum[lane] = xi - x;
+    }
+    __syncthreads();
+    const uint32_t fexcl0 = wsum[w] + fincl - fmine;
+    __syncthreads();  // wsum is reused below
+    const uint32_t sub_tiles = it_tiles / kSplit;
+    uint32_t mine = 0;
+    {
+        uint32_t fexcl = fexcl0;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const uint32_t i = tid * R + r;
+            if (len[r]) atomicAdd(reinterpret_cast<unsigned long long*>(pa.scanned + i / nprobe), (unsigned long long)len[r]);
+            const uint32_t tiles = (len[r] + kTileEntries - 1) / kTileEntries;
+            const uint32_t nit = (tiles + it_tiles - 1) / it_tiles;
+            if (nit) {  // nit - 1 full items (the first `split - fexcl` of them cut), then the remainder
+                const uint32_t full = nit - 1;
+                const uint32_t cut = fexcl < split ? min(full, split - fexcl) : 0u;
+                if (full > cut) atomicAdd(&bucket_cnt[31 - __clz(it_tiles)], full - cut);
+                if (cut) atomicAdd(&bucket_cnt[31 - __clz(sub_tiles)], cut * kSplit);
+                atomicAdd(&bucket_cnt[31 - __clz(tiles - full * it_tiles)], 1u);
+                mine += nit + cut * (kSplit - 1);
+                fexcl += full;
+            }
+        }
     }
     // exclusive block prefix of `mine` (pair order = thread order)
     uint32_t incl = mine;
@@ -160,6 +208,7 @@ __device__ __noinline__ void plan_items_regs(const uint32_t* __restrict__ probe,
     }
     __syncthreads();
     uint32_t excl = wsum[w] + incl - mine;
+    uint32_t fexcl = fexcl0;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const uint32_t i = tid * R + r;
@@ -168,15 +217,30 @@ __device__ __noinline__ void plan_items_regs(const uint32_t* __restrict__ probe,
         if (i % nprobe == 0) pa.q_item_off[i / nprobe] = excl;
         const uint32_t tiles = (len[r] + kTileEntries - 1) / kTileEntries;
         const uint32_t nit = (tiles + it_tiles - 1) / it_tiles;
+        uint32_t nout = 0;  // items this pair emits (pool slots excl .. excl + nout)
         if (nit) {
             const uint32_t full = nit - 1;
-            const uint32_t b0 = full ? atomicAdd(&bucket_pos[31 - __clz(it_tiles)], full) : 0u;
-            for (uint32_t j = 0; j < full; ++j)
-                if (b0 + j < pa.item_cap) pa.items[b0 + j] = make_uint4(i, j * it_tiles, (j + 1) * it_tiles, excl + j);
+            const uint32_t cut = fexcl < split ? min(full, split - fexcl) : 0u;
+            // the first `cut` full items in kSplit pieces (the queue's tail)
+            const uint32_t c0 = cut ? atomicAdd(&bucket_pos[31 - __clz(sub_tiles)], cut * kSplit) : 0u;
+            for (uint32_t j = 0; j < cut; ++j)
+                for (uint32_t h = 0; h < kSplit; ++h) {
+                    const uint32_t tb = j * it_tiles + h * sub_tiles, n = j * kSplit + h;
+                    if (c0 + n < pa.item_cap) pa.items[c0 + n] = make_uint4(i, tb, tb + sub_tiles, excl + n);
+                }
+            nout = cut * kSplit;
+            const uint32_t b0 = full > cut ? atomicAdd(&bucket_pos[31 - __clz(it_tiles)], full - cut) : 0u;
+            for (uint32_t j = cut; j < full; ++j) {
+                const uint32_t n = b0 + (j - cut);
+                if (n < pa.item_cap) pa.items[n] = make_uint4(i, j * it_tiles, (j + 1) * it_tiles, excl + nout);
+                ++nout;
+            }
             const uint32_t slot = atomicAdd(&bucket_pos[31 - __clz(tiles - full * it_tiles)], 1u);
-            if (slot < pa.item_cap) pa.items[slot] = make_uint4(i, full * it_tiles, tiles, excl + full);
+            if (slot < pa.item_cap) pa.items[slot] = make_uint4(i, full * it_tiles, tiles, excl + nout);
+            ++nout;
+            fexcl += full;
         }
-        excl += nit;
+        excl += nout;
     }
     if (tid == 0) {
         *pa.num_items = wsum[32];
@@ -415,6 +479,19 @@ struct SkewCfg<64> {
 };
 
 constexpr uint32_t kEndItem = 0xffffffffu;
+
+#ifdef PRAG_K3_TRACE
+// Debug build only (make EXTRA=-DPRAG_K3_TRACE): per-CTA globaltimer events of
+// K3 -- [0] after pdl_wait, then per item consumed by warp 0: (start, end,
+// tiles), finally the exit time. Read back with prag_gpu_debug_k3_trace.
+constexpr uint32_t kTraceSlots = 256;
+__device__ unsigned long long g_k3_trace[160 * kTraceSlots];
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
 constexpr uint32_t kMinWarpTiles = 4;  // a warp re-reads one tail tile per range: keep ranges >= 4 tiles
 constexpr uint32_t kHeadTiles = 4;     // first tiles of each warp range the producer requests into L2
 
@@ -705,6 +782,11 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
     __syncthreads();
     pdl_wait();  // items, LUTs and thresholds come from the previous kernels
     const uint32_t total = *num_items;
+#ifdef PRAG_K3_TRACE
+    unsigned long long* tr = g_k3_trace + size_t(blockIdx.x) * kTraceSlots;
+    uint32_t ntr = 1;
+    if (threadIdx.x == 0) tr[0] = gtime();
+#endif
 
     // Barrier 1 + b: consumers arrive when done with image buffer b,
     // expanders sync before overwriting it. Barrier 1 + NB: expanders arrive
@@ -853,7 +935,16 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
         const uint32_t b = i % NB;
         mbar_wait(img_full + b, (i / NB) & 1u);
         const ItemSlot sl = slots[b];
-        if (sl.pair == kEndItem) break;
+#ifdef PRAG_K3_TRACE
+        const unsigned long long t_item = gtime();
+#endif
+        if (sl.pair == kEndItem) {
+#ifdef PRAG_K3_TRACE
+            if (warp == 0 && lane == 0 && ntr < kTraceSlots) tr[ntr++] = t_item | (1ull << 63);
+            if (warp == 0 && lane == 0) tr[kTraceSlots - 1] = ntr;
+#endif
+            break;
+        }
         uint32_t a, e_end;
         warp_range<W>(sl, warp, a, e_end);
         if (a < e_end) {
@@ -865,12 +956,25 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
             else
                 scan_range<M, 1>(cx, sl, a, e_end, mk, nk, l2_prefetch);
         }
+#ifdef PRAG_K3_TRACE
+        if (warp == 0 && lane == 0 && ntr + 3 < kTraceSlots) {
+            tr[ntr++] = t_item;
+            tr[ntr++] = gtime();
+            tr[ntr++] = sl.te - sl.tb;
+        }
+#endif
         __syncwarp();
         named_arrive(1 + b, kImgEmptyCount);  // image buffer b is free
     }
 }
 
 }  // namespace
+
+#ifdef PRAG_K3_TRACE
+extern "C" int prag_gpu_debug_k3_trace(unsigned long long* out, size_t n) {
+    return cudaMemcpyFromSymbol(out, g_k3_trace, std::min(n, size_t(160 * kTraceSlots)) * 8) == cudaSuccess ? 0 : 3;
+}
+#endif
 
 uint32_t skew_item_tiles(uint64_t est_tiles, uint32_t grid) {
     // enough items for ~per_cta per CTA, within [kMinItemTiles, kMaxItemTiles]
@@ -899,9 +1003,19 @@ static int check(const char* what) {
 int launch_lut_images(const DeviceIndex& ix, const float* queries, const uint32_t* probe, uint32_t nq,
                       uint32_t nprobe, float* luts, uint32_t it_tiles, uint64_t* scanned, uint4* items,
                       uint32_t* num_items, uint32_t* cursor, uint32_t* q_item_off, uint32_t* gthr,
-                      uint32_t* pair_off, uint64_t item_cap, cudaStream_t s) {
+                      uint32_t* pair_off, uint64_t item_cap, uint32_t scan_grid, cudaStream_t s) {
     const uint32_t npairs = nq * nprobe;
-    const PlanArgs pa{it_tiles, scanned, items, num_items, cursor, q_item_off, gthr, pair_off, item_cap};
+    // tail splitting (register planners only, nq * nprobe <= 2048): off by
+    // default. Measured (tools/item_sweep.py, PRAG_GPU_SPLIT_ITEMS = 0 / 148 /
+    // 296 / 592 split items): config C batch 1 at nprobe 128 / 256 within
+    // +-1%, nprobe 64 -6%, config B nq 64 -3%. The K3 timeline
+    // (tools/k3_trace.py) shows why: CTAs finish within ~8 us of each other
+    // (p10-p90) already; the time goes to the fold itself (warp 0 busy 86% of
+    // the span at config C batch 1), not to the last items.
+    const char* se = getenv("PRAG_GPU_SPLIT_ITEMS");
+    const uint32_t split = se ? uint32_t(atoi(se)) : 0u;
+    (void)scan_grid;
+    const PlanArgs pa{it_tiles, split, scanned, items, num_items, cursor, q_item_off, gthr, pair_off, item_cap};
     // CTA shape (subquantizers x 8*PCH pairs), from tools/sweep_lut.sh:
     // small batches 2 x 8 (enough CTAs to fill the GPU), large ones 2 x 16.
     // The kernel sits near its FP32-pipe bound either way (3 separately
