@@ -86,28 +86,26 @@ struct B1Args {
     uint64_t* o_scanned;
     uint64_t* coarse;          // [G][nprobe]
     unsigned char* images;     // [nprobe][kImgStride]
+    uint4* caux;               // [G][nprobe] per coarse key: {list_len, list_off, skew_off lo, skew_off hi}
     uint32_t* cand_key;        // [G][32]
     uint64_t* cand_id;         // [G][32]
-    unsigned* sync;            // [0] barrier arrivals, [1] barrier generation, [2] finish ticket
+    unsigned* sync;            // [0] barrier arrivals (2 G per launch), [2] finish ticket
 };
 
-// Grid-wide barrier (all CTAs co-resident: cooperative launch). The last
-// arrival resets the count and bumps the generation, so the counters are back
-// to their start state once every barrier of a launch has completed.
-__device__ __forceinline__ void grid_barrier(unsigned* sync) {
+// Grid-wide barrier (all CTAs co-resident: cooperative launch): one
+// monotone arrival counter per launch, barrier n waits for n * G arrivals
+// (one atomic and an acquire-poll, no generation round trip). The CTA that
+// takes the last finish ticket -- after every CTA has passed both barriers --
+// returns the counter to 0 for the next launch.
+__device__ __forceinline__ void grid_barrier(unsigned* count, unsigned target) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        volatile unsigned* gen = sync + 1;
-        const unsigned g = *gen;
         __threadfence();
-        if (atomicAdd(sync, 1u) == gridDim.x - 1) {
-            *reinterpret_cast<volatile unsigned*>(sync) = 0;
-            __threadfence();
-            atomicAdd(sync + 1, 1u);
-        } else {
-            while (*gen == g) __nanosleep(64);
-        }
-        __threadfence();
+        atomicAdd(count, 1u);
+        unsigned v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(count) : "memory");
+        } while (v < target);
     }
     __syncthreads();
 }
@@ -152,6 +150,24 @@ __device__ void bitonic_pairs(uint32_t* key, uint64_t* id, uint32_t n) {
     }
 }
 
+#ifdef PRAG_B1_TRACE
+// Debug build only (make EXTRA=-DPRAG_B1_TRACE): globaltimer at the phase
+// boundaries, per CTA; read back with prag_gpu_debug_b1_trace.
+__device__ unsigned long long g_b1_trace[256 * 16];
+#define B1_MARK(i)                                                                           \
+    do {                                                                                     \
+        if (threadIdx.x == 0) {                                                              \
+            unsigned long long t_;                                                           \
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_));                            \
+            g_b1_trace[blockIdx.x * 16 + (i)] = t_;                                          \
+        }                                                                                    \
+    } while (0)
+#else
+#define B1_MARK(i) \
+    do {           \
+    } while (0)
+#endif
+
 __device__ __forceinline__ uint32_t pow2_ceil(uint32_t x) { return x <= 1 ? 1u : 1u << (32 - __clz(x - 1)); }
 
 template <int M>
@@ -181,9 +197,7 @@ __global__ void __launch_bounds__(kThreads, 1) search1_kernel(const B1Args a) {
         mbar_init(bars + 1, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    for (uint32_t i = tid; i < d; i += kThreads) q_s[i] = a.query[i];
-    __syncthreads();
-
+    B1_MARK(0);
     // ---------------------------------------------------------- 1. coarse
     // The slice's centroids are staged [d/4][chunk] float4 in the (not yet
     // used) image region with coalesced loads, one memory round trip per
@@ -192,11 +206,20 @@ __global__ void __launch_bounds__(kThreads, 1) search1_kernel(const B1Args a) {
     const uint32_t per = (nlist + G - 1) / G;
     const uint32_t c0 = cta * per;
     const uint32_t cn = c0 < nlist ? min(per, nlist - c0) : 0u;
+    // the list metadata the later phases need travels with the coarse keys
+    // (loaded here, in the same round trip as the query and the slice)
+    uint4 my_aux = make_uint4(0, 0, 0, 0);
+    if (tid < cn) {
+        const uint32_t c = c0 + tid;
+        const uint64_t so = a.skew_off[c];
+        my_aux = make_uint4(a.list_len[c], uint32_t(a.list_off[c]), uint32_t(so), uint32_t(so >> 32));
+    }
+    for (uint32_t i = tid; i < d; i += kThreads) q_s[i] = a.query[i];
     {
         float4* stg = reinterpret_cast<float4*>(smem + img_off - L::kGuard);
         const uint32_t d4 = d / 4, chunk = min(uint32_t(kThreads), (L::kImgSpan / 16) / d4);
-        for (uint32_t cb = 0; cb < cn; cb += chunk) {
-            const uint32_t nc = min(chunk, cn - cb);
+        for (uint32_t cb = 0; cb < cn || cb == 0; cb += chunk) {
+            const uint32_t nc = cn > cb ? min(chunk, cn - cb) : 0u;
             for (uint32_t i = tid; i < d4 * nc; i += kThreads) {
                 const uint32_t j4 = i / nc, c = i - j4 * nc;
                 stg[i] = __ldg(a.centroids4 + size_t(j4) * nlist + c0 + cb + c);
@@ -224,10 +247,15 @@ __global__ void __launch_bounds__(kThreads, 1) search1_kernel(const B1Args a) {
         const uint64_t me = skey[tid];
         uint32_t r = 0;
         for (uint32_t i = 0; i < cn; ++i) r += skey[i] < me;
-        if (r < nprobe) a.coarse[size_t(cta) * nprobe + r] = me;
+        if (r < nprobe) {
+            a.coarse[size_t(cta) * nprobe + r] = me;
+            a.caux[size_t(cta) * nprobe + r] = my_aux;
+        }
     }
     for (uint32_t r = cn + tid; r < nprobe; r += kThreads) a.coarse[size_t(cta) * nprobe + r] = ~0ull;
-    grid_barrier(a.sync);
+    B1_MARK(1);
+    grid_barrier(a.sync, G);
+    B1_MARK(2);
 
     // ---------------------------------------------- 2. global top-nprobe
     // U = the nprobe-th smallest list head: the global top-nprobe keys are
@@ -239,9 +267,23 @@ __global__ void __launch_bounds__(kThreads, 1) search1_kernel(const B1Args a) {
         s_u = ~0ull;
         s_n = 0;
     }
-    __syncthreads();
-    // (other CTAs wrote these: read through L2)
-    for (uint32_t b = tid; b < G; b += kThreads) heads[b] = __ldcg(a.coarse + size_t(b) * nprobe);
+    // one pass: every key (and its list metadata) of every CTA's list into
+    // registers; the heads go to SMEM for the bound (other CTAs wrote these:
+    // read through L2)
+    constexpr uint32_t kKpt = (kMaxGrid * kMaxProbe + kThreads - 1) / kThreads;  // keys per thread at most
+    const uint32_t nkeys = G * nprobe;
+    uint64_t kreg[kKpt];
+    uint32_t kidx[kKpt];
+#pragma unroll
+    for (uint32_t u = 0; u < kKpt; ++u) {
+        const uint32_t i = tid + u * kThreads;
+        kidx[u] = i;
+        kreg[u] = i < nkeys ? __ldcg(a.coarse + i) : ~0ull;
+    }
+    __syncthreads();  // s_u / s_n initialised
+#pragma unroll
+    for (uint32_t u = 0; u < kKpt; ++u)
+        if (kidx[u] < nkeys && kidx[u] % nprobe == 0) heads[kidx[u] / nprobe] = kreg[u];
     __syncthreads();
     for (uint32_t b = tid; b < G; b += kThreads) {
         const uint64_t h = heads[b];
@@ -251,23 +293,43 @@ __global__ void __launch_bounds__(kThreads, 1) search1_kernel(const B1Args a) {
     }
     __syncthreads();
     const uint64_t U = s_u;
-    for (uint32_t i = tid; i < G * nprobe; i += kThreads) {
-        const uint64_t x = __ldcg(a.coarse + i);
+    uint32_t* sidx = reinterpret_cast<uint32_t*>(smem + img_off - L::kGuard);  // [kSortCap] key -> its slot
+#pragma unroll
+    for (uint32_t u = 0; u < kKpt; ++u) {
+        const uint64_t x = kreg[u];
         if (x <= U && x != ~0ull) {
             const uint32_t pos = atomicAdd(&s_n, 1u);
-            if (pos < kSortCap) skey[pos] = x;
+            if (pos < kSortCap) {
+                skey[pos] = x;
+                sidx[pos] = kidx[u];
+            }
         }
     }
     __syncthreads();
     const uint32_t nsel = min(s_n, kSortCap);
     const uint32_t npad = pow2_ceil(nsel);
+    // keys are unique: after sorting, the slot of key x is found by a scan of
+    // the unsorted copy (nsel is ~nprobe + a few)
+    uint64_t* sunsorted = reinterpret_cast<uint64_t*>(sidx + kSortCap);
+    for (uint32_t i = tid; i < nsel; i += kThreads) sunsorted[i] = skey[i];
     for (uint32_t i = nsel + tid; i < npad; i += kThreads) skey[i] = ~0ull;
     __syncthreads();
     bitonic64(skey, npad);
+    uint4 paux = make_uint4(0, 0, 0, 0);
     if (tid < nprobe) {
-        const uint32_t list = uint32_t(skey[tid]);
-        probe[tid] = list;
-        plen[tid] = a.list_len[list];
+        const uint64_t me = skey[tid];
+        uint32_t slot = 0;
+        for (uint32_t i = 0; i < nsel; ++i)
+            if (sunsorted[i] == me) slot = sidx[i];
+        paux = __ldcg(a.caux + slot);
+        probe[tid] = uint32_t(me);
+        plen[tid] = paux.x;
+    }
+    uint32_t* plo = reinterpret_cast<uint32_t*>(stash);  // [kMaxProbe] list_off (stash is free until the scan)
+    uint64_t* pso = reinterpret_cast<uint64_t*>(plo + kMaxProbe);  // [kMaxProbe] skew_off
+    if (tid < nprobe) {
+        plo[tid] = paux.y;
+        pso[tid] = uint64_t(paux.z) | (uint64_t(paux.w) << 32);
     }
     __syncthreads();
     if (warp == 0) {  // entry-tile prefix over the probed lists, scanned_vectors
@@ -305,13 +367,14 @@ __global__ void __launch_bounds__(kThreads, 1) search1_kernel(const B1Args a) {
             const uint32_t lo = max(g0, toff[p]), hi = min(g1, toff[p + 1]);
             if (lo >= hi) continue;
             if (warp == seen % kWarps && lane == 0) {
-                const unsigned char* src = a.skew_codes + (a.skew_off[probe[p]] + (lo - toff[p])) * (32ull * M);
+                const unsigned char* src = a.skew_codes + (pso[p] + (lo - toff[p])) * (32ull * M);
                 prefetch_l2(src, (hi - lo + 1) * 32u * M);
             }
             ++seen;
         }
     }
 
+    B1_MARK(3);
     // ------------------------------------------------ 3. ADC table images
     // rows (probe p, code) split over the CTAs in contiguous chunks; the
     // residuals q - c_list of the chunk's probes are staged in SMEM (stride
@@ -379,7 +442,9 @@ __global__ void __launch_bounds__(kThreads, 1) search1_kernel(const B1Args a) {
     }
     // the images are read by other CTAs' bulk copies (the async proxy)
     asm volatile("fence.proxy.async.global;" ::: "memory");
-    grid_barrier(a.sync);
+    B1_MARK(4);
+    grid_barrier(a.sync, 2 * G);
+    B1_MARK(5);
 
     // ------------------------------------------------------------- 4. scan
     float mk[32], nk[32];
@@ -435,8 +500,8 @@ __global__ void __launch_bounds__(kThreads, 1) search1_kernel(const B1Args a) {
         const uint32_t wper = (ntile + nw - 1) / nw;
         const uint32_t wa = lo + warp * wper, we = min(hi, wa + wper);
         const bool active = warp < nw && wa < we;
-        const uint32_t list = probe[p], len = plen[p];
-        const unsigned char* src_lane = a.skew_codes + a.skew_off[list] * (32ull * M) + lane * 16;
+        const uint32_t len = plen[p];
+        const unsigned char* src_lane = a.skew_codes + pso[p] * (32ull * M) + lane * 16;
         uint4 A[M / 16], B[M / 16];
         if (active) {
             load_tile<M>(A, src_lane, wa);
@@ -445,7 +510,7 @@ __global__ void __launch_bounds__(kThreads, 1) search1_kernel(const B1Args a) {
         mbar_wait(bars + b, phase[b]);
         phase[b] ^= 1u;
         if (active) {
-            const uint32_t lbase = uint32_t(a.list_off[list]);
+            const uint32_t lbase = plo[p];
             float cur = 0.0f, prev = 0.0f;
             for (uint32_t j = wa;; j += 2) {
                 if (b == 0)
@@ -484,6 +549,7 @@ __global__ void __launch_bounds__(kThreads, 1) search1_kernel(const B1Args a) {
             ++nseg;
         }
     }
+    B1_MARK(6);
     // CTA top-k: k rounds of the smallest (key, id) among the warp list heads
     stash[warp * 64 + lane] = lane < k ? t.key : 0xffffffffu;
     stash[warp * 64 + 32 + lane] = t.pos;
@@ -532,26 +598,41 @@ __global__ void __launch_bounds__(kThreads, 1) search1_kernel(const B1Args a) {
         s_last = atomicAdd(a.sync + 2, 1u) == G - 1;
     }
     __syncthreads();
+    B1_MARK(7);
     if (!s_last) return;
     __threadfence();
     if (tid == 0) {
-        a.sync[2] = 0;  // ticket back to its start state
+        a.sync[2] = 0;  // ticket and barrier counter back to their start state
+        a.sync[0] = 0;  // (every CTA has passed both barriers: it took a ticket)
         s_n = 0;
     }
-    // U2 = the k-th smallest CTA head by (distance, id); keep what is <= U2
+    // one pass over the k meaningful slots of every CTA's list (sorted by
+    // (distance, id)); U2 = the k-th smallest CTA head; keep what is <= U2
     __shared__ uint32_t s_uk;
     __shared__ uint64_t s_uid;
     if (tid == 0) {
         s_uk = 0xffffffffu;
         s_uid = ~0ull;
     }
-    __syncthreads();
-    const uint32_t* ck = a.cand_key;
-    const uint64_t* ci = a.cand_id;
+    constexpr uint32_t kCpt = (kMaxGrid * 32 + kThreads - 1) / kThreads;
+    const uint32_t ncand = G * k;
+    uint32_t ckr[kCpt];
+    uint64_t cir[kCpt];
+#pragma unroll
+    for (uint32_t u = 0; u < kCpt; ++u) {
+        const uint32_t i = tid + u * kThreads;
+        const uint32_t b = i / k, j = i - b * k;
+        ckr[u] = i < ncand ? __ldcg(a.cand_key + b * 32 + j) : 0xffffffffu;
+        cir[u] = i < ncand ? __ldcg(a.cand_id + b * 32 + j) : ~0ull;
+    }
     uint32_t* hkey = probe;  // probe info is no longer needed: [G] head keys, ids in `heads`
-    for (uint32_t b = tid; b < G; b += kThreads) {
-        hkey[b] = __ldcg(ck + b * 32);
-        heads[b] = __ldcg(ci + b * 32);
+#pragma unroll
+    for (uint32_t u = 0; u < kCpt; ++u) {
+        const uint32_t i = tid + u * kThreads;
+        if (i < ncand && i % k == 0) {
+            hkey[i / k] = ckr[u];
+            heads[i / k] = cir[u];
+        }
     }
     __syncthreads();
     for (uint32_t b = tid; b < G; b += kThreads) {
@@ -571,9 +652,10 @@ __global__ void __launch_bounds__(kThreads, 1) search1_kernel(const B1Args a) {
     __syncthreads();
     const uint32_t uk = s_uk;
     const uint64_t uid = s_uid;
-    for (uint32_t i = tid; i < G * 32; i += kThreads) {
-        const uint32_t x = __ldcg(ck + i);
-        const uint64_t xi = __ldcg(ci + i);
+#pragma unroll
+    for (uint32_t u = 0; u < kCpt; ++u) {
+        const uint32_t x = ckr[u];
+        const uint64_t xi = cir[u];
         if (x != 0xffffffffu && (x < uk || (x == uk && xi <= uid))) {
             const uint32_t pos = atomicAdd(&s_n, 1u);
             if (pos < kFinalCap) {
@@ -600,6 +682,7 @@ __global__ void __launch_bounds__(kThreads, 1) search1_kernel(const B1Args a) {
         *a.o_count = count;
         if (a.o_scanned) *a.o_scanned = scanned;
     }
+    B1_MARK(8);
 }
 
 }  // namespace
@@ -614,6 +697,12 @@ static bool batch1_enabled() {
     return e != nullptr && e[0] == '1';
 }
 
+#ifdef PRAG_B1_TRACE
+extern "C" int prag_gpu_debug_b1_trace(unsigned long long* out, size_t n) {
+    return cudaMemcpyFromSymbol(out, g_b1_trace, (n < 256 * 16 ? n : 256 * 16) * 8) == cudaSuccess ? 0 : 3;
+}
+#endif
+
 bool search1_eligible(const DeviceIndex& d, uint32_t nq, uint32_t nprobe, uint32_t k, int sms) {
     return nq == 1 && d.code_layout == 1 && (d.nsq == 32 || d.nsq == 64) && d.centroids4 && d.codewords &&
            d.d % 4 == 0 && k >= 1 && k <= 32 && nprobe >= 1 &&
@@ -626,6 +715,7 @@ size_t search1_scratch_bytes(const DeviceIndex& d, uint32_t nprobe, int grid) {
     Carver c{nullptr};
     c.take<uint64_t>(size_t(grid) * nprobe);
     c.take<unsigned char>(size_t(nprobe) * stride);
+    c.take<uint4>(size_t(grid) * nprobe);
     c.take<uint32_t>(size_t(grid) * 32);
     c.take<uint64_t>(size_t(grid) * 32);
     return c.off + 256;
@@ -657,6 +747,7 @@ int launch_search1(const DeviceIndex& d, const float* dq, uint32_t nprobe, uint3
     a.o_scanned = o_scanned;
     a.coarse = c.take<uint64_t>(size_t(grid) * nprobe);
     a.images = c.take<unsigned char>(size_t(nprobe) * stride);
+    a.caux = c.take<uint4>(size_t(grid) * nprobe);
     a.cand_key = c.take<uint32_t>(size_t(grid) * 32);
     a.cand_id = c.take<uint64_t>(size_t(grid) * 32);
     a.sync = sync;
