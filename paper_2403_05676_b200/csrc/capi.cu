@@ -667,6 +667,126 @@ static int any_pass(prag_gpu_index* ix, Workspace* w, const float* dq, uint32_t 
     return search_pass(ix, w, dq, nq, nprobe, k, o_ids, o_dist, o_count, o_scanned, s, tm, rerank);
 }
 
+void free_host_plan(HostPlan* h) {
+    if (!h) return;
+    if (h->plan) prag_gpu_plan_free(h->plan);
+    cudaFree(h->dq);
+    cudaFree(h->dout);
+    cudaFreeHost(h->hout);
+    delete h;
+}
+
+// Small host-buffer searches (nq <= kHostPlanMaxNq: GpuRetriever's batch-1
+// retrieve) replay a captured plan per (nq, nprobe, k, stream) shape: one H2D
+// copy, one graph launch, one D2H copy of the four outputs, instead of the
+// chain's kernel launches. Measured (tools/host_path_time.py, config B, wall
+// clock per call): batch 1 at nprobe 1 / 16 / 128 48 / 57 / 85 us with the
+// plan vs 56 / 57 / 93 us without; nq 16 / 64 slower with the plan (122 vs
+// 108, 206 vs 203 us: the graph loses the PDL overlap the direct launches
+// keep), so larger batches take the direct path. Up to kHostPlans shapes per
+// index are kept (least recently used evicted). Returns -1 when the call
+// should take the ordinary path (a larger batch, another call holds the
+// shape's plan, profiling, a sharded handle, or PRAG_GPU_HOST_PLANS=0).
+constexpr size_t kHostPlans = 8;
+constexpr uint32_t kHostPlanMaxNq = 4;
+
+int host_plan_search(prag_gpu_index* ix, const float* queries, uint32_t nq, uint32_t nprobe, uint32_t k,
+                     uint64_t* out_ids, float* out_dist, uint32_t* out_count, uint64_t* out_scanned,
+                     cudaStream_t s) {
+    static const bool enabled = [] {
+        const char* e = getenv("PRAG_GPU_HOST_PLANS");
+        return !(e && e[0] == '0');
+    }();
+    if (!enabled || nq > kHostPlanMaxNq || ix->profiling || ix->is_group() || ix->comm ||
+        pass_chunk(ix, nq, nprobe, k, false) < nq)
+        return -1;
+    static std::atomic<uint64_t> clock{0};
+    HostPlan* hp = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(ix->mu);
+        for (HostPlan* h : ix->host_plans)
+            if (h->nq == nq && h->nprobe == nprobe && h->k == k && h->stream == s) {
+                if (h->busy) return -1;
+                hp = h;
+                break;
+            }
+        if (hp) hp->busy = true;
+    }
+    const DeviceIndex& d = ix->dev;
+    Carver c{nullptr};
+    c.take<uint64_t>(size_t(nq) * k);
+    c.take<float>(size_t(nq) * k);
+    c.take<uint32_t>(nq);
+    c.take<uint64_t>(nq);
+    const size_t out_bytes = c.off;
+    auto carve = [&](char* base, uint64_t** i, float** dd, uint32_t** cnt, uint64_t** sc) {
+        Carver v{base};
+        *i = v.take<uint64_t>(size_t(nq) * k);
+        *dd = v.take<float>(size_t(nq) * k);
+        *cnt = v.take<uint32_t>(nq);
+        *sc = v.take<uint64_t>(nq);
+    };
+    if (!hp) {  // build the shape's plan (an ordinary pass, then its capture)
+        auto h = std::make_unique<HostPlan>();
+        h->nq = nq, h->nprobe = nprobe, h->k = k, h->stream = s, h->out_bytes = out_bytes;
+        struct Guard {
+            std::unique_ptr<HostPlan>& h;
+            ~Guard() {
+                if (h) free_host_plan(h.release());
+            }
+        } guard{h};
+        PG_CUDA(cudaMalloc(&h->dq, size_t(nq) * d.d * 4));
+        PG_CUDA(cudaMalloc(&h->dout, out_bytes));
+        PG_CUDA(cudaMallocHost(&h->hout, out_bytes));
+        PG_CUDA(cudaMemcpyAsync(h->dq, queries, size_t(nq) * d.d * 4, cudaMemcpyHostToDevice, s));
+        uint64_t *i, *sc;
+        float* dd;
+        uint32_t* cnt;
+        carve(h->dout, &i, &dd, &cnt, &sc);
+        PG_TRY(prag_gpu_plan_create(ix, h->dq, nq, nprobe, k, i, dd, cnt, sc, s, &h->plan));
+        h->busy = true;
+        HostPlan* evict = nullptr;
+        {
+            std::lock_guard<std::mutex> lk(ix->mu);
+            if (ix->host_plans.size() >= kHostPlans) {
+                auto it = std::min_element(ix->host_plans.begin(), ix->host_plans.end(), [](HostPlan* a, HostPlan* b) {
+                    return (a->busy ? UINT64_MAX : a->last_use) < (b->busy ? UINT64_MAX : b->last_use);
+                });
+                if (!(*it)->busy) {
+                    evict = *it;
+                    ix->host_plans.erase(it);
+                }
+            }
+            hp = h.release();
+            ix->host_plans.push_back(hp);
+        }
+        if (evict) free_host_plan(evict);
+    } else {
+        PG_CUDA(cudaMemcpyAsync(hp->dq, queries, size_t(nq) * d.d * 4, cudaMemcpyHostToDevice, s));
+    }
+    struct Release {
+        prag_gpu_index* ix;
+        HostPlan* hp;
+        ~Release() {
+            std::lock_guard<std::mutex> lk(ix->mu);
+            hp->busy = false;
+            hp->last_use = ++clock;
+        }
+    } rel{ix, hp};
+    PG_TRY(prag_gpu_plan_launch(hp->plan, s));
+    PG_CUDA(cudaMemcpyAsync(hp->hout, hp->dout, out_bytes, cudaMemcpyDeviceToHost, s));
+    PG_CUDA(cudaStreamSynchronize(s));
+    uint64_t *hi, *hs;
+    float* hd;
+    uint32_t* hc;
+    carve(hp->hout, &hi, &hd, &hc, &hs);
+    std::memcpy(out_ids, hi, size_t(nq) * k * 8);
+    std::memcpy(out_dist, hd, size_t(nq) * k * 4);
+    std::memcpy(out_count, hc, size_t(nq) * 4);
+    if (out_scanned) std::memcpy(out_scanned, hs, size_t(nq) * 8);
+    return PRAG_GPU_OK;
+}
+
 int do_search(prag_gpu_index* ix, const float* queries, uint32_t nq, uint32_t nprobe, uint32_t k,
               uint64_t* out_ids, float* out_dist, uint32_t* out_count, uint64_t* out_scanned, cudaStream_t s,
               bool rerank, bool all_device) {
@@ -689,6 +809,10 @@ int do_search(prag_gpu_index* ix, const float* queries, uint32_t nq, uint32_t np
     const bool o_dev = all_device || (is_device_ptr(out_ids) && is_device_ptr(out_dist) && is_device_ptr(out_count) &&
                                       (out_scanned == nullptr || is_device_ptr(out_scanned)));
     const uint32_t chunk = pass_chunk(ix, nq, nprobe, k, rerank);
+    if (!q_dev && !o_dev && !rerank) {
+        const int rc = host_plan_search(ix, queries, nq, nprobe, k, out_ids, out_dist, out_count, out_scanned, s);
+        if (rc >= 0) return rc;
+    }
 
     Workspace* w = acquire_ws(ix, s);
     struct Rel {
@@ -1025,6 +1149,8 @@ void prag_gpu_index_free(prag_gpu_index* ix) {
     {
         DeviceGuard g(ix->device);
         cudaDeviceSynchronize();
+        for (HostPlan* h : ix->host_plans) free_host_plan(h);
+        ix->host_plans.clear();
         for (Workspace* w : ix->pool) free_ws(w);
         free_device_index(ix->dev);
         cudaFree(ix->emb);

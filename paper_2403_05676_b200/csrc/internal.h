@@ -168,6 +168,20 @@ struct Workspace {
     unsigned long long* win_stat = nullptr;  // profiling: sum of K1b window sizes
 };
 
+// A captured search over fixed device buffers, serving prag_gpu_search calls
+// with host queries and outputs of one (nq, nprobe, k, stream) shape.
+struct HostPlan {
+    uint32_t nq = 0, nprobe = 0, k = 0;
+    cudaStream_t stream = nullptr;
+    prag_gpu_plan* plan = nullptr;
+    float* dq = nullptr;         // [nq][d]
+    char* dout = nullptr;        // ids | dist | count | scanned (Carver offsets)
+    char* hout = nullptr;        // pinned copy of dout
+    size_t out_bytes = 0;
+    bool busy = false;
+    uint64_t last_use = 0;
+};
+
 struct SearchPlanSizes {
     uint32_t nq_chunk;     // queries per pass
     uint64_t cand_cap;     // candidate slots per pass
@@ -206,6 +220,8 @@ struct prag_gpu_index {
     // multi-process: this shard is rank comm->rank of a distributed index;
     // prag_gpu_search on it is collective (NCCL all-gather + merge)
     prag_gpu_comm* comm = nullptr;
+    // host-buffer searches replayed as captured plans (capi.cu host_plan_search)
+    std::vector<pg::HostPlan*> host_plans;
     bool is_group() const { return !shards.empty(); }
 };
 
