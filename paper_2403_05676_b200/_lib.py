@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libprag_gpu.so")
+LIB_PATH = os.environ.get("PRAG_GPU_LIB") or os.path.join(HERE, "libprag_gpu.so")  # override: A/B builds in tools/
 
 OK, CONFIG, FORMAT, CUDA, NCCL, OOM, NO_DEVICE = range(7)
 

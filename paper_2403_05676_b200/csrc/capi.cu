@@ -1838,3 +1838,19 @@ int prag_gpu_last_timings(const prag_gpu_index* ix, prag_gpu_timings* out) {
 }
 
 }  // extern "C"
+
+#ifdef PRAG_CHAIN_TRACE
+// Debug build only: op 0 zeroes the chain trace (allocating it on first use),
+// op 1 copies its pg::kChainWords values to `out` (see internal.h).
+extern "C" int prag_gpu_debug_chain_trace(int op, unsigned long long* out) {
+    static unsigned long long* buf = nullptr;
+    if (!buf) {
+        if (cudaMalloc(&buf, pg::kChainWords * 8) != cudaSuccess) return 3;
+        pg::ct_bind_coarse(buf);
+        pg::ct_bind_skew(buf);
+        pg::ct_bind_kernels(buf);
+    }
+    if (op == 0) return cudaMemset(buf, 0, pg::kChainWords * 8) == cudaSuccess ? 0 : 3;
+    return cudaMemcpy(out, buf, pg::kChainWords * 8, cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 3;
+}
+#endif

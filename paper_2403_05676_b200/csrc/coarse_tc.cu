@@ -141,6 +141,7 @@ __global__ void __launch_bounds__(128, 1) coarse_tc_kernel(const float* __restri
                                                            const float* __restrict__ queries, uint32_t nq,
                                                            uint32_t nlist, uint32_t d, uint32_t n_tile,
                                                            float* __restrict__ partial) {
+    CT_BEGIN;
     extern __shared__ __align__(1024) unsigned char sm[];
     const uint32_t N = n_tile;                                // multiple of 8, <= kTcMaxN
     const uint32_t kA = 2 * kTcRows * kTcKBlock * 4;          // one K block of A, hi + lo: 32 KiB
@@ -174,6 +175,7 @@ __global__ void __launch_bounds__(128, 1) coarse_tc_kernel(const float* __restri
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     pdl_wait();
+    CT_WAITED(0);
     // B: element (n, k) of a part at (k/4) * (N * 16) + (n/8) * 128 + (n%8) * 16 + (k%4) * 4,
     // so the 4 consecutive k of one float4 are one 16-byte store. Lane = float4
     // of the row (nkb * 8 <= 24 lanes busy), warp w takes rows w, w + 4, ...
@@ -260,6 +262,7 @@ __global__ void __launch_bounds__(128, 1) coarse_tc_kernel(const float* __restri
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols));
+    CT_END(0);
 }
 
 // ------------------------------------------------------------------ K1b
@@ -408,6 +411,7 @@ __global__ void __launch_bounds__(kWinThreads) select_window_kernel(
     const float* __restrict__ centroids, const float* __restrict__ queries, uint32_t nq, uint32_t nlist, uint32_t d,
     uint32_t nprobe, uint32_t* __restrict__ probe, float* __restrict__ probe_dist,
     unsigned long long* __restrict__ win_stat, uint32_t kStageRows) {
+    CT_BEGIN;
     extern __shared__ __align__(1024) unsigned char sm[];
     uint32_t* hist = reinterpret_cast<uint32_t*>(sm);          // [256]
     uint32_t* misc = hist + 256;                               // [8]: [1] rank, [2..3] selected key, [4] count, [5..7] two-level U
@@ -438,6 +442,7 @@ __global__ void __launch_bounds__(kWinThreads) select_window_kernel(
     for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
     if ((tid & 31) == 0) red[tid >> 5] = part;
     pdl_wait();
+    CT_WAITED(1);
     // q.c: sum of K1's slices in slice order; up to ZB slices' loads are
     // issued together before the first add
     float dot[VPT];
@@ -642,9 +647,14 @@ __global__ void __launch_bounds__(kWinThreads) select_window_kernel(
             probe_dist[size_t(q) * nprobe + r] = di;
         }
     }
+    CT_END(1);
 }
 
 }  // namespace
+
+#ifdef PRAG_CHAIN_TRACE
+CT_BIND_FN(ct_bind_coarse)
+#endif
 
 // rows per rescoring batch: up to kStageRowsMax while the double-buffered
 // staging fits the 227 KiB opt-in (more rows fold in parallel for large nprobe)

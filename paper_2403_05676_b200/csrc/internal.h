@@ -25,6 +25,52 @@ namespace pg {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// Chain trace (debug build only: make EXTRA=-DPRAG_CHAIN_TRACE). Per kernel
+// of the search chain, per CTA (< kChainCtas) and warp: the CTA's start, the
+// warp's PDL-wait return and the warp's end, as globaltimer values in plain
+// stores (no atomics: the trace must not serialise the kernels it times);
+// tools/chain_trace.py reads them back with prag_gpu_debug_chain_trace. Ids:
+// 0 K1, 1 K1b, 2 K2, 3 planner CTA, 4 K3, 5 K4.
+#ifdef PRAG_CHAIN_TRACE
+constexpr int kChainKernels = 6;
+constexpr uint32_t kChainCtas = 8192, kChainWarps = 32;
+constexpr size_t kChainWords = size_t(kChainKernels) * kChainCtas * kChainWarps * 3;
+static __constant__ unsigned long long* c_chain;
+__device__ __forceinline__ unsigned long long ct_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ unsigned long long* ct_slot(int k) {
+    const uint32_t cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    if (cta >= kChainCtas || (threadIdx.x & 31u) != 0) return nullptr;
+    return c_chain + ((size_t(k) * kChainCtas + cta) * kChainWarps + (threadIdx.x >> 5)) * 3;
+}
+#define CT_BEGIN const unsigned long long ct_t0 = ::pg::ct_now()
+#define CT_WAITED(k)                                          \
+    do {                                                      \
+        unsigned long long* p_ = ::pg::ct_slot(k);            \
+        if (p_) {                                             \
+            p_[0] = ct_t0;                                    \
+            p_[1] = ::pg::ct_now();                           \
+        }                                                     \
+    } while (0)
+#define CT_END(k)                                             \
+    do {                                                      \
+        unsigned long long* p_ = ::pg::ct_slot(k);            \
+        if (p_) p_[2] = ::pg::ct_now();                       \
+    } while (0)
+#define CT_BIND_FN(name) \
+    void name(void* p) { cudaMemcpyToSymbol(c_chain, &p, sizeof(p)); }
+void ct_bind_coarse(void* p);
+void ct_bind_skew(void* p);
+void ct_bind_kernels(void* p);
+#else
+#define CT_BEGIN
+#define CT_WAITED(k)
+#define CT_END(k)
+#endif
+
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                        Args&&... args) {

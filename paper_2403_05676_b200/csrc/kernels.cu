@@ -614,8 +614,10 @@ __global__ void __launch_bounds__(kPoolThreads) select_pool_kernel(
     __shared__ uint32_t vkey[kPoolCap];
     __shared__ uint64_t vid[kPoolCap];
     __shared__ uint32_t nsurv;
+    CT_BEGIN;
     const uint32_t q = blockIdx.x, tid = threadIdx.x, lane = tid & 31u;
     pdl_wait();  // the pool (and its offsets, from the planner) come from earlier kernels
+    CT_WAITED(5);
     const size_t off = size_t(q_item_off[q]) * k;
     const uint32_t n = (q_item_off[q + 1] - q_item_off[q]) * k;
     const uint32_t total = uint32_t(min(scanned[q], uint64_t(k)));
@@ -648,7 +650,10 @@ __global__ void __launch_bounds__(kPoolThreads) select_pool_kernel(
         }
     }
     __syncthreads();
-    if (tid >= 32) return;
+    if (tid >= 32) {
+        CT_END(5);
+        return;
+    }
     const uint32_t c = nsurv;
     const bool from_smem = c <= kPoolCap;
     const uint32_t m = from_smem ? c : n;
@@ -689,9 +694,14 @@ __global__ void __launch_bounds__(kPoolThreads) select_pool_kernel(
         out_ids[size_t(q) * k + lane] = lid;
     }
     if (lane == 0) out_count[q] = total;
+    CT_END(5);
 }
 
 }  // namespace
+
+#ifdef PRAG_CHAIN_TRACE
+CT_BIND_FN(ct_bind_kernels)
+#endif
 
 int launch_select_pool(const uint32_t* pool_key, const uint64_t* pool_id, const uint64_t* scanned,
                        const uint32_t* q_item_off, const uint32_t* gthr, uint32_t nq, uint32_t k, uint64_t* out_ids,

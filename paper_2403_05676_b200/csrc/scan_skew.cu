@@ -72,9 +72,10 @@ constexpr uint32_t image_floats() {
 }
 
 // Work items for the fast path: per (q, p) pair, ceil(len/32) tiles cut into
-// items of <= it_tiles tiles, emitted largest-first (log2 size buckets) so
-// the big lists set each query's threshold early and the small ones fill the
-// tail. q_item_off[q] = prefix of per-query item counts (candidate-pool
+// items of <= it_tiles tiles, emitted largest-first (a counting sort on the
+// item's tile count) so the big lists set each query's threshold early, the
+// small ones fill the tail, and the persistent CTAs, which pull items a few
+// ahead of scanning them, finish together. q_item_off[q] = prefix of per-query item counts (candidate-pool
 // offsets). Also resets the per-query threshold and pool counters, and
 // writes scanned_vectors (annindex.hpp:305: the sum of probed list sizes).
 struct PlanArgs {
@@ -97,6 +98,47 @@ struct PlanArgs {
 // in a smaller size bucket, i.e. at the end of the queue ("guided" tail).
 constexpr uint32_t kSplit = 4;
 
+// pos[b] = sum of cnt[b'] over b' > b (b < nb): bucket start positions with
+// the largest bucket first. Called by the whole block; ends synchronised.
+__device__ __forceinline__ void desc_positions(const uint32_t* cnt, uint32_t* pos, uint32_t nb, uint32_t* ws) {
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, w = tid >> 5, nw = blockDim.x >> 5;
+    const uint32_t per = (nb + blockDim.x - 1) / blockDim.x;  // reversed buckets [tid*per, +per) per thread
+    __syncthreads();  // counts complete
+    uint32_t local = 0;
+    for (uint32_t j = 0; j < per; ++j) {
+        const uint32_t r = tid * per + j;
+        if (r < nb) local += cnt[nb - 1 - r];
+    }
+    uint32_t incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= uint32_t(o)) incl += t;
+    }
+    if (lane == 31) ws[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+        const uint32_t x = lane < nw ? ws[lane] : 0u;
+        uint32_t xi = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, xi, o);
+            if (lane >= uint32_t(o)) xi += t;
+        }
+        if (lane < nw) ws[lane] = xi - x;
+    }
+    __syncthreads();
+    uint32_t run = ws[w] + incl - local;
+    for (uint32_t j = 0; j < per; ++j) {
+        const uint32_t r = tid * per + j;
+        if (r < nb) {
+            pos[nb - 1 - r] = run;
+            run += cnt[nb - 1 - r];
+        }
+    }
+    __syncthreads();
+}
+
 // plan_items for up to R pairs per thread (P <= R * blockDim.x): thread t
 // owns pairs [t*R, t*R + R), so every probe[] / list_len[] load is issued up
 // front (two dependent rounds in all), the pair-order prefix is one serial
@@ -106,10 +148,11 @@ template <int R>
 __device__ __noinline__ void plan_items_regs(const uint32_t* __restrict__ probe, const uint32_t* __restrict__ list_len,
                                              uint32_t nq, uint32_t nprobe, const PlanArgs pa) {
     const uint32_t it_tiles = pa.it_tiles;
-    __shared__ uint32_t wsum[33];
-    __shared__ uint32_t bucket_cnt[32], bucket_pos[32];
+    __shared__ uint32_t wsum[33], bws[33];
+    __shared__ uint32_t bucket_cnt[kMaxItemTiles + 1], bucket_pos[kMaxItemTiles + 1];
     const uint32_t P = nq * nprobe, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    if (tid < 32) bucket_cnt[tid] = 0;
+    const uint32_t nb = it_tiles + 1;  // one bucket per item size (tiles)
+    for (uint32_t b = tid; b < nb; b += blockDim.x) bucket_cnt[b] = 0;
     for (uint32_t q = tid; q < nq; q += blockDim.x) {
         pa.scanned[q] = 0;
         pa.gthr[q] = 0xffffffffu;
@@ -170,9 +213,9 @@ __device__ __noinline__ void plan_items_regs(const uint32_t* __restrict__ probe,
             if (nit) {  // nit - 1 full items (the first `split - fexcl` of them cut), then the remainder
                 const uint32_t full = nit - 1;
                 const uint32_t cut = fexcl < split ? min(full, split - fexcl) : 0u;
-                if (full > cut) atomicAdd(&bucket_cnt[31 - __clz(it_tiles)], full - cut);
-                if (cut) atomicAdd(&bucket_cnt[31 - __clz(sub_tiles)], cut * kSplit);
-                atomicAdd(&bucket_cnt[31 - __clz(tiles - full * it_tiles)], 1u);
+                if (full > cut) atomicAdd(&bucket_cnt[it_tiles], full - cut);
+                if (cut) atomicAdd(&bucket_cnt[sub_tiles], cut * kSplit);
+                atomicAdd(&bucket_cnt[tiles - full * it_tiles], 1u);
                 mine += nit + cut * (kSplit - 1);
                 fexcl += full;
             }
@@ -199,13 +242,7 @@ __device__ __noinline__ void plan_items_regs(const uint32_t* __restrict__ probe,
         if (lane < nw) wsum[lane] = xi - x;
         if (lane == nw - 1) wsum[32] = xi;
     }
-    if (tid == 0) {
-        uint32_t pos = 0;
-        for (int bkt = 31; bkt >= 0; --bkt) {
-            bucket_pos[bkt] = pos;
-            pos += bucket_cnt[bkt];
-        }
-    }
+    desc_positions(bucket_cnt, bucket_pos, nb, bws);
     __syncthreads();
     uint32_t excl = wsum[w] + incl - mine;
     uint32_t fexcl = fexcl0;
@@ -222,20 +259,20 @@ __device__ __noinline__ void plan_items_regs(const uint32_t* __restrict__ probe,
             const uint32_t full = nit - 1;
             const uint32_t cut = fexcl < split ? min(full, split - fexcl) : 0u;
             // the first `cut` full items in kSplit pieces (the queue's tail)
-            const uint32_t c0 = cut ? atomicAdd(&bucket_pos[31 - __clz(sub_tiles)], cut * kSplit) : 0u;
+            const uint32_t c0 = cut ? atomicAdd(&bucket_pos[sub_tiles], cut * kSplit) : 0u;
             for (uint32_t j = 0; j < cut; ++j)
                 for (uint32_t h = 0; h < kSplit; ++h) {
                     const uint32_t tb = j * it_tiles + h * sub_tiles, n = j * kSplit + h;
                     if (c0 + n < pa.item_cap) pa.items[c0 + n] = make_uint4(i, tb, tb + sub_tiles, excl + n);
                 }
             nout = cut * kSplit;
-            const uint32_t b0 = full > cut ? atomicAdd(&bucket_pos[31 - __clz(it_tiles)], full - cut) : 0u;
+            const uint32_t b0 = full > cut ? atomicAdd(&bucket_pos[it_tiles], full - cut) : 0u;
             for (uint32_t j = cut; j < full; ++j) {
                 const uint32_t n = b0 + (j - cut);
                 if (n < pa.item_cap) pa.items[n] = make_uint4(i, j * it_tiles, (j + 1) * it_tiles, excl + nout);
                 ++nout;
             }
-            const uint32_t slot = atomicAdd(&bucket_pos[31 - __clz(tiles - full * it_tiles)], 1u);
+            const uint32_t slot = atomicAdd(&bucket_pos[tiles - full * it_tiles], 1u);
             if (slot < pa.item_cap) pa.items[slot] = make_uint4(i, full * it_tiles, tiles, excl + nout);
             ++nout;
             fexcl += full;
@@ -262,10 +299,11 @@ __device__ __noinline__ void plan_items(const uint32_t* __restrict__ probe, cons
     uint32_t* __restrict__ gthr = pa.gthr;
     uint32_t* __restrict__ pair_off = pa.pair_off;
     const uint64_t item_cap = pa.item_cap;
-    __shared__ uint32_t tmp[33];
-    __shared__ uint32_t bucket_cnt[32], bucket_pos[32];
+    __shared__ uint32_t tmp[33], bws[33];
+    __shared__ uint32_t bucket_cnt[kMaxItemTiles + 1], bucket_pos[kMaxItemTiles + 1];
     const uint32_t P = nq * nprobe;
-    if (threadIdx.x < 32) bucket_cnt[threadIdx.x] = 0;
+    const uint32_t nb = it_tiles + 1;  // one bucket per item size (tiles)
+    for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) bucket_cnt[b] = 0;
     for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x) scanned[q] = 0;
     __syncthreads();
     // pass 1: per-query item counts (prefix) and bucket histogram
@@ -279,7 +317,7 @@ __device__ __noinline__ void plan_items(const uint32_t* __restrict__ probe, cons
         const uint32_t nit = (tiles + it_tiles - 1) / it_tiles;
         for (uint32_t j = 0; j < nit; ++j) {
             const uint32_t t = min(tiles, (j + 1) * it_tiles) - j * it_tiles;
-            atomicAdd(&bucket_cnt[31 - __clz(t)], 1u);
+            atomicAdd(&bucket_cnt[t], 1u);
         }
         const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
         uint32_t incl = nit;
@@ -308,15 +346,8 @@ __device__ __noinline__ void plan_items(const uint32_t* __restrict__ probe, cons
         carry += tmp[32];
         __syncthreads();
     }
-    // bucket start positions, largest bucket first
-    if (threadIdx.x == 0) {
-        uint32_t pos = 0;
-        for (int bkt = 31; bkt >= 0; --bkt) {
-            bucket_pos[bkt] = pos;
-            pos += bucket_cnt[bkt];
-        }
-    }
-    __syncthreads();
+    // bucket start positions, largest item first
+    desc_positions(bucket_cnt, bucket_pos, nb, bws);
     // pass 2: scatter items
     for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) {
         const uint32_t len = list_len[probe[i]];
@@ -324,7 +355,7 @@ __device__ __noinline__ void plan_items(const uint32_t* __restrict__ probe, cons
         const uint32_t nit = (tiles + it_tiles - 1) / it_tiles;
         for (uint32_t j = 0; j < nit; ++j) {
             const uint32_t te = min(tiles, (j + 1) * it_tiles);
-            const uint32_t slot = atomicAdd(&bucket_pos[31 - __clz(te - j * it_tiles)], 1u);
+            const uint32_t slot = atomicAdd(&bucket_pos[te - j * it_tiles], 1u);
             // .w: the item's slot in the candidate pool (pair order, so a query's
             // items are contiguous: [q_item_off[q], q_item_off[q + 1]))
             if (slot < item_cap) items[slot] = make_uint4(i, j * it_tiles, te, pair_off[i] + j);
@@ -358,10 +389,12 @@ __global__ void __launch_bounds__(256, 2) lut_image_kernel(const float* __restri
                                                            const uint32_t* __restrict__ list_len, uint32_t nq,
                                                            uint32_t nprobe, uint32_t d, uint32_t sub,
                                                            float* __restrict__ luts, const PlanArgs pa) {
+    CT_BEGIN;
     constexpr int P = 8 * PCH;
     if (blockIdx.x == gridDim.x - 1) {  // the planning CTA
         if (blockIdx.y == 0) {
             pdl_wait();  // probe[] comes from the previous kernel
+            CT_WAITED(3);
             const uint32_t P = nq * nprobe;
             if (P <= blockDim.x)
                 plan_items_regs<1>(probe, list_len, nq, nprobe, pa);
@@ -371,6 +404,7 @@ __global__ void __launch_bounds__(256, 2) lut_image_kernel(const float* __restri
                 plan_items_regs<8>(probe, list_len, nq, nprobe, pa);
             else
                 plan_items(probe, list_len, nq, nprobe, pa);
+            CT_END(3);
         }
         return;
     }
@@ -388,6 +422,7 @@ __global__ void __launch_bounds__(256, 2) lut_image_kernel(const float* __restri
     for (int j = 0; j < JMAX; ++j)
         if (j < int(sub)) wn[j] = __ldg(codewordsT + (size_t(sq0) * sub + j) * 256 + code);
     pdl_wait();  // probe[] comes from the previous kernel
+    CT_WAITED(2);
     if (threadIdx.x < P) {
         const uint32_t pair = p0 + threadIdx.x;
         s_q[threadIdx.x] = pair / nprobe;
@@ -452,6 +487,7 @@ __global__ void __launch_bounds__(256, 2) lut_image_kernel(const float* __restri
         }
     }
     pdl_trigger();
+    CT_END(2);
 }
 
 // ------------------------------------------------------------------- scan
@@ -486,6 +522,14 @@ constexpr uint32_t kEndItem = 0xffffffffu;
 // tiles), finally the exit time. Read back with prag_gpu_debug_k3_trace.
 constexpr uint32_t kTraceSlots = 256;
 __device__ unsigned long long g_k3_trace[160 * kTraceSlots];
+// per CTA, per item (< 32): [0] producer has the item's info, [1] producer
+// issued its table copy, [2] expander 0 saw the table staged, [3] expander 0
+// got the image buffer, [4] image ready, [5] last consumer warp done with it
+__device__ unsigned long long g_k3_trace2[160 * 6 * 32];
+#define K3T2(kind, idx, t)                                                                        \
+    do {                                                                                          \
+        if ((idx) < 32u) g_k3_trace2[(size_t(blockIdx.x) * 6 + (kind)) * 32 + (idx)] = (t);        \
+    } while (0)
 __device__ __forceinline__ unsigned long long gtime() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -601,66 +645,12 @@ __device__ __forceinline__ uint32_t warp_count(const ItemSlot& sl) {
     return min(nw, (ntile + per - 1) / per);
 }
 
-// One consumer warp's share [a, e_end] of an item: tiles a..e_end inclusive
-// (tile e_end holds the tails of the range's last entries) are loaded into
-// registers one tile ahead (A, B alternate) and folded against the SMEM
-// image; lane 0 keeps the next kPrefetch tiles requested into L2 (the
-// producer requested each range's first tiles when it fetched the item).
-// Completed entries of each pair of tiles are
-// offered to the warp's exact top-k, which is finally merged with the item's
-// other warps and published to the query's candidate pool.
-// BUF: the image buffer (compile-time: its offset from image 0 is part of
-// every gather's immediate).
-template <int M, int BUF>
-__device__ __forceinline__ void scan_range(const ScanCtx& cx, const ItemSlot& sl, uint32_t a, uint32_t e_end,
-                                           const float* mk, const float* nk, uint32_t P) {
-    constexpr uint32_t kTileBytes = 32u * M;
-    const uint32_t lane = cx.lane, bt = cx.bt, k = cx.k;
+// Stash the warp's list of the item; the item's last warp merges the lists
+// and publishes the item's top-k to its pool slot.
+__device__ __forceinline__ void merge_publish(const ScanCtx& cx, const ItemSlot& sl, const WarpTopK& t,
+                                              uint32_t* gthr_q) {
+    const uint32_t lane = cx.lane, k = cx.k;
     const uint64_t* __restrict__ ids = cx.ids;
-    uint32_t* gthr_q = cx.gthr + sl.q;
-    const unsigned char* tiles = cx.skew_codes + sl.tile_byte_off;
-    const unsigned char* src_lane = tiles + lane * 16;
-    // the query's shared threshold (other CTAs' k-th distances), read once
-    // per range; the producer's snapshot from item fetch time bounds it too
-    WarpTopK t{0xffffffffu, 0xffffffffu, 0xffffffffu, min(sl.thr, ld_relaxed(gthr_q))};
-    uint4 A[M / 16], B[M / 16];
-    load_tile<M>(A, src_lane, a);
-    load_tile<M>(B, src_lane, a + 1);  // ranges have >= 2 tiles
-    // L2 window: tiles [a + 2, pf) requested so far (the producer requested
-    // [a, a + kHeadTiles) at item fetch)
-    uint32_t pf = P ? min(a + uint32_t(kHeadTiles), e_end + 1) : e_end + 1;
-    const uint32_t lbase = uint32_t(sl.lbase), len = sl.len;
-    float cur = 0.0f, prev = 0.0f;
-    for (uint32_t j = a;; j += 2) {
-        // ---- tile j (registers A)
-        skew_round<M, BUF * int(SkewSmem<M>::kImgStride)>(A, bt, cur, prev, mk, nk, std::make_integer_sequence<int, M>{});
-        if (j + 2 <= e_end) load_tile<M>(A, src_lane, j + 2);
-        const uint32_t ea = (j - 1) * kTileEntries + lane;  // entry completed in `prev`
-        const uint32_t ka = __float_as_uint(prev);
-        const bool va = j > a && ea < len;
-        prev = cur;
-        cur = 0.0f;
-        if (j + 1 > e_end) {
-            topk_offer2(t, ka, va, lbase + ea, 0xffffffffu, false, 0u, lane, k, ids, gthr_q, cx.cta_thr);
-            break;
-        }
-        // ---- tile j + 1 (registers B)
-        skew_round<M, BUF * int(SkewSmem<M>::kImgStride)>(B, bt, cur, prev, mk, nk, std::make_integer_sequence<int, M>{});
-        if (j + 3 <= e_end) load_tile<M>(B, src_lane, j + 3);
-        const uint32_t eb = j * kTileEntries + lane;
-        const uint32_t kb = __float_as_uint(prev);
-        const bool vb = eb < len;
-        prev = cur;
-        cur = 0.0f;
-        // slide the L2 window two tiles (kPrefetch ahead of the loads)
-        if (pf <= e_end && pf < j + 4 + P) {
-            const uint32_t pe = min(pf + 2, e_end + 1);
-            if (lane == 0) prefetch_l2(tiles + size_t(pf) * kTileBytes, (pe - pf) * kTileBytes);
-            pf = pe;
-        }
-        topk_offer2(t, ka, va, lbase + ea, kb, vb, lbase + eb, lane, k, ids, gthr_q, cx.cta_thr);
-        if (j + 2 > e_end) break;
-    }
     // Stash this warp's list; the item's last warp merges the stashed lists
     // into the CTA's exact top-k of the item and publishes only that (k
     // entries per item reach the query's pool instead of k per warp).
@@ -721,6 +711,69 @@ __device__ __forceinline__ void scan_range(const ScanCtx& cx, const ItemSlot& sl
     }
 }
 
+// One consumer warp's share [a, e_end] of an item: tiles a..e_end inclusive
+// (tile e_end holds the tails of the range's last entries) are loaded into
+// registers one tile ahead (A, B alternate) and folded against the SMEM
+// image; lane 0 keeps the next kPrefetch tiles requested into L2 (the
+// producer requested each range's first tiles when it fetched the item).
+// Completed entries of each pair of tiles are
+// offered to the warp's exact top-k, which is finally merged with the item's
+// other warps and published to the query's candidate pool.
+// BUF: the image buffer (compile-time: its offset from image 0 is part of
+// every gather's immediate).
+template <int M, int BUF>
+__device__ __forceinline__ void scan_range(const ScanCtx& cx, const ItemSlot& sl, uint32_t a, uint32_t e_end,
+                                           const float* mk, const float* nk, uint32_t P) {
+    constexpr uint32_t kTileBytes = 32u * M;
+    const uint32_t lane = cx.lane, bt = cx.bt, k = cx.k;
+    const uint64_t* __restrict__ ids = cx.ids;
+    uint32_t* gthr_q = cx.gthr + sl.q;
+    const unsigned char* tiles = cx.skew_codes + sl.tile_byte_off;
+    const unsigned char* src_lane = tiles + lane * 16;
+    // the query's shared threshold (other CTAs' k-th distances), read once
+    // per range; the producer's snapshot from item fetch time bounds it too
+    WarpTopK t{0xffffffffu, 0xffffffffu, 0xffffffffu, min(sl.thr, ld_relaxed(gthr_q))};
+    uint4 A[M / 16], B[M / 16];
+    load_tile<M>(A, src_lane, a);
+    load_tile<M>(B, src_lane, a + 1);  // ranges have >= 2 tiles
+    // L2 window: tiles [a + 2, pf) requested so far (the producer requested
+    // [a, a + kHeadTiles) at item fetch)
+    uint32_t pf = P ? min(a + uint32_t(kHeadTiles), e_end + 1) : e_end + 1;
+    const uint32_t lbase = uint32_t(sl.lbase), len = sl.len;
+    float cur = 0.0f, prev = 0.0f;
+    for (uint32_t j = a;; j += 2) {
+        // ---- tile j (registers A)
+        skew_round<M, BUF * int(SkewSmem<M>::kImgStride)>(A, bt, cur, prev, mk, nk, std::make_integer_sequence<int, M>{});
+        if (j + 2 <= e_end) load_tile<M>(A, src_lane, j + 2);
+        const uint32_t ea = (j - 1) * kTileEntries + lane;  // entry completed in `prev`
+        const uint32_t ka = __float_as_uint(prev);
+        const bool va = j > a && ea < len;
+        prev = cur;
+        cur = 0.0f;
+        if (j + 1 > e_end) {
+            topk_offer2(t, ka, va, lbase + ea, 0xffffffffu, false, 0u, lane, k, ids, gthr_q, cx.cta_thr);
+            break;
+        }
+        // ---- tile j + 1 (registers B)
+        skew_round<M, BUF * int(SkewSmem<M>::kImgStride)>(B, bt, cur, prev, mk, nk, std::make_integer_sequence<int, M>{});
+        if (j + 3 <= e_end) load_tile<M>(B, src_lane, j + 3);
+        const uint32_t eb = j * kTileEntries + lane;
+        const uint32_t kb = __float_as_uint(prev);
+        const bool vb = eb < len;
+        prev = cur;
+        cur = 0.0f;
+        // slide the L2 window two tiles (kPrefetch ahead of the loads)
+        if (pf <= e_end && pf < j + 4 + P) {
+            const uint32_t pe = min(pf + 2, e_end + 1);
+            if (lane == 0) prefetch_l2(tiles + size_t(pf) * kTileBytes, (pe - pf) * kTileBytes);
+            pf = pe;
+        }
+        topk_offer2(t, ka, va, lbase + ea, kb, vb, lbase + eb, lane, k, ids, gthr_q, cx.cta_thr);
+        if (j + 2 > e_end) break;
+    }
+    merge_publish(cx, sl, t, gthr_q);
+}
+
 // Persistent, one CTA per SM, warp-specialised:
 //  * producer warp (one lane): pulls work items {pair, tile_begin,
 //    tile_end} (largest first), resolves the list's metadata and bulk-copies
@@ -748,6 +801,7 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
                      const uint64_t* __restrict__ ids, const float* __restrict__ luts, uint32_t nprobe,
                      uint32_t k, uint32_t* __restrict__ gthr, uint32_t* __restrict__ pool_key,
                      uint64_t* __restrict__ pool_id, uint32_t l2_prefetch) {
+    CT_BEGIN;
     using L = SkewSmem<M>;
     constexpr int W = L::W, NB = L::NB;
     constexpr int kExpWarps = SkewCfg<M>::kExp;
@@ -781,6 +835,7 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
     }
     __syncthreads();
     pdl_wait();  // items, LUTs and thresholds come from the previous kernels
+    CT_WAITED(4);
     const uint32_t total = *num_items;
 #ifdef PRAG_K3_TRACE
     unsigned long long* tr = g_k3_trace + size_t(blockIdx.x) * kTraceSlots;
@@ -799,6 +854,9 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
         uint32_t nx = 0;
         if (lane == 0) nx = atomicAdd(cursor, 1u);
         uint32_t round = 0;  // staging rounds issued (kHalves per item)
+#ifdef PRAG_K3_TRACE
+        uint32_t pit = 0;
+#endif
         for (;;) {
             ItemSlot sl{};
             sl.pair = kEndItem;
@@ -817,6 +875,9 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
                 nx = atomicAdd(cursor, 1u);  // next item's index, fetched ahead
             }
             const uint32_t pair = __shfl_sync(0xffffffffu, sl.pair, 0);
+#ifdef PRAG_K3_TRACE
+            if (lane == 0 && pair != kEndItem) K3T2(0, pit, gtime());
+#endif
             if (pair == kEndItem) {
                 pdl_trigger();  // no more work items: let the pool selection launch
                 if (round > 0) named_sync(kStgBar, kStgEmptyCount);
@@ -824,6 +885,7 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
                     *stg_slot = sl;
                     mbar_arrive(stg_full);
                 }
+                CT_END(4);
                 break;
             }
             {  // request the head of every consumer warp's range into L2 now, an
@@ -845,8 +907,14 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     mbar_expect_tx(stg_full, kStageBytes);
                     bulk_g2s(stage, src + h * kStageBytes, kStageBytes, stg_full);
+#ifdef PRAG_K3_TRACE
+                    if (h == 0) K3T2(1, pit, gtime());
+#endif
                 }
             }
+#ifdef PRAG_K3_TRACE
+            ++pit;
+#endif
         }
         return;
     }
@@ -857,8 +925,14 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
         for (uint32_t i = 0;; ++i) {
             const uint32_t b = i % NB;
             mbar_wait(stg_full, round & 1u);
+#ifdef PRAG_K3_TRACE
+            if (ew == 0 && lane == 0) K3T2(2, i, gtime());
+#endif
             const ItemSlot sl = *stg_slot;
             if (i >= uint32_t(NB)) named_sync(1 + b, kImgEmptyCount);  // consumers done with item i - NB
+#ifdef PRAG_K3_TRACE
+            if (ew == 0 && lane == 0) K3T2(3, i, gtime());
+#endif
             if (sl.pair == kEndItem) {
                 __syncwarp();
                 if (lane == 0) {
@@ -868,6 +942,7 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
                     }
                     mbar_arrive(img_full + b);
                 }
+                CT_END(4);
                 break;
             }
             float* img = reinterpret_cast<float*>(smem + img_off + b * L::kImgStride);
@@ -913,6 +988,9 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
                     cta_thr[b] = 0xffffffffu;
                 }
                 mbar_arrive(img_full + b);
+#ifdef PRAG_K3_TRACE
+                if (ew == 0) K3T2(4, i, gtime());
+#endif
             }
         }
         return;
@@ -943,6 +1021,7 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
             if (warp == 0 && lane == 0 && ntr < kTraceSlots) tr[ntr++] = t_item | (1ull << 63);
             if (warp == 0 && lane == 0) tr[kTraceSlots - 1] = ntr;
 #endif
+            CT_END(4);
             break;
         }
         uint32_t a, e_end;
@@ -957,6 +1036,7 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
                 scan_range<M, 1>(cx, sl, a, e_end, mk, nk, l2_prefetch);
         }
 #ifdef PRAG_K3_TRACE
+        if (warp == uint32_t(W) - 1 && lane == 0) K3T2(5, i, gtime());
         if (warp == 0 && lane == 0 && ntr + 3 < kTraceSlots) {
             tr[ntr++] = t_item;
             tr[ntr++] = gtime();
@@ -970,9 +1050,16 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
 
 }  // namespace
 
+#ifdef PRAG_CHAIN_TRACE
+CT_BIND_FN(ct_bind_skew)
+#endif
+
 #ifdef PRAG_K3_TRACE
 extern "C" int prag_gpu_debug_k3_trace(unsigned long long* out, size_t n) {
     return cudaMemcpyFromSymbol(out, g_k3_trace, std::min(n, size_t(160 * kTraceSlots)) * 8) == cudaSuccess ? 0 : 3;
+}
+extern "C" int prag_gpu_debug_k3_trace2(unsigned long long* out, size_t n) {
+    return cudaMemcpyFromSymbol(out, g_k3_trace2, std::min(n, size_t(160 * 6 * 32)) * 8) == cudaSuccess ? 0 : 3;
 }
 #endif
 

@@ -150,10 +150,62 @@ struct WarpTopK {
     uint32_t key, pos, thr, g;
 };
 
-// Inserts the lanes' candidates that pass (rare after the first tiles).
+// (key, entry slot) order, used by the batched insertion below
+__device__ __forceinline__ bool kp_less(uint32_t ka, uint32_t pa, uint32_t kb, uint32_t pb) {
+    return ka < kb || (ka == kb && pa < pb);
+}
+
+// One compare-exchange step of a 32-lane bitonic network: the lower lane of
+// each (lane, lane ^ stride) pair keeps the smaller (key, slot) when `asc`.
+__device__ __forceinline__ void kp_cas(uint32_t& key, uint32_t& pos, uint32_t lane, uint32_t stride, bool asc) {
+    const uint32_t ok = __shfl_xor_sync(0xffffffffu, key, stride);
+    const uint32_t op = __shfl_xor_sync(0xffffffffu, pos, stride);
+    const bool keep_small = ((lane & stride) == 0) == asc;
+    if (keep_small == kp_less(ok, op, key, pos)) {
+        key = ok;
+        pos = op;
+    }
+}
+
+// Batched insertion of the passing lanes (>= kBatchInsert of them): sort them
+// across the warp (bitonic, by (key, slot)), merge with the sorted list
+// (elementwise minimum against the reversed candidates, then a bitonic
+// merge), keep the smallest 32. Orders ties by entry slot, not chunk id, so
+// when the new first k + 1 hold an exact distance tie the list is restored
+// and the exact one-at-a-time insertion runs instead (returns false).
+#ifndef PRAG_BATCH_INSERT
+#define PRAG_BATCH_INSERT 4
+#endif
+constexpr int kBatchInsert = PRAG_BATCH_INSERT;
+__device__ __forceinline__ bool topk_insert_batch(WarpTopK& t, uint32_t key, bool pass, uint32_t mypos, uint32_t lane,
+                                                  uint32_t k) {
+    uint32_t ck = pass ? key : 0xffffffffu, cp = pass ? mypos : 0xffffffffu;
+#pragma unroll
+    for (uint32_t size = 2; size <= 32; size <<= 1)
+#pragma unroll
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) kp_cas(ck, cp, lane, stride, (lane & size) == 0);
+    const uint32_t rk = __shfl_sync(0xffffffffu, ck, 31 - lane), rp = __shfl_sync(0xffffffffu, cp, 31 - lane);
+    uint32_t mk = t.key, mp = t.pos;
+    if (kp_less(rk, rp, mk, mp)) {
+        mk = rk;
+        mp = rp;
+    }
+#pragma unroll
+    for (uint32_t stride = 16; stride > 0; stride >>= 1) kp_cas(mk, mp, lane, stride, true);
+    const uint32_t nk = __shfl_down_sync(0xffffffffu, mk, 1);
+    if (__any_sync(0xffffffffu, lane < k && lane < 31 && mk == nk && mk != 0xffffffffu)) return false;
+    t.key = mk;
+    t.pos = mp;
+    t.thr = __shfl_sync(0xffffffffu, t.key, k - 1);
+    return true;
+}
+
+// Inserts the lanes' candidates that pass (rare after the first tiles; many
+// at once go through the batched merge).
 __device__ __forceinline__ void topk_insert(WarpTopK& t, uint32_t key, bool pass, uint32_t mypos, uint32_t lane,
                                             uint32_t k, const uint64_t* __restrict__ ids) {
     unsigned bal = __ballot_sync(0xffffffffu, pass);
+    if (__popc(bal) >= kBatchInsert && topk_insert_batch(t, key, pass, mypos, lane, k)) return;
     while (bal) {
         const int src = __ffs(bal) - 1;
         bal &= bal - 1;

@@ -18,6 +18,7 @@ ap.add_argument("--m", type=int, default=64)
 ap.add_argument("--seed", type=int, default=3)
 ap.add_argument("--nq", type=int, default=1)
 ap.add_argument("--nprobe", type=int, default=128)
+ap.add_argument("--tail", action="store_true", help="also print the last items of the last CTAs to finish")
 a = ap.parse_args()
 path, q, _ = F.ensure_fixture(a.n, 384, a.nlist, a.m, a.seed, nq=64, log=lambda *x: None)
 ix = pg.GpuIndex.load(path, 0)
@@ -74,3 +75,25 @@ print(json.dumps({
     "gap_between_items_us": [pct(gaps, 50), pct(gaps, 90), pct(gaps, 100)] if gaps else None,
     "busy_frac_warp0": round(float(np.mean(busy)) / max(ends), 3),
 }))
+if a.tail:
+    f2 = L.prag_gpu_debug_k3_trace2
+    f2.argtypes = [C.c_void_p, C.c_size_t]
+    b2 = np.zeros(160 * 6 * 32, dtype=np.uint64)
+    assert f2(b2.ctypes.data, b2.size) == 0
+    t2 = b2.reshape(160, 6, 32).astype(np.int64)
+    order = np.argsort(ends)
+    for c in list(order[:2]) + list(order[-4:]):
+        n = len(ctas[c][1])
+        ev = [[round((int(t2[c, k, j]) - base) / 1e3, 2) if t2[c, k, j] else None for k in range(6)] for j in range(n)]
+        print(json.dumps({"cta": int(c), "tiles": [int(t_) for (_, _, t_) in ctas[c][1]],
+                          "per_item_fetched_staged_stgseen_buffree_imgready_lastwarpdone": ev}))
+    for c in list(order[:3]) + list(order[-8:]):
+        t0, items, end = ctas[c]
+        print(json.dumps({"cta": int(c), "end": round(ends[c], 2), "n_items": len(items),
+                          "last_items_start_end_tiles": [[round((s_ - base) / 1e3, 2), round((e_ - base) / 1e3, 2), int(t_)]
+                                                         for (s_, e_, t_) in items[-6:]]}))
+    allit = sorted(((s_ - base) / 1e3, t_) for c in ctas for (s_, e_, t_) in c[1])
+    print(json.dumps({"items_total": len(allit), "tiles_total": int(sum(t for _, t in allit)),
+                      "tiles_of_items_started_after_p50_finish": int(sum(t for s_, t in allit if s_ > pct(ends, 50))),
+                      "items_started_after_p50_finish": int(sum(1 for s_, t in allit if s_ > pct(ends, 50))),
+                      "last_30_items_tiles": [int(t) for _, t in allit[-30:]]}))
