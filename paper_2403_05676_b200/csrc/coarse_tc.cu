@@ -142,6 +142,9 @@ __global__ void __launch_bounds__(128, 1) coarse_tc_kernel(const float* __restri
                                                            uint32_t nlist, uint32_t d, uint32_t n_tile,
                                                            float* __restrict__ partial) {
     CT_BEGIN;
+    // let K1b's CTAs launch onto free SMs now (griddepcontrol.wait in K1b
+    // still waits for this whole grid and its memory)
+    pdl_trigger();
     extern __shared__ __align__(1024) unsigned char sm[];
     const uint32_t N = n_tile;                                // multiple of 8, <= kTcMaxN
     const uint32_t kA = 2 * kTcRows * kTcKBlock * 4;          // one K block of A, hi + lo: 32 KiB
@@ -214,6 +217,7 @@ __global__ void __launch_bounds__(128, 1) coarse_tc_kernel(const float* __restri
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    CT_MARK(6);
     const uint32_t tmem = *tmem_slot;
     if (tid == 0) {
         bar_wait(bars, 0);
@@ -238,7 +242,7 @@ __global__ void __launch_bounds__(128, 1) coarse_tc_kernel(const float* __restri
     __syncwarp();
     bar_wait(bars + 1, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    pdl_trigger();
+    CT_MARK(7);
     // epilogue: TMEM lane = centroid row (warp w owns lanes 32w..32w+31);
     // 32 columns per TMEM load
     const uint32_t c = tile * kTcRows + warp * 32 + lane;
@@ -412,6 +416,10 @@ __global__ void __launch_bounds__(kWinThreads) select_window_kernel(
     uint32_t nprobe, uint32_t* __restrict__ probe, float* __restrict__ probe_dist,
     unsigned long long* __restrict__ win_stat, uint32_t kStageRows) {
     CT_BEGIN;
+    // K2's CTAs (tables, planner) may take the SMs K1b leaves idle now: they
+    // run their index-only prologue there and wait for this grid in
+    // griddepcontrol.wait
+    pdl_trigger();
     extern __shared__ __align__(1024) unsigned char sm[];
     uint32_t* hist = reinterpret_cast<uint32_t*>(sm);          // [256]
     uint32_t* misc = hist + 256;                               // [8]: [1] rank, [2..3] selected key, [4] count, [5..7] two-level U
@@ -486,6 +494,7 @@ __global__ void __launch_bounds__(kWinThreads) select_window_kernel(
             lov[i] = __fsub_rn(a, e);
         }
     }
+    CT_MARK(8);
     float* upq = partial + size_t(q) * nlist;  // slice-0 row: scratch for the exact fallback
     // U = the nprobe-th smallest key. Two levels when every thread holds
     // several keys: the nprobe-th smallest of the 512 per-thread minima is an
@@ -563,6 +572,7 @@ __global__ void __launch_bounds__(kWinThreads) select_window_kernel(
     } else {
         ukey = block_select_kth<VPT>(key, nlist, nprobe, hist, misc);
     }
+    CT_MARK(9);
     // window: lists whose lower bound A - E does not exceed U
     // lov[] is in registers: collect through a per-thread test (c = i*512 + tid)
     uint32_t W;
@@ -587,6 +597,7 @@ __global__ void __launch_bounds__(kWinThreads) select_window_kernel(
         W = misc[4];
         if (win_stat && tid == 0) atomicAdd(win_stat, (unsigned long long)W);
     }
+    CT_MARK(10);
     const uint32_t rs = d + 1;
     if (W <= kWinCap) {
         // exact rescoring (common.hpp:73-80 via annindex.hpp:279): rows staged
@@ -632,7 +643,7 @@ __global__ void __launch_bounds__(kWinThreads) select_window_kernel(
         W = exact_fallback<VPT>(upq, centroids, sq, nlist, d, nprobe, hist, misc, win, wd);
     }
     __syncthreads();
-    pdl_trigger();
+    CT_MARK(11);
     // rank by (distance, list id) (annindex.hpp:281 std::sort of pairs)
     for (uint32_t i = tid; i < W; i += kWinThreads) {
         const float di = wd[i];

@@ -30,9 +30,10 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 // warp's PDL-wait return and the warp's end, as globaltimer values in plain
 // stores (no atomics: the trace must not serialise the kernels it times);
 // tools/chain_trace.py reads them back with prag_gpu_debug_chain_trace. Ids:
-// 0 K1, 1 K1b, 2 K2, 3 planner CTA, 4 K3, 5 K4.
+// 0 K1, 1 K1b, 2 K2, 3 planner CTA, 4 K3, 5 K4; 6.. phase marks inside a
+// kernel (CT_MARK: the time a warp passed the mark, in the "waited" field).
 #ifdef PRAG_CHAIN_TRACE
-constexpr int kChainKernels = 6;
+constexpr int kChainKernels = 20;
 constexpr uint32_t kChainCtas = 8192, kChainWarps = 32;
 constexpr size_t kChainWords = size_t(kChainKernels) * kChainCtas * kChainWarps * 3;
 static __constant__ unsigned long long* c_chain;
@@ -55,6 +56,7 @@ __device__ __forceinline__ unsigned long long* ct_slot(int k) {
             p_[1] = ::pg::ct_now();                           \
         }                                                     \
     } while (0)
+#define CT_MARK(k) CT_WAITED(k)
 #define CT_END(k)                                             \
     do {                                                      \
         unsigned long long* p_ = ::pg::ct_slot(k);            \
@@ -67,6 +69,7 @@ void ct_bind_skew(void* p);
 void ct_bind_kernels(void* p);
 #else
 #define CT_BEGIN
+#define CT_MARK(k)
 #define CT_WAITED(k)
 #define CT_END(k)
 #endif

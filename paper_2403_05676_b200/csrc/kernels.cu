@@ -603,10 +603,11 @@ __global__ void __launch_bounds__(kSelThreads) merge_kernel(
 // leaves, per work item, the CTA's exact top-k of that item (k slots, +inf
 // sentinels), so a query's pool is k x its item count, contiguous. The CTA
 // keeps the keys <= the query's final shared threshold T0 (some item left k
-// candidates <= T0, so every top-k member is <= T0) in SMEM, then one warp
-// runs an exact (distance, chunk_id) insertion top-k over them
-// (annindex.hpp:54-60); if more than kPoolCap keys survive, the warp streams
-// the whole pool instead. count = min(scanned_vectors, k) (annindex.hpp:313).
+// candidates <= T0, so every top-k member is <= T0) in SMEM; up to one per
+// thread (about k in practice), each survivor's rank by (distance, chunk_id)
+// (annindex.hpp:54-60) is counted against the others and it is written to
+// that output slot; otherwise one warp runs an exact insertion top-k over
+// them, streaming the whole pool if more than kPoolCap keys survive. count = min(scanned_vectors, k) (annindex.hpp:313).
 __global__ void __launch_bounds__(kPoolThreads) select_pool_kernel(
     const uint32_t* __restrict__ pool_key, const uint64_t* __restrict__ pool_id,
     const uint64_t* __restrict__ scanned, const uint32_t* __restrict__ q_item_off, const uint32_t* __restrict__ gthr,
@@ -616,45 +617,83 @@ __global__ void __launch_bounds__(kPoolThreads) select_pool_kernel(
     __shared__ uint32_t nsurv;
     CT_BEGIN;
     const uint32_t q = blockIdx.x, tid = threadIdx.x, lane = tid & 31u;
-    pdl_wait();  // the pool (and its offsets, from the planner) come from earlier kernels
-    CT_WAITED(5);
-    const size_t off = size_t(q_item_off[q]) * k;
-    const uint32_t n = (q_item_off[q + 1] - q_item_off[q]) * k;
-    const uint32_t total = uint32_t(min(scanned[q], uint64_t(k)));
-    const uint32_t graw = gthr[q];  // raw distance bits (distances are >= 0); the pool holds ord_key()s
-    const uint32_t T0 = graw != 0xffffffffu ? ord_key(__uint_as_float(graw)) : 0xfffffffeu;
-    if (tid == 0) nsurv = 0;
-    __syncthreads();
-    for (uint32_t b0 = 0; b0 < n; b0 += 4 * kPoolThreads) {
-        uint32_t key[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const uint32_t i = b0 + u * kPoolThreads + tid;
-            key[u] = i < n ? pool_key[off + i] : 0xffffffffu;
+    size_t off;
+    uint32_t n, total, T0, c;
+    // Pass 0 runs the same code on four dummy keys with no global reads or
+    // writes before waiting on K3 (this grid launches when K3 runs out of
+    // work items): it pulls the instruction lines in while K3 drains.
+    for (int pass = 0; pass < 2; ++pass) {
+        const bool dry = pass == 0;
+        if (!dry) {
+            pdl_wait();  // the pool (and its offsets, from the planner) come from earlier kernels
+            CT_WAITED(5);
         }
+        off = dry ? 0 : size_t(q_item_off[q]) * k;
+        n = dry ? 4u : (q_item_off[q + 1] - q_item_off[q]) * k;
+        total = dry ? 0u : uint32_t(min(scanned[q], uint64_t(k)));
+        const uint32_t graw = dry ? 0xffffffffu : gthr[q];  // raw distance bits (distances are >= 0); the pool holds ord_key()s
+        T0 = graw != 0xffffffffu ? ord_key(__uint_as_float(graw)) : 0xfffffffeu;
+        if (tid == 0) nsurv = 0;
+        __syncthreads();
+        for (uint32_t b0 = 0; b0 < n; b0 += 4 * kPoolThreads) {
+            uint32_t key[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const uint32_t i = b0 + u * kPoolThreads + tid;
-            const bool take = key[u] <= T0;  // also drops the +inf sentinels and the tail
-            const unsigned bal = __ballot_sync(0xffffffffu, take);
-            uint32_t base = 0;
-            if (lane == 0 && bal) base = atomicAdd(&nsurv, __popc(bal));
-            base = __shfl_sync(0xffffffffu, base, 0);
-            if (take) {
-                const uint32_t pos = base + __popc(bal & ((1u << lane) - 1));
-                if (pos < kPoolCap) {
-                    vkey[pos] = key[u];
-                    vid[pos] = pool_id[off + i];
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t i = b0 + u * kPoolThreads + tid;
+                key[u] = i < n ? (dry ? i : pool_key[off + i]) : 0xffffffffu;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t i = b0 + u * kPoolThreads + tid;
+                const bool take = key[u] <= T0;  // also drops the +inf sentinels and the tail
+                const unsigned bal = __ballot_sync(0xffffffffu, take);
+                uint32_t base = 0;
+                if (lane == 0 && bal) base = atomicAdd(&nsurv, __popc(bal));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (take) {
+                    const uint32_t pos = base + __popc(bal & ((1u << lane) - 1));
+                    if (pos < kPoolCap) {
+                        vkey[pos] = key[u];
+                        vid[pos] = dry ? 0ull : pool_id[off + i];
+                    }
                 }
             }
         }
+        __syncthreads();
+        c = nsurv;
+        if (c <= uint32_t(kPoolThreads)) {
+            // few survivors (the usual case: about k): each one's rank by (distance,
+            // chunk id) among them, counted by its own thread
+            if (tid < c) {
+                const uint32_t mk = vkey[tid];
+                const uint64_t mi = vid[tid];
+                uint32_t r = 0;
+                for (uint32_t j = 0; j < c; ++j) {
+                    const uint32_t kj = vkey[j];
+                    r += kj < mk || (kj == mk && vid[j] < mi);
+                }
+                if (r < total) {
+                    out_dist[size_t(q) * k + r] = key_float(mk);
+                    out_ids[size_t(q) * k + r] = mi;
+                }
+            } else if (tid < total) {  // fewer survivors than results: unfilled slots
+                out_dist[size_t(q) * k + tid] = key_float(0xffffffffu);
+                out_ids[size_t(q) * k + tid] = ~0ull;
+            }
+            if (dry) {
+                __syncthreads();  // vkey / nsurv are reused by the real pass
+                continue;
+            }
+            if (tid == 0) out_count[q] = total;
+            CT_END(5);
+            return;
+        }
+        break;
     }
-    __syncthreads();
     if (tid >= 32) {
         CT_END(5);
         return;
     }
-    const uint32_t c = nsurv;
     const bool from_smem = c <= kPoolCap;
     const uint32_t m = from_smem ? c : n;
     // lane r holds the r-th best (key, id); (thk, thid) is the k-th

@@ -98,6 +98,13 @@ struct PlanArgs {
 // in a smaller size bucket, i.e. at the end of the queue ("guided" tail).
 constexpr uint32_t kSplit = 4;
 
+// Fire-and-forget 64-bit add to global memory (a plain atomicAdd on a generic
+// pointer compiles to a blocking generic atomic with a shared-memory CAS
+// fallback).
+__device__ __forceinline__ void red_add_u64(uint64_t* p, uint64_t v) {
+    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(__cvta_generic_to_global(p)), "l"(v) : "memory");
+}
+
 // pos[b] = sum of cnt[b'] over b' > b (b < nb): bucket start positions with
 // the largest bucket first. Called by the whole block; ends synchronised.
 __device__ __forceinline__ void desc_positions(const uint32_t* cnt, uint32_t* pos, uint32_t nb, uint32_t* ws) {
@@ -144,30 +151,39 @@ __device__ __forceinline__ void desc_positions(const uint32_t* cnt, uint32_t* po
 // front (two dependent rounds in all), the pair-order prefix is one serial
 // sum per thread plus one block scan, and the scatter reuses the registers.
 // Same outputs as plan_items.
+// dry: the same instruction stream with no memory reads or global writes (one
+// tile per pair). The planner CTA runs it before waiting on K1b: K2's CTAs
+// launch early (K1b triggers at its start), and the planner is one CTA
+// running this code once, so otherwise nearly every instruction line is an
+// instruction-cache miss (measured: most of its ~17 us was no_instruction
+// stalls at nq 64, nprobe 16).
 template <int R>
 __device__ __noinline__ void plan_items_regs(const uint32_t* __restrict__ probe, const uint32_t* __restrict__ list_len,
-                                             uint32_t nq, uint32_t nprobe, const PlanArgs pa) {
+                                             uint32_t nq, uint32_t nprobe, const PlanArgs pa, bool dry) {
+    CT_BEGIN;
     const uint32_t it_tiles = pa.it_tiles;
     __shared__ uint32_t wsum[33], bws[33];
     __shared__ uint32_t bucket_cnt[kMaxItemTiles + 1], bucket_pos[kMaxItemTiles + 1];
     const uint32_t P = nq * nprobe, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const uint32_t nb = it_tiles + 1;  // one bucket per item size (tiles)
     for (uint32_t b = tid; b < nb; b += blockDim.x) bucket_cnt[b] = 0;
-    for (uint32_t q = tid; q < nq; q += blockDim.x) {
-        pa.scanned[q] = 0;
-        pa.gthr[q] = 0xffffffffu;
-    }
+    if (!dry)
+        for (uint32_t q = tid; q < nq; q += blockDim.x) {
+            pa.scanned[q] = 0;
+            pa.gthr[q] = 0xffffffffu;
+        }
     uint32_t len[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const uint32_t i = tid * R + r;
-        len[r] = i < P ? probe[i] : 0u;  // list id for now
+        len[r] = i < P && !dry ? probe[i] : 0u;  // list id for now
     }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const uint32_t i = tid * R + r;
-        len[r] = i < P ? list_len[len[r]] : 0u;
+        len[r] = i < P ? (dry ? kTileEntries : list_len[len[r]]) : 0u;
     }
+    CT_MARK(12);
     // full items of this thread's pairs, and their exclusive prefix over the
     // block (pair order): full item number g < split is cut into kSplit pieces
     uint32_t fmine = 0;
@@ -200,6 +216,7 @@ __device__ __noinline__ void plan_items_regs(const uint32_t* __restrict__ probe,
     __syncthreads();
     const uint32_t fexcl0 = wsum[w] + fincl - fmine;
     __syncthreads();  // wsum is reused below
+    CT_MARK(13);
     const uint32_t sub_tiles = it_tiles / kSplit;
     uint32_t mine = 0;
     {
@@ -207,7 +224,7 @@ __device__ __noinline__ void plan_items_regs(const uint32_t* __restrict__ probe,
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const uint32_t i = tid * R + r;
-            if (len[r]) atomicAdd(reinterpret_cast<unsigned long long*>(pa.scanned + i / nprobe), (unsigned long long)len[r]);
+            if (len[r] && !dry) red_add_u64(pa.scanned + i / nprobe, len[r]);
             const uint32_t tiles = (len[r] + kTileEntries - 1) / kTileEntries;
             const uint32_t nit = (tiles + it_tiles - 1) / it_tiles;
             if (nit) {  // nit - 1 full items (the first `split - fexcl` of them cut), then the remainder
@@ -244,14 +261,17 @@ __device__ __noinline__ void plan_items_regs(const uint32_t* __restrict__ probe,
     }
     desc_positions(bucket_cnt, bucket_pos, nb, bws);
     __syncthreads();
+    CT_MARK(14);
     uint32_t excl = wsum[w] + incl - mine;
     uint32_t fexcl = fexcl0;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const uint32_t i = tid * R + r;
         if (i >= P) break;
-        pa.pair_off[i] = excl;
-        if (i % nprobe == 0) pa.q_item_off[i / nprobe] = excl;
+        if (!dry) {
+            pa.pair_off[i] = excl;
+            if (i % nprobe == 0) pa.q_item_off[i / nprobe] = excl;
+        }
         const uint32_t tiles = (len[r] + kTileEntries - 1) / kTileEntries;
         const uint32_t nit = (tiles + it_tiles - 1) / it_tiles;
         uint32_t nout = 0;  // items this pair emits (pool slots excl .. excl + nout)
@@ -263,27 +283,37 @@ __device__ __noinline__ void plan_items_regs(const uint32_t* __restrict__ probe,
             for (uint32_t j = 0; j < cut; ++j)
                 for (uint32_t h = 0; h < kSplit; ++h) {
                     const uint32_t tb = j * it_tiles + h * sub_tiles, n = j * kSplit + h;
-                    if (c0 + n < pa.item_cap) pa.items[c0 + n] = make_uint4(i, tb, tb + sub_tiles, excl + n);
+                    if (c0 + n < pa.item_cap && !dry) pa.items[c0 + n] = make_uint4(i, tb, tb + sub_tiles, excl + n);
                 }
             nout = cut * kSplit;
             const uint32_t b0 = full > cut ? atomicAdd(&bucket_pos[it_tiles], full - cut) : 0u;
             for (uint32_t j = cut; j < full; ++j) {
                 const uint32_t n = b0 + (j - cut);
-                if (n < pa.item_cap) pa.items[n] = make_uint4(i, j * it_tiles, (j + 1) * it_tiles, excl + nout);
+                if (n < pa.item_cap && !dry) pa.items[n] = make_uint4(i, j * it_tiles, (j + 1) * it_tiles, excl + nout);
                 ++nout;
             }
+#ifdef PRAG_EXP_NOATOM
+            const uint32_t slot = i;
+#else
             const uint32_t slot = atomicAdd(&bucket_pos[tiles - full * it_tiles], 1u);
-            if (slot < pa.item_cap) pa.items[slot] = make_uint4(i, full * it_tiles, tiles, excl + nout);
+#endif
+#ifndef PRAG_EXP_NOSTORE
+            if (slot < pa.item_cap && !dry) pa.items[slot] = make_uint4(i, full * it_tiles, tiles, excl + nout);
+#endif
             ++nout;
             fexcl += full;
         }
         excl += nout;
+        if (r == 0) CT_MARK(16);
+        if (r == 1) CT_MARK(17);
+        if (r == 2) CT_MARK(18);
     }
-    if (tid == 0) {
+    if (tid == 0 && !dry) {
         *pa.num_items = wsum[32];
         *pa.cursor = 0;
         pa.q_item_off[nq] = wsum[32];
     }
+    CT_MARK(15);
 }
 
 // Runs on one CTA (any block size that is a multiple of 32, <= 1024): the
@@ -312,7 +342,7 @@ __device__ __noinline__ void plan_items(const uint32_t* __restrict__ probe, cons
         const uint32_t i = base + threadIdx.x;
         const bool valid = i < P;
         const uint32_t len = valid ? list_len[probe[i]] : 0;
-        if (len) atomicAdd(reinterpret_cast<unsigned long long*>(scanned + i / nprobe), (unsigned long long)len);
+        if (len) red_add_u64(scanned + i / nprobe, len);
         const uint32_t tiles = (len + kTileEntries - 1) / kTileEntries;
         const uint32_t nit = (tiles + it_tiles - 1) / it_tiles;
         for (uint32_t j = 0; j < nit; ++j) {
@@ -393,17 +423,23 @@ __global__ void __launch_bounds__(256, 2) lut_image_kernel(const float* __restri
     constexpr int P = 8 * PCH;
     if (blockIdx.x == gridDim.x - 1) {  // the planning CTA
         if (blockIdx.y == 0) {
-            pdl_wait();  // probe[] comes from the previous kernel
-            CT_WAITED(3);
             const uint32_t P = nq * nprobe;
-            if (P <= blockDim.x)
-                plan_items_regs<1>(probe, list_len, nq, nprobe, pa);
-            else if (P <= 4 * blockDim.x)
-                plan_items_regs<4>(probe, list_len, nq, nprobe, pa);
-            else if (P <= 8 * blockDim.x)
-                plan_items_regs<8>(probe, list_len, nq, nprobe, pa);
-            else
-                plan_items(probe, list_len, nq, nprobe, pa);
+            const int R = P <= blockDim.x ? 1 : P <= 4 * blockDim.x ? 4 : P <= 8 * blockDim.x ? 8 : 0;
+            for (int pass = 0; pass < 2; ++pass) {  // 0: instruction-cache warm-up (dry), 1: the plan
+                const bool dry = pass == 0;
+                if (!dry) {
+                    pdl_wait();  // probe[] comes from the previous kernel
+                    CT_WAITED(3);
+                }
+                if (R == 1)
+                    plan_items_regs<1>(probe, list_len, nq, nprobe, pa, dry);
+                else if (R == 4)
+                    plan_items_regs<4>(probe, list_len, nq, nprobe, pa, dry);
+                else if (R == 8)
+                    plan_items_regs<8>(probe, list_len, nq, nprobe, pa, dry);
+                else if (!dry)
+                    plan_items(probe, list_len, nq, nprobe, pa);
+            }
             CT_END(3);
         }
         return;

@@ -19,7 +19,7 @@ import paper_2403_05676_b200 as pg  # noqa: E402
 from paper_2403_05676_b200 import fixtures as F  # noqa: E402
 from paper_2403_05676_b200._lib import lib  # noqa: E402
 
-NAMES = ["K1", "K1b", "K2", "planner", "K3", "K4"]
+NAMES = ["K1", "K1b", "K2", "planner", "K3", "K4", "K1:B-operand-ready", "K1:MMA-done", "K1b:keys", "K1b:U", "K1b:window", "K1b:rescored", "plan:lens", "plan:prefix1", "plan:buckets", "plan:end", "scatter:r0", "scatter:r1", "scatter:r2", "unused"]
 ap = argparse.ArgumentParser()
 ap.add_argument("--nq", type=int, default=64)
 ap.add_argument("--nprobe", type=int, default=16)
@@ -28,6 +28,8 @@ ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--n", type=int, default=10_000_000)
 ap.add_argument("--nlist", type=int, default=4096)
 ap.add_argument("--m", type=int, default=32)
+ap.add_argument("--flush", default="write", choices=["write", "read", "none"],
+                help="L2 flush before each search: memset (bench.py's), a read sweep (clean lines), or none")
 a = ap.parse_args()
 path, q, _ = F.ensure_fixture(a.n, 384, a.nlist, a.m, 1, nq=64, log=lambda *x: None)
 ix = pg.GpuIndex.load(path, 0)
@@ -57,18 +59,22 @@ def timeline():
         ends = t[i][..., 2]
         cta_end = np.where(ends > 0, (ends - base) / 1e3, -np.inf).max(axis=1)
         cta_end = cta_end[np.isfinite(cta_end)]
-        row[nm] = {"ctas": int(np.isfinite(cta_end).sum()), "start": q3(start), "waited": q3(waited),
-                   "cta_end": q3(cta_end)}
+        row[nm] = {"start": q3(start), "waited": q3(waited)}
+        if cta_end.size:
+            row[nm].update({"ctas": int(cta_end.size), "cta_end": q3(cta_end)})
     return row
 
 
-out = {"nq": a.nq, "nprobe": a.nprobe, "k": a.k}
+out = {"nq": a.nq, "nprobe": a.nprobe, "k": a.k, "flush": a.flush}
 assert f(0, None) == 0  # allocates and binds the trace buffer before any search
 res = ix.search_batch(qd, a.k, a.nprobe)
 plan = ix.plan(qd, a.k, a.nprobe, res)
 for mode in ("direct", "plan"):
     for rep in range(a.reps):
-        flush.zero_()
+        if a.flush == "write":
+            flush.zero_()
+        elif a.flush == "read":
+            flush.sum(dtype=torch.int64)
         torch.cuda.synchronize()
         assert f(0, None) == 0
         if mode == "direct":
