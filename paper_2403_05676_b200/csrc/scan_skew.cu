@@ -836,7 +836,7 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
                      const uint8_t* __restrict__ skew_codes, const uint64_t* __restrict__ list_off,
                      const uint64_t* __restrict__ ids, const float* __restrict__ luts, uint32_t nprobe,
                      uint32_t k, uint32_t* __restrict__ gthr, uint32_t* __restrict__ pool_key,
-                     uint64_t* __restrict__ pool_id, uint32_t l2_prefetch) {
+                     uint64_t* __restrict__ pool_id, uint32_t l2_prefetch, uint32_t tail_od) {
     CT_BEGIN;
     using L = SkewSmem<M>;
     constexpr int W = L::W, NB = L::NB;
@@ -887,15 +887,27 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
     constexpr uint32_t kStgBar = 1 + NB;
     if (warp == uint32_t(W)) {
         // ------------------------------------------------------ producer
+        // The next item's index is normally reserved one item ahead (its
+        // metadata loads overlap the staging wait); within the last tail_od
+        // items of the queue it is reserved only once the staging buffer is
+        // free, so a CTA does not hold a tail item it cannot start soon.
         uint32_t nx = 0;
         if (lane == 0) nx = atomicAdd(cursor, 1u);
+        bool held = true;     // nx is a reserved index
         uint32_t round = 0;  // staging rounds issued (kHalves per item)
 #ifdef PRAG_K3_TRACE
         uint32_t pit = 0;
 #endif
         for (;;) {
+            bool synced = false;  // staging-free barrier already passed this item
+            if (!held) {
+                if (round > 0) named_sync(kStgBar, kStgEmptyCount);
+                synced = true;
+                if (lane == 0) nx = atomicAdd(cursor, 1u);
+            }
             ItemSlot sl{};
             sl.pair = kEndItem;
+            held = true;
             if (lane == 0 && nx < total) {
                 const uint4 w4 = items[nx];
                 const uint32_t list = probe[w4.x];
@@ -908,15 +920,19 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
                 sl.lbase = list_off[list];
                 sl.thr = ld_relaxed(gthr + sl.q);
                 sl.pslot = w4.w;
-                nx = atomicAdd(cursor, 1u);  // next item's index, fetched ahead
+                if (total - nx > tail_od)
+                    nx = atomicAdd(cursor, 1u);  // next item's index, fetched ahead
+                else
+                    held = false;
             }
+            held = __shfl_sync(0xffffffffu, held ? 1u : 0u, 0) != 0;
             const uint32_t pair = __shfl_sync(0xffffffffu, sl.pair, 0);
 #ifdef PRAG_K3_TRACE
             if (lane == 0 && pair != kEndItem) K3T2(0, pit, gtime());
 #endif
             if (pair == kEndItem) {
                 pdl_trigger();  // no more work items: let the pool selection launch
-                if (round > 0) named_sync(kStgBar, kStgEmptyCount);
+                if (round > 0 && !synced) named_sync(kStgBar, kStgEmptyCount);
                 if (lane == 0) {
                     *stg_slot = sl;
                     mbar_arrive(stg_full);
@@ -937,7 +953,7 @@ __global__ void __launch_bounds__(SkewSmem<M>::threads, 1)
             }
             const unsigned char* src = reinterpret_cast<const unsigned char*>(luts) + size_t(pair) * M * 1024;
             for (uint32_t h = 0; h < kHalves; ++h, ++round) {
-                if (round > 0) named_sync(kStgBar, kStgEmptyCount);
+                if (round > 0 && !(h == 0 && synced)) named_sync(kStgBar, kStgEmptyCount);
                 if (lane == 0) {
                     if (h == 0) *stg_slot = sl;
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -1192,18 +1208,24 @@ int launch_scan_skew(const DeviceIndex& ix, const uint4* items, const uint32_t* 
     // L2 prefetch distance in tiles (0: off); PRAG_GPU_L2_PREFETCH overrides (tuning knob)
     const char* pe = getenv("PRAG_GPU_L2_PREFETCH");
     const uint32_t l2pf = pe ? uint32_t(atoi(pe)) : uint32_t(ix.nsq == 32 ? SkewCfg<32>::kPrefetch : SkewCfg<64>::kPrefetch);
+    // on-demand reservation of the queue's last 4 x grid items (0: always one
+    // ahead). Measured (tools/r3_knobs*.sh, 0 / 148 / 296 / 592 / 1184 / all):
+    // 592 best or tied on every config B / C row (config B nq 8, nprobe 64
+    // -8%, nq 64, nprobe 16 -1.5%). PRAG_GPU_TAIL_ONDEMAND overrides (tuning knob).
+    const char* te = getenv("PRAG_GPU_TAIL_ONDEMAND");
+    const uint32_t tail_od = te ? uint32_t(atoi(te)) : 4u * uint32_t(grid);
     if (ix.nsq == 32) {
         const size_t smem = skew_smem_bytes<32>();
         PG_CUDA(ensure_smem(reinterpret_cast<const void*>(scan_skew_kernel<32>), int(smem)));
         PG_CUDA(launch_pdl(scan_skew_kernel<32>, dim3(grid), dim3(SkewSmem<32>::threads), smem, s, items, num_items,
                            cursor, probe, ix.list_len, ix.skew_off, ix.skew_codes, ix.list_off, ix.ids, luts, nprobe, k,
-                           gthr, pool_key, pool_id, l2pf));
+                           gthr, pool_key, pool_id, l2pf, tail_od));
     } else {
         const size_t smem = skew_smem_bytes<64>();
         PG_CUDA(ensure_smem(reinterpret_cast<const void*>(scan_skew_kernel<64>), int(smem)));
         PG_CUDA(launch_pdl(scan_skew_kernel<64>, dim3(grid), dim3(SkewSmem<64>::threads), smem, s, items, num_items,
                            cursor, probe, ix.list_len, ix.skew_off, ix.skew_codes, ix.list_off, ix.ids, luts, nprobe, k,
-                           gthr, pool_key, pool_id, l2pf));
+                           gthr, pool_key, pool_id, l2pf, tail_od));
     }
     return check("scan_skew");
 }
