@@ -400,19 +400,45 @@ __device__ __noinline__ void plan_items(const uint32_t* __restrict__ probe, cons
 }
 
 
-// Grid: (ceil(npairs / (8 * PCH)) + 1, m / SQB); the last column of CTAs is
-// the work-item planner (plan_items), which overlaps the table computation.
-// CTA: 256 threads = 256 codes; it computes subquantizers [SQB*blockIdx.y,
-// +SQB) of T[sq][code] = squared_l2(r_sq, w[sq][code], sub_dim)
-// (annindex.hpp:292-297, residual r = q - c_list, annindex.hpp:287-289) for
-// 8 * PCH pairs and writes them as the compact table luts[pair][sq][256]
-// (each store: 256 consecutive codes of one (pair, sq)). A thread's codeword
-// w[sq][code] is loaded once per subquantizer (transposed [sq][j][256] copy:
-// coalesced; the next subquantizer's prefetched while the current one is
-// folded) and reused for all 8 * PCH pairs; residuals sit in SMEM as
-// [sq][j][pair] so one LDS.128 broadcasts four pairs' values.
-template <int M, int SUBC, int SQB, int PCH>  // SUBC: compile-time sub_dim (0 = runtime `sub`, <= 16)
-__global__ void __launch_bounds__(256, 2) lut_image_kernel(const float* __restrict__ queries,
+// The planner CTA of K2 (the grid's last block): work items of the scan.
+__device__ __forceinline__ void planner_cta(const uint32_t* __restrict__ probe, const uint32_t* __restrict__ list_len,
+                                            uint32_t nq, uint32_t nprobe, const PlanArgs& pa) {
+    CT_BEGIN;
+    const uint32_t P = nq * nprobe;
+    const int R = P <= blockDim.x ? 1 : P <= 4 * blockDim.x ? 4 : P <= 8 * blockDim.x ? 8 : 0;
+    for (int pass = 0; pass < 2; ++pass) {  // 0: instruction-cache warm-up (dry), 1: the plan
+        const bool dry = pass == 0;
+        if (!dry) {
+            pdl_wait();  // probe[] comes from the previous kernel
+            CT_WAITED(3);
+        }
+        if (R == 1)
+            plan_items_regs<1>(probe, list_len, nq, nprobe, pa, dry);
+        else if (R == 4)
+            plan_items_regs<4>(probe, list_len, nq, nprobe, pa, dry);
+        else if (R == 8)
+            plan_items_regs<8>(probe, list_len, nq, nprobe, pa, dry);
+        else if (!dry)
+            plan_items(probe, list_len, nq, nprobe, pa);
+    }
+}
+
+// K2: the ADC tables T[pair][sq][256] (annindex.hpp:292-297: squared_l2 of
+// the residual r = q - c_list (annindex.hpp:287-289) against every codeword
+// of subquantizer sq) as a persistent kernel: G table CTAs (two per SM of the
+// search's SM budget, less one for the planner) + the planner CTA (block 0).
+// Task t = (chunk of
+// kTaskPairs pairs t / m, subquantizer t % m); CTA c takes tasks c, c + G, ...
+// (equal cost: static). Thread = code: its codeword w[sq][code][0..sub) comes
+// from the transposed codebook (coalesced); the task's residuals sit in SMEM as
+// [j][pair], so one LDS.128 broadcasts four pairs. Software pipeline per task:
+// the next task's codewords and residual inputs, and the list ids of the task
+// after it, load while this task is folded, so no CTA waits on memory between
+// tasks (the one-task-per-CTA form paid a launch-and-load prologue per CTA
+// and a partial last wave: ~17.5 us at config B vs ~8 us of FP32 work).
+constexpr uint32_t kTaskPairs = 16;
+template <int M, int SUBC>  // SUBC: compile-time sub_dim (0 = runtime `sub`, <= 16)
+__global__ void __launch_bounds__(256, 2) lut_tasks_kernel(const float* __restrict__ queries,
                                                            const float* __restrict__ centroids,
                                                            const float* __restrict__ codewordsT,
                                                            const uint32_t* __restrict__ probe,
@@ -420,107 +446,107 @@ __global__ void __launch_bounds__(256, 2) lut_image_kernel(const float* __restri
                                                            uint32_t nprobe, uint32_t d, uint32_t sub,
                                                            float* __restrict__ luts, const PlanArgs pa) {
     CT_BEGIN;
-    constexpr int P = 8 * PCH;
-    if (blockIdx.x == gridDim.x - 1) {  // the planning CTA
-        if (blockIdx.y == 0) {
-            const uint32_t P = nq * nprobe;
-            const int R = P <= blockDim.x ? 1 : P <= 4 * blockDim.x ? 4 : P <= 8 * blockDim.x ? 8 : 0;
-            for (int pass = 0; pass < 2; ++pass) {  // 0: instruction-cache warm-up (dry), 1: the plan
-                const bool dry = pass == 0;
-                if (!dry) {
-                    pdl_wait();  // probe[] comes from the previous kernel
-                    CT_WAITED(3);
-                }
-                if (R == 1)
-                    plan_items_regs<1>(probe, list_len, nq, nprobe, pa, dry);
-                else if (R == 4)
-                    plan_items_regs<4>(probe, list_len, nq, nprobe, pa, dry);
-                else if (R == 8)
-                    plan_items_regs<8>(probe, list_len, nq, nprobe, pa, dry);
-                else if (!dry)
-                    plan_items(probe, list_len, nq, nprobe, pa);
-            }
-            CT_END(3);
-        }
+    if (blockIdx.x == 0) {  // block 0: launched first, so it never waits for an SM
+        planner_cta(probe, list_len, nq, nprobe, pa);
+        CT_END(3);
         return;
     }
+    constexpr uint32_t P = kTaskPairs;
     constexpr int JMAX = SUBC ? SUBC : 16;
     if (SUBC) sub = SUBC;
-    __shared__ __align__(16) float resid[SQB * 16 * P];  // [sq_local][j][pair]
-    __shared__ uint32_t s_q[P], s_list[P];
+    __shared__ __align__(16) float resid[2][16 * P];  // [buffer][j][pair]
     const uint32_t npairs = nq * nprobe;
-    const uint32_t p0 = blockIdx.x * P;
-    const uint32_t sq0 = blockIdx.y * SQB;
-    const uint32_t code = threadIdx.x;
-    // prefetch the first subquantizer's codeword before anything else
-    float wn[JMAX];
+    const uint32_t nchunks = (npairs + P - 1) / P;
+    const uint32_t ntasks = nchunks * M;
+    const uint32_t G = gridDim.x - 1, code = threadIdx.x, tid = threadIdx.x;
+    // residual-input role of this thread: pair pl of the task, dimension jj
+    const bool rin = tid < P * sub;
+    const uint32_t pl = rin ? tid / sub : 0u, jj = rin ? tid - pl * sub : 0u;
+    uint32_t t = blockIdx.x - 1;
+    if (t >= ntasks) {
+        pdl_trigger();
+        return;
+    }
+    // task t's codewords first (index data, before the dependency wait)
+    float w[JMAX];
 #pragma unroll
     for (int j = 0; j < JMAX; ++j)
-        if (j < int(sub)) wn[j] = __ldg(codewordsT + (size_t(sq0) * sub + j) * 256 + code);
+        if (j < int(sub)) w[j] = __ldg(codewordsT + (size_t(t % M) * sub + j) * 256 + code);
     pdl_wait();  // probe[] comes from the previous kernel
     CT_WAITED(2);
-    if (threadIdx.x < P) {
-        const uint32_t pair = p0 + threadIdx.x;
-        s_q[threadIdx.x] = pair / nprobe;
-        s_list[threadIdx.x] = pair < npairs ? probe[pair] : 0xffffffffu;
-    }
-    __syncthreads();
-    // residual r = q - c_list (annindex.hpp:288) for this CTA's subquantizers
-    // (tables of empty lists are computed too: the scan never reads them)
-    const uint32_t span = SQB * sub;  // contiguous dims [sq0*sub, +span)
-    for (uint32_t t = threadIdx.x; t < span * P; t += blockDim.x) {
-        const uint32_t p = t / span, k = t - p * span;
-        const uint32_t sl = k / sub, j = k - sl * sub;
-        float v = 0.0f;
-        if (s_list[p] != 0xffffffffu) {
-            const uint32_t dim = sq0 * sub + k;
-            v = __fsub_rn(queries[size_t(s_q[p]) * d + dim], centroids[size_t(s_list[p]) * d + dim]);
+    // list id of this thread's pair in task t and in task t + G
+    auto list_of = [&](uint32_t task) -> uint32_t {
+        const uint32_t pair = (task / M) * P + pl;
+        return (rin && task < ntasks && pair < npairs) ? probe[pair] : 0xffffffffu;
+    };
+    auto resid_in = [&](uint32_t task, uint32_t list, float& qv, float& cv) {
+        qv = cv = 0.0f;
+        if (list != 0xffffffffu) {
+            const uint32_t pair = (task / M) * P + pl, dim = (task % M) * sub + jj;
+            qv = queries[size_t(pair / nprobe) * d + dim];
+            cv = centroids[size_t(list) * d + dim];
         }
-        resid[(sl * 16 + j) * P + p] = v;
-    }
-    __syncthreads();
-    const uint32_t nlive = npairs > p0 ? min(uint32_t(P), npairs - p0) : 0u;
-#pragma unroll 1
-    for (int i = 0; i < SQB; ++i) {
-        float w[JMAX];
-#pragma unroll
-        for (int j = 0; j < JMAX; ++j) w[j] = wn[j];
-        if (i + 1 < SQB) {
+    };
+    uint32_t lcur = list_of(t), lnext = list_of(t + G);
+    float qv, cv;
+    resid_in(t, lcur, qv, cv);
+    uint32_t buf = 0;
+    for (;;) {
+        // residuals of task t (tables of empty lists are computed too: the
+        // scan never reads them)
+        if (rin) resid[buf][jj * P + pl] = lcur != 0xffffffffu ? __fsub_rn(qv, cv) : 0.0f;
+        __syncthreads();
+        // next task's inputs, loaded while this one is folded
+        const uint32_t tn = t + G;
+        float wn[JMAX];
+        float qn = 0.0f, cn = 0.0f;
+        uint32_t lnn = 0xffffffffu;
+        if (tn < ntasks) {
 #pragma unroll
             for (int j = 0; j < JMAX; ++j)
-                if (j < int(sub)) wn[j] = __ldg(codewordsT + (size_t(sq0 + i + 1) * sub + j) * 256 + code);
+                if (j < int(sub)) wn[j] = __ldg(codewordsT + (size_t(tn % M) * sub + j) * 256 + code);
+            resid_in(tn, lnext, qn, cn);
+            lnn = list_of(tn + G);
         }
-        const float* rr = resid + (i * 16) * P;
+        const uint32_t p0 = (t / M) * P, sq = t % M;
+        const uint32_t nlive = min(P, npairs - p0);
+        const float* rr = resid[buf];
 #pragma unroll 1
-        for (int c = 0; c < PCH; ++c) {
-            if (uint32_t(c * 8) >= nlive) break;
+        for (uint32_t c = 0; c < P / 8; ++c) {
+            if (c * 8 >= nlive) break;
             // FADD2 (r - w) and FMUL2 (square) two pairs at a time, scalar
-            // FADD accumulation: every step separately rounded, and no
-            // FMUL2 -> FADD2 pair for ptxas to contract into an FFMA2. (A
-            // packed accumulation measured slower: the packed FP32 ops do
-            // not raise the FMA-pipe rate this kernel is bound by.)
+            // FADD accumulation in j order: every step separately rounded, no
+            // FMUL2 -> FADD2 pair for ptxas to contract into an FFMA2 (the
+            // first term is the accumulator itself: 0 + x = x exactly)
             float acc[8];
-#pragma unroll
-            for (int p = 0; p < 8; ++p) acc[p] = 0.0f;
 #pragma unroll
             for (int j = 0; j < JMAX; ++j) {
                 if (j < int(sub)) {
                     const float4 ra = *reinterpret_cast<const float4*>(rr + j * P + c * 8);
                     const float4 rb = *reinterpret_cast<const float4*>(rr + j * P + c * 8 + 4);
-                    float sq[8];  // fl(fl(r - w)^2)
-                    subsq2_bcast(ra.x, ra.y, w[j], sq[0], sq[1]);
-                    subsq2_bcast(ra.z, ra.w, w[j], sq[2], sq[3]);
-                    subsq2_bcast(rb.x, rb.y, w[j], sq[4], sq[5]);
-                    subsq2_bcast(rb.z, rb.w, w[j], sq[6], sq[7]);
+                    float sqv[8];  // fl(fl(r - w)^2)
+                    subsq2_bcast(ra.x, ra.y, w[j], sqv[0], sqv[1]);
+                    subsq2_bcast(ra.z, ra.w, w[j], sqv[2], sqv[3]);
+                    subsq2_bcast(rb.x, rb.y, w[j], sqv[4], sqv[5]);
+                    subsq2_bcast(rb.z, rb.w, w[j], sqv[6], sqv[7]);
 #pragma unroll
-                    for (int p = 0; p < 8; ++p) acc[p] = __fadd_rn(acc[p], sq[p]);
+                    for (int p = 0; p < 8; ++p) acc[p] = j == 0 ? sqv[p] : __fadd_rn(acc[p], sqv[p]);
                 }
             }
-            float* dst = luts + (size_t(p0 + c * 8) * M + sq0 + i) * 256 + code;
+            float* dst = luts + (size_t(p0 + c * 8) * M + sq) * 256 + code;
 #pragma unroll
             for (int p = 0; p < 8; ++p)
-                if (uint32_t(c * 8 + p) < nlive) dst[size_t(p) * M * 256] = acc[p];
+                if (c * 8 + p < nlive) dst[size_t(p) * M * 256] = acc[p];
         }
+        if (tn >= ntasks) break;
+        t = tn;
+#pragma unroll
+        for (int j = 0; j < JMAX; ++j) w[j] = wn[j];
+        qv = qn;
+        cv = cn;
+        lcur = lnext;
+        lnext = lnn;
+        buf ^= 1u;
     }
     pdl_trigger();
     CT_END(2);
@@ -1153,42 +1179,15 @@ int launch_lut_images(const DeviceIndex& ix, const float* queries, const uint32_
     // the span at config C batch 1), not to the last items.
     const char* se = getenv("PRAG_GPU_SPLIT_ITEMS");
     const uint32_t split = se ? uint32_t(atoi(se)) : 0u;
-    (void)scan_grid;
     const PlanArgs pa{it_tiles, split, scanned, items, num_items, cursor, q_item_off, gthr, pair_off, item_cap};
-    // CTA shape (subquantizers x 8*PCH pairs), from tools/sweep_lut.sh:
-    // small batches 2 x 8 (enough CTAs to fill the GPU), large ones 2 x 16.
-    // The kernel sits near its FP32-pipe bound either way (3 separately
-    // rounded ops per (code, pair, dim) term). PRAG_GPU_LUT_CFG="SQB,PCH"
-    // overrides (tuning knob).
-    static const int cfg_env = [] {
-        const char* e = getenv("PRAG_GPU_LUT_CFG");
-        int a = 0, b = 0;
-        return (e && sscanf(e, "%d,%d", &a, &b) == 2) ? a * 16 + b : 0;
-    }();
-    int sqb, pch;
-    if (cfg_env) {
-        sqb = cfg_env / 16;
-        pch = cfg_env % 16;
-    } else {
-        const bool small = uint64_t((npairs + 15) / 16) * (ix.nsq / 2) < 2 * 148;
-        sqb = 2;
-        pch = small ? 1 : 2;
-    }
-    const uint32_t ppc = 8u * pch;
-    dim3 grid((npairs + ppc - 1) / ppc + 1, ix.nsq / sqb);
-#define PG_LUT1(MM, SS, Q, C)                                                                                   \
-    PG_CUDA(launch_pdl(lut_image_kernel<MM, SS, Q, C>, grid, dim3(256), 0, s, queries, ix.centroids,            \
-                       ix.codewordsT, probe, ix.list_len, nq, nprobe, ix.d, ix.sub_dim, luts, pa))
+    // G table CTAs: two per SM of the search's SM budget with the planner
+    // taking one of the slots, at most one per task
+    const uint32_t ntasks = (npairs + kTaskPairs - 1) / kTaskPairs * ix.nsq;
+    const uint32_t G = std::max<uint32_t>(1u, std::min<uint32_t>(2u * scan_grid - 1u, ntasks));
+    const dim3 grid(G + 1);
 #define PG_LUT(MM, SS)                                                                                          \
-    do {                                                                                                        \
-        if (sqb == 2 && pch == 1) PG_LUT1(MM, SS, 2, 1);                                                        \
-        else if (sqb == 2 && pch == 2) PG_LUT1(MM, SS, 2, 2);                                                   \
-        else if (sqb == 2 && pch == 4) PG_LUT1(MM, SS, 2, 4);                                                   \
-        else if (sqb == 4 && pch == 1) PG_LUT1(MM, SS, 4, 1);                                                   \
-        else if (sqb == 4 && pch == 2) PG_LUT1(MM, SS, 4, 2);                                                   \
-        else if (sqb == 8 && pch == 1) PG_LUT1(MM, SS, 8, 1);                                                   \
-        else PG_LUT1(MM, SS, 4, 4);                                                                             \
-    } while (0)
+    PG_CUDA(launch_pdl(lut_tasks_kernel<MM, SS>, grid, dim3(256), 0, s, queries, ix.centroids, ix.codewordsT,   \
+                       probe, ix.list_len, nq, nprobe, ix.d, ix.sub_dim, luts, pa))
     if (ix.nsq == 32 && ix.sub_dim == 12)
         PG_LUT(32, 12);
     else if (ix.nsq == 32)
@@ -1197,7 +1196,6 @@ int launch_lut_images(const DeviceIndex& ix, const float* queries, const uint32_
         PG_LUT(64, 6);
     else
         PG_LUT(64, 0);
-#undef PG_LUT1
 #undef PG_LUT
     return check("lut_images");
 }
