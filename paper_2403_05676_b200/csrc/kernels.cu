@@ -612,7 +612,7 @@ __global__ void __launch_bounds__(kPoolThreads) select_pool_kernel(
     const uint32_t* __restrict__ pool_key, const uint64_t* __restrict__ pool_id,
     const uint64_t* __restrict__ scanned, const uint32_t* __restrict__ q_item_off, const uint32_t* __restrict__ gthr,
     uint32_t k, uint64_t* __restrict__ out_ids, float* __restrict__ out_dist, uint32_t* __restrict__ out_count) {
-    __shared__ uint32_t vkey[kPoolCap];
+    __shared__ __align__(16) uint32_t vkey[kPoolCap + 4];  // + padding for the 4-wide rank loop
     __shared__ uint64_t vid[kPoolCap];
     __shared__ uint32_t nsurv;
     CT_BEGIN;
@@ -663,14 +663,20 @@ __global__ void __launch_bounds__(kPoolThreads) select_pool_kernel(
         c = nsurv;
         if (c <= uint32_t(kPoolThreads)) {
             // few survivors (the usual case: about k): each one's rank by (distance,
-            // chunk id) among them, counted by its own thread
+            // chunk id) among them, counted by its own thread, four keys per LDS.128
+            if (tid < 4) vkey[c + tid] = 0xffffffffu;  // above every survivor (all <= T0 < 0xffffffff)
+            __syncthreads();
             if (tid < c) {
                 const uint32_t mk = vkey[tid];
                 const uint64_t mi = vid[tid];
                 uint32_t r = 0;
-                for (uint32_t j = 0; j < c; ++j) {
-                    const uint32_t kj = vkey[j];
-                    r += kj < mk || (kj == mk && vid[j] < mi);
+                for (uint32_t j = 0; j < c; j += 4) {
+                    const uint4 kj = *reinterpret_cast<const uint4*>(vkey + j);
+                    r += uint32_t(kj.x < mk) + uint32_t(kj.y < mk) + uint32_t(kj.z < mk) + uint32_t(kj.w < mk);
+                    if (kj.x == mk || kj.y == mk || kj.z == mk || kj.w == mk) {  // distance ties: by chunk id
+                        r += uint32_t(kj.x == mk && vid[j] < mi) + uint32_t(kj.y == mk && vid[j + 1] < mi) +
+                             uint32_t(kj.z == mk && vid[j + 2] < mi) + uint32_t(kj.w == mk && vid[j + 3] < mi);
+                    }
                 }
                 if (r < total) {
                     out_dist[size_t(q) * k + r] = key_float(mk);
