@@ -599,15 +599,100 @@ __global__ void __launch_bounds__(kSelThreads) merge_kernel(
                out_ids + size_t(q) * k, out_count + q);
 }
 
+// K4 helper: more survivors than threads. The min(k, c)-th smallest key K of
+// vkey[0, c) by a 4-pass radix select (8 bits per pass, SMEM histogram), then
+// the survivors with key <= K (k of them plus any distance ties at K) are
+// compacted to the front of vkey / vid; returns their count. Whole block.
+__device__ __noinline__ uint32_t narrow_survivors(uint32_t* vkey, uint64_t* vid, uint32_t c, uint32_t k,
+                                                  uint32_t* nsurv) {
+    __shared__ uint32_t hist[256];
+    __shared__ uint32_t sel[2];  // selected key prefix, rank still to find within it
+    const uint32_t tid = threadIdx.x, lane = tid & 31u;
+    if (tid == 0) {
+        sel[0] = 0;
+        sel[1] = min(k, c);
+    }
+    uint32_t mask = 0;
+    for (int shift = 24; shift >= 0; shift -= 8) {
+        for (uint32_t b = tid; b < 256; b += blockDim.x) hist[b] = 0;
+        __syncthreads();
+        const uint32_t prefix = sel[0];
+        for (uint32_t i = tid; i < c; i += blockDim.x) {
+            const uint32_t key = vkey[i];
+            if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+        }
+        __syncthreads();
+        if (tid < 32) {
+            uint32_t v[8], local = 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                v[i] = hist[lane * 8 + i];
+                local += v[i];
+            }
+            uint32_t incl = local;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= uint32_t(o)) incl += t;
+            }
+            const uint32_t r = sel[1];
+            __syncwarp();
+            uint32_t acc = incl - local;
+            if (acc < r && r <= incl) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    if (acc + v[i] >= r) {
+                        sel[0] = prefix | ((lane * 8u + uint32_t(i)) << shift);
+                        sel[1] = r - acc;
+                        break;
+                    }
+                    acc += v[i];
+                }
+            }
+        }
+        __syncthreads();
+        mask |= 255u << shift;
+    }
+    const uint32_t K = sel[0];
+    constexpr int kPer = int(kPoolCap / kPoolThreads);
+    uint32_t kk[kPer];
+    uint64_t ii[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+        const uint32_t i = uint32_t(u) * blockDim.x + tid;
+        kk[u] = i < c ? vkey[i] : 0xffffffffu;
+        ii[u] = i < c ? vid[i] : ~0ull;
+    }
+    if (tid == 0) *nsurv = 0;
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+        const bool take = kk[u] <= K;
+        const unsigned bal = __ballot_sync(0xffffffffu, take);
+        uint32_t base = 0;
+        if (lane == 0 && bal) base = atomicAdd(nsurv, __popc(bal));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (take) {
+            const uint32_t pos = base + __popc(bal & ((1u << lane) - 1));
+            vkey[pos] = kk[u];
+            vid[pos] = ii[u];
+        }
+    }
+    __syncthreads();
+    return *nsurv;
+}
+
 // K4 (fast path): exact top-k of a query's candidate pool. The fused scan
 // leaves, per work item, the CTA's exact top-k of that item (k slots, +inf
 // sentinels), so a query's pool is k x its item count, contiguous. The CTA
 // keeps the keys <= the query's final shared threshold T0 (some item left k
 // candidates <= T0, so every top-k member is <= T0) in SMEM; up to one per
-// thread (about k in practice), each survivor's rank by (distance, chunk_id)
-// (annindex.hpp:54-60) is counted against the others and it is written to
-// that output slot; otherwise one warp runs an exact insertion top-k over
-// them, streaming the whole pool if more than kPoolCap keys survive. count = min(scanned_vectors, k) (annindex.hpp:313).
+// thread (about k in practice; more are first narrowed to the keys <= the
+// k-th smallest by a radix select), each survivor's rank by (distance,
+// chunk_id) (annindex.hpp:54-60) is counted against the others and it is
+// written to that output slot; otherwise (ties beyond the block, or more than
+// kPoolCap survivors) one warp runs an exact insertion top-k, streaming the
+// whole pool past kPoolCap. count = min(scanned_vectors, k) (annindex.hpp:313).
 __global__ void __launch_bounds__(kPoolThreads) select_pool_kernel(
     const uint32_t* __restrict__ pool_key, const uint64_t* __restrict__ pool_id,
     const uint64_t* __restrict__ scanned, const uint32_t* __restrict__ q_item_off, const uint32_t* __restrict__ gthr,
@@ -661,6 +746,7 @@ __global__ void __launch_bounds__(kPoolThreads) select_pool_kernel(
         }
         __syncthreads();
         c = nsurv;
+        if (c > uint32_t(kPoolThreads) && c <= kPoolCap) c = narrow_survivors(vkey, vid, c, k, &nsurv);
         if (c <= uint32_t(kPoolThreads)) {
             // few survivors (the usual case: about k): each one's rank by (distance,
             // chunk id) among them, counted by its own thread, four keys per LDS.128
