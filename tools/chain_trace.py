@@ -45,6 +45,10 @@ def q3(v):
     return [round(float(np.min(v)), 2), round(float(np.median(v)), 2), round(float(np.max(v)), 2)]
 
 
+def q5(v):
+    return [round(float(np.percentile(v, p)), 2) for p in (0, 10, 50, 90, 99, 100)]
+
+
 def timeline():
     t = buf.reshape(len(NAMES), CTAS, WARPS, 3).astype(np.int64)
     w = t[..., 1] > 0
@@ -61,7 +65,7 @@ def timeline():
         cta_end = cta_end[np.isfinite(cta_end)]
         row[nm] = {"start": q3(start), "waited": q3(waited)}
         if cta_end.size:
-            row[nm].update({"ctas": int(cta_end.size), "cta_end": q3(cta_end)})
+            row[nm].update({"ctas": int(cta_end.size), "cta_end": q3(cta_end), "cta_end_p0_10_50_90_99_100": q5(cta_end)})
     return row
 
 
