@@ -493,7 +493,7 @@ int search_pass_skew(prag_gpu_index* ix, Workspace* w, const float* dq, uint32_t
     if (prof) cudaEventRecord(w->ev[3], s);
     PG_TRY(launch_scan_skew(d, items, ctr, ctr + 1, probe, images, nprobe, k, gthr, pool_key, pool_id, grid, s));
     if (prof) cudaEventRecord(w->ev[4], s);
-    PG_TRY(launch_select_pool(pool_key, pool_id, o_scanned, q_item_off, gthr, nq, k, o_ids, o_dist, o_count, fkey,
+    PG_TRY(launch_select_pool(pool_key, pool_id, d.ids, o_scanned, q_item_off, gthr, nq, k, o_ids, o_dist, o_count, fkey,
                               ftie, pw_f, s));
     if (prof) {
         cudaEventRecord(w->ev[5], s);

@@ -334,7 +334,7 @@ int launch_scan_skew(const DeviceIndex& ix, const uint4* items, const uint32_t* 
                      uint32_t* pool_key, uint64_t* pool_id, int grid, cudaStream_t s);
 // K4: per query, exact top-k of its items' pool slots (k entries per item,
 // [q_item_off[q] * k, q_item_off[q + 1] * k)); count = min(scanned[q], k)
-int launch_select_pool(const uint32_t* pool_key, const uint64_t* pool_id, const uint64_t* scanned,
+int launch_select_pool(const uint32_t* pool_key, const uint64_t* pool_id, const uint64_t* ids, const uint64_t* scanned,
                        const uint32_t* q_item_off, const uint32_t* gthr, uint32_t nq, uint32_t k, uint64_t* out_ids,
                        float* out_dist, uint32_t* out_count, uint32_t* gkey, uint64_t* gtie, uint32_t pw,
                        cudaStream_t s);

@@ -683,7 +683,8 @@ __device__ __noinline__ uint32_t narrow_survivors(uint32_t* vkey, uint64_t* vid,
 }
 
 // K4 (fast path): exact top-k of a query's candidate pool. The fused scan
-// leaves, per work item, the CTA's exact top-k of that item (k slots, +inf
+// leaves, per work item, the CTA's exact top-k of that item as (key, entry
+// slot) pairs (k slots, +inf
 // sentinels), so a query's pool is k x its item count, contiguous. The CTA
 // keeps the keys <= the query's final shared threshold T0 (some item left k
 // candidates <= T0, so every top-k member is <= T0) in SMEM; up to one per
@@ -694,7 +695,7 @@ __device__ __noinline__ uint32_t narrow_survivors(uint32_t* vkey, uint64_t* vid,
 // kPoolCap survivors) one warp runs an exact insertion top-k, streaming the
 // whole pool past kPoolCap. count = min(scanned_vectors, k) (annindex.hpp:313).
 __global__ void __launch_bounds__(kPoolThreads) select_pool_kernel(
-    const uint32_t* __restrict__ pool_key, const uint64_t* __restrict__ pool_id,
+    const uint32_t* __restrict__ pool_key, const uint64_t* __restrict__ pool_id, const uint64_t* __restrict__ ids,
     const uint64_t* __restrict__ scanned, const uint32_t* __restrict__ q_item_off, const uint32_t* __restrict__ gthr,
     uint32_t k, uint64_t* __restrict__ out_ids, float* __restrict__ out_dist, uint32_t* __restrict__ out_count) {
     __shared__ __align__(16) uint32_t vkey[kPoolCap + 4];  // + padding for the 4-wide rank loop
@@ -739,7 +740,7 @@ __global__ void __launch_bounds__(kPoolThreads) select_pool_kernel(
                     const uint32_t pos = base + __popc(bal & ((1u << lane) - 1));
                     if (pos < kPoolCap) {
                         vkey[pos] = key[u];
-                        vid[pos] = dry ? 0ull : pool_id[off + i];
+                        vid[pos] = dry ? 0ull : ids[pool_id[off + i]];  // the pool holds entry slots
                     }
                 }
             }
@@ -798,7 +799,7 @@ __global__ void __launch_bounds__(kPoolThreads) select_pool_kernel(
         const bool pre = key <= min(T0, thk);
         unsigned bal = __ballot_sync(0xffffffffu, pre);
         if (!bal) continue;
-        const uint64_t id = pre ? (from_smem ? vid[i] : pool_id[off + i]) : ~0ull;
+        const uint64_t id = pre ? (from_smem ? vid[i] : ids[pool_id[off + i]]) : ~0ull;
         while (bal) {
             const int src = __ffs(bal) - 1;
             bal &= bal - 1;
@@ -834,14 +835,14 @@ __global__ void __launch_bounds__(kPoolThreads) select_pool_kernel(
 CT_BIND_FN(ct_bind_kernels)
 #endif
 
-int launch_select_pool(const uint32_t* pool_key, const uint64_t* pool_id, const uint64_t* scanned,
+int launch_select_pool(const uint32_t* pool_key, const uint64_t* pool_id, const uint64_t* ids, const uint64_t* scanned,
                        const uint32_t* q_item_off, const uint32_t* gthr, uint32_t nq, uint32_t k, uint64_t* out_ids,
                        float* out_dist, uint32_t* out_count, uint32_t* gkey, uint64_t* gtie, uint32_t pw,
                        cudaStream_t s) {
     (void)gkey;
     (void)gtie;
     (void)pw;
-    cudaError_t e = launch_pdl(select_pool_kernel, dim3(nq), dim3(kPoolThreads), 0, s, pool_key, pool_id, scanned,
+    cudaError_t e = launch_pdl(select_pool_kernel, dim3(nq), dim3(kPoolThreads), 0, s, pool_key, pool_id, ids, scanned,
                                q_item_off, gthr, k, out_ids, out_dist, out_count);
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) {
