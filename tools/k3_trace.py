@@ -81,7 +81,24 @@ if a.tail:
     b2 = np.zeros(160 * 6 * 32, dtype=np.uint64)
     assert f2(b2.ctypes.data, b2.size) == 0
     t2 = b2.reshape(160, 6, 32).astype(np.int64)
+    # per-warp item ends: only builds that record them (prag_gpu_debug_k3_trace3)
+    b3 = np.zeros(160 * 16 * 32, dtype=np.uint64)
+    if hasattr(L, "prag_gpu_debug_k3_trace3"):
+        f3 = L.prag_gpu_debug_k3_trace3
+        f3.argtypes = [C.c_void_p, C.c_size_t]
+        assert f3(b3.ctypes.data, b3.size) == 0
+    t3 = b3.reshape(160, 16, 32).astype(np.int64)
     order = np.argsort(ends)
+    lag = []  # per CTA and item: slowest consumer warp's range end minus the median warp's
+    for c in range(sms):
+        for j in range(len(ctas[c][1])):
+            v = [int(t3[c, w, j]) for w in range(16) if t3[c, w, j]]
+            if len(v) > 2:
+                lag.append((max(v) - float(np.median(v))) / 1e3)
+    print(json.dumps({"item_warp_lag_us_p50_p90_max": [pct(lag, 50), pct(lag, 90), pct(lag, 100)]}))
+    for c in list(order[-2:]):
+        n = len(ctas[c][1])
+        print(json.dumps({"cta": int(c), "per_item_warp_end_us": [[round((int(t3[c, w, j]) - base) / 1e3, 1) if t3[c, w, j] else None for w in range(16)] for j in range(n)]}))
     for c in list(order[:2]) + list(order[-4:]):
         n = len(ctas[c][1])
         ev = [[round((int(t2[c, k, j]) - base) / 1e3, 2) if t2[c, k, j] else None for k in range(6)] for j in range(n)]
