@@ -288,7 +288,8 @@ def main():
     workload = workload_name(cfg, world, mode)
     scaling = "weak" if mode == "replicas" else "strong"
     parallelism = {"single": "single GPU", "replicas": f"query-parallel replicas x{world}",
-                   "shard-lists": f"inverted lists sharded over {world} GPUs (LPT on bytes), NCCL all-gather "
+                   "shard-lists": f"inverted lists sharded over {world} GPUs (LPT on bytes, lists >= 4x the mean "
+                                  f"striped over all ranks), NCCL all-gather "
                                   f"of per-shard top-k + exact merge"}[mode]
 
     import paper_2403_05676_b200 as pg

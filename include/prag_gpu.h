@@ -227,11 +227,19 @@ int prag_gpu_probe(prag_gpu_index* index, const float* queries, uint32_t nq, uin
                    uint32_t* out_lists, float* out_dist, void* stream);
 
 /* ------------------------------------------------------ multi-GPU pieces */
-/* LPT placement of lists on `world` shards by bytes (|l| * m): lists in
- * descending size (ties by lower id) each go to the least-loaded shard (ties
- * by lower rank). Host-only; never touches a GPU. */
+/* Placement of lists on `world` shards by bytes (|l| * m). Large lists (at
+ * least 4x the mean list size and 1024 entries per stripe) are STRIPED over
+ * all ranks -- rank r holds entries [len*r/world, len*(r+1)/world) -- and get
+ * out_owner = world; the rest go whole by LPT: descending size (ties by lower
+ * id), each to the least-loaded shard (ties by lower rank), the striped
+ * loads counted first. Host-only; never touches a GPU. */
 int prag_gpu_plan_shards(const uint64_t* list_sizes, uint32_t nlist, uint32_t world,
                          uint32_t* out_owner);
+/* The same placement as the entry range [out_begin[l], out_end[l]) of every
+ * list held by `rank` (empty when the list is not resident there): what
+ * load_shard / synthetic_shard / the sharded loaders keep. */
+int prag_gpu_plan_shard_ranges(const uint64_t* list_sizes, uint32_t nlist, uint32_t world, uint32_t rank,
+                               uint64_t* out_begin, uint64_t* out_end);
 
 /* Exact top-k of the union of `nparts` per-shard top-k lists, per query.
  * Inputs device or host: ids/dist [nparts][nq][kin], count [nparts][nq];

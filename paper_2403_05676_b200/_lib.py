@@ -100,6 +100,7 @@ SYMBOLS = [
     ("prag_gpu_search_rerank", C.c_int, [P, P, C.c_uint32, C.c_uint32, C.c_uint32, P, P, P, P, P]),
     ("prag_gpu_brute_force", C.c_int, [P, C.c_uint64, C.c_uint32, P, C.c_uint32, C.c_uint32, C.c_int, P, P, P]),
     ("prag_gpu_plan_shards", C.c_int, [P, C.c_uint32, C.c_uint32, P]),
+    ("prag_gpu_plan_shard_ranges", C.c_int, [P, C.c_uint32, C.c_uint32, C.c_uint32, P, P]),
     ("prag_gpu_merge_topk", C.c_int,
      [P, P, P, P, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, P, P, P, P, C.c_int, P]),
     ("prag_gpu_calibrate_retrieval", C.c_int,

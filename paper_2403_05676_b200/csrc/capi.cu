@@ -928,14 +928,14 @@ int build_synthetic(uint32_t nlist, uint32_t d, uint32_t nsq, uint64_t ntotal, u
     dv.plain_codes = false;
     std::vector<uint64_t> sizes;  // the whole index's lists
     synth_list_sizes(nlist, ntotal, seed, sigma, sizes);
-    // shard: the lists prag_gpu_plan_shards gives `rank`; every entry keeps
-    // its global list-major position g (chunk id g, codes from g)
-    std::vector<uint64_t> rsz(sizes);
+    // shard: the entry ranges prag_gpu_plan_shard_ranges gives `rank` (whole
+    // lists, or a stripe of a large one); every entry keeps its global
+    // list-major position g (chunk id g, codes from g)
+    std::vector<uint64_t> rsz(sizes), rbeg(nlist, 0);
     if (world > 1) {
-        std::vector<uint32_t> owner(nlist);
-        plan_shards_lpt(sizes.data(), nlist, uint32_t(world), owner.data());
-        for (uint32_t l = 0; l < nlist; ++l)
-            if (owner[l] != uint32_t(rank)) rsz[l] = 0;
+        std::vector<uint64_t> rend(nlist);
+        plan_shard_ranges(sizes.data(), nlist, uint32_t(world), uint32_t(rank), rbeg.data(), rend.data());
+        for (uint32_t l = 0; l < nlist; ++l) rsz[l] = rend[l] - rbeg[l];
     }
     ix->shard_rank = rank;
     ix->shard_world = world;
@@ -999,7 +999,9 @@ int build_synthetic(uint32_t nlist, uint32_t d, uint32_t nsq, uint64_t ntotal, u
     cp(dv.list_off, poff.data(), poff.size() * 8);
     cp(dv.list_len, len.data(), len.size() * 4);
     cp(dv.skew_off, soff.data(), soff.size() * 8);
-    cp(dloff, gbase.data(), gbase.size() * 8);
+    std::vector<uint64_t> ebase(gbase);  // global position of each list's first resident entry
+    for (uint32_t l = 0; l < nlist; ++l) ebase[l] += rbeg[l];
+    cp(dloff, ebase.data(), ebase.size() * 8);
     cp(dloff + nlist + 1, rsz.data(), size_t(nlist) * 8);
     if (e != cudaSuccess) {
         cudaFree(dloff);
@@ -1074,10 +1076,11 @@ int prag_gpu_index_load_shard(const char* path, int device, int rank, int world,
     PG_TRY(require_device(device));
     std::vector<uint64_t> sizes;
     PG_TRY(read_pragix01_list_sizes(path, sizes));
-    std::vector<uint32_t> owner(sizes.size());
-    plan_shards_lpt(sizes.data(), uint32_t(sizes.size()), uint32_t(world), owner.data());
-    std::vector<uint8_t> keep(sizes.size());
-    for (size_t l = 0; l < sizes.size(); ++l) keep[l] = owner[l] == uint32_t(rank);
+    KeepRanges keep;
+    keep.begin.resize(sizes.size());
+    keep.end.resize(sizes.size());
+    plan_shard_ranges(sizes.data(), uint32_t(sizes.size()), uint32_t(world), uint32_t(rank), keep.begin.data(),
+                      keep.end.data());
     HostIndex h;
     PG_TRY(read_pragix01(path, h, &keep));
     auto ix = std::make_unique<prag_gpu_index>();
@@ -1583,6 +1586,22 @@ int prag_gpu_plan_shards(const uint64_t* sizes, uint32_t nlist, uint32_t world, 
         return PRAG_GPU_CONFIG;
     }
     plan_shards_lpt(sizes, nlist, world, owner);
+    return PRAG_GPU_OK;
+    PG_API_END
+}
+
+int prag_gpu_plan_shard_ranges(const uint64_t* sizes, uint32_t nlist, uint32_t world, uint32_t rank,
+                               uint64_t* out_begin, uint64_t* out_end) {
+    PG_API_BEGIN
+    if ((!sizes || !out_begin || !out_end) && nlist) {
+        set_error("null argument");
+        return PRAG_GPU_CONFIG;
+    }
+    if (world < 1 || rank >= world) {
+        set_error("world must be >= 1 and rank < world");
+        return PRAG_GPU_CONFIG;
+    }
+    plan_shard_ranges(sizes, nlist, world, rank, out_begin, out_end);
     return PRAG_GPU_OK;
     PG_API_END
 }

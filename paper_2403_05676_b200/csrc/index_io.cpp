@@ -7,6 +7,7 @@
 // Errors reproduce the reference FormatError texts including byte offsets.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <numeric>
@@ -33,7 +34,7 @@ struct Reader {
 
 }  // namespace
 
-int read_pragix01(const std::string& path, HostIndex& out, const std::vector<uint8_t>* keep) {
+int read_pragix01(const std::string& path, HostIndex& out, const KeepRanges* keep) {
     FILE* fp = fopen(path.c_str(), "rb");
     if (!fp) {
         set_error("cannot open for reading: " + path);
@@ -116,7 +117,8 @@ int read_pragix01(const std::string& path, HostIndex& out, const std::vector<uin
         }
         offset += 8;
         global += len;
-        const bool kept = keep == nullptr || (*keep)[l];
+        const bool kept = keep == nullptr || (l < keep->begin.size() && keep->begin[l] < keep->end[l] &&
+                                              keep->end[l] <= len);
         if (!kept) {
             // A shard seeks past lists it does not keep; a short file fails
             // on the same record (and offset) the reference loader would.
@@ -174,6 +176,13 @@ int read_pragix01(const std::string& path, HostIndex& out, const std::vector<uin
             e += n;
         }
         offset += len * rec;
+        if (keep && (keep->begin[l] > 0 || keep->end[l] < len)) {  // a stripe of the list
+            const uint64_t b = keep->begin[l], n = keep->end[l] - b;
+            std::memmove(&out.ids[base], &out.ids[base + b], n * 8);
+            std::memmove(&out.codes[base * out.nsq], &out.codes[(base + b) * out.nsq], n * out.nsq);
+            out.ids.resize(base + n);
+            out.codes.resize((base + n) * out.nsq);
+        }
         out.list_off[l + 1] = out.ids.size();
     }
     out.ntotal_global = global;
@@ -211,18 +220,61 @@ int read_pragix01_list_sizes(const std::string& path, std::vector<uint64_t>& siz
     return PRAG_GPU_OK;
 }
 
+// Placement of lists on `world` shards. Lists of
+// at least kStripeFactor x the mean list size (and >= kStripeMin entries per
+// stripe) are STRIPED: rank r holds entries [len*r/world, len*(r+1)/world).
+// Probes are size-biased (queries sit where the data is dense, so the lists
+// they probe are the large ones), and a large list kept whole puts all of its
+// scan on one GPU for every query that probes it. The other lists go whole
+// by LPT on entries (descending size, ties by lower id; least-loaded shard,
+// ties by lower rank), starting from the striped loads. owner[l] = world
+// marks a striped list.
+constexpr uint64_t kStripeFactor = 4;
+constexpr uint64_t kStripeMin = 1024;  // entries per stripe (32 tiles) at least
+
 void plan_shards_lpt(const uint64_t* sizes, uint32_t nlist, uint32_t world, uint32_t* owner) {
-    std::vector<uint32_t> order(nlist);
-    std::iota(order.begin(), order.end(), 0u);
-    std::stable_sort(order.begin(), order.end(),
-                     [&](uint32_t a, uint32_t b) { return sizes[a] > sizes[b]; });
+    // PRAG_GPU_STRIPE=0: whole lists only (the round-1 placement; an A/B
+    // knob -- every rank of a world must see the same value)
+    const char* env = getenv("PRAG_GPU_STRIPE");
+    const bool striping = !(env && env[0] == '0');
     std::vector<uint64_t> load(world, 0);
+    uint64_t total = 0;
+    for (uint32_t l = 0; l < nlist; ++l) total += sizes[l];
+    std::vector<uint32_t> order;
+    order.reserve(nlist);
+    for (uint32_t l = 0; l < nlist; ++l) {
+        // sizes[l] >= kStripeFactor * total / nlist, in integers
+        const bool stripe = striping && world > 1 && nlist > 0 && sizes[l] >= uint64_t(world) * kStripeMin &&
+                            (unsigned __int128)sizes[l] * nlist >= (unsigned __int128)kStripeFactor * total;
+        if (stripe) {
+            owner[l] = world;
+            for (uint32_t r = 0; r < world; ++r) load[r] += stripe_end(sizes[l], world, r) - stripe_begin(sizes[l], world, r);
+        } else {
+            order.push_back(l);
+        }
+    }
+    std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return sizes[a] > sizes[b]; });
     for (uint32_t l : order) {
         uint32_t best = 0;
         for (uint32_t r = 1; r < world; ++r)
             if (load[r] < load[best]) best = r;
         owner[l] = best;
         load[best] += sizes[l];
+    }
+}
+
+void plan_shard_ranges(const uint64_t* sizes, uint32_t nlist, uint32_t world, uint32_t rank, uint64_t* begin,
+                       uint64_t* end) {
+    std::vector<uint32_t> owner(nlist);
+    plan_shards_lpt(sizes, nlist, world, owner.data());
+    for (uint32_t l = 0; l < nlist; ++l) {
+        if (owner[l] == world) {
+            begin[l] = stripe_begin(sizes[l], world, rank);
+            end[l] = stripe_end(sizes[l], world, rank);
+        } else {
+            begin[l] = 0;
+            end[l] = owner[l] == rank ? sizes[l] : 0;
+        }
     }
 }
 

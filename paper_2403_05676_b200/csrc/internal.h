@@ -154,11 +154,24 @@ struct HostIndex {
     uint64_t ntotal_global = 0;
 };
 
-// Parses PRAGIX01 (annindex.hpp:361-411). keep(list) selects resident lists
-// (sharding); others are kept empty. Returns status, error text set.
-int read_pragix01(const std::string& path, HostIndex& out, const std::vector<uint8_t>* keep);
+// Parses PRAGIX01 (annindex.hpp:361-411). keep = {begin[nlist], end[nlist]}
+// selects each list's resident entry range (sharding; empty ranges are
+// skipped on disk). Returns status, error text set.
+struct KeepRanges {
+    std::vector<uint64_t> begin, end;
+};
+int read_pragix01(const std::string& path, HostIndex& out, const KeepRanges* keep);
 int read_pragix01_list_sizes(const std::string& path, std::vector<uint64_t>& sizes);
+// Shard placement (index_io.cpp): owner[l] = the rank holding list l whole,
+// or world when the list is striped over all ranks; plan_shard_ranges gives
+// rank's entry range [begin, end) of every list (empty when not resident).
 void plan_shards_lpt(const uint64_t* sizes, uint32_t nlist, uint32_t world, uint32_t* owner);
+void plan_shard_ranges(const uint64_t* sizes, uint32_t nlist, uint32_t world, uint32_t rank, uint64_t* begin,
+                       uint64_t* end);
+inline uint64_t stripe_begin(uint64_t len, uint32_t world, uint32_t r) {
+    return uint64_t((unsigned __int128)len * r / world);
+}
+inline uint64_t stripe_end(uint64_t len, uint32_t world, uint32_t r) { return stripe_begin(len, world, r + 1); }
 
 // ----------------------------------------------------------- device index
 constexpr uint32_t kListPad = 32;  // lists padded to a multiple of 32 entries

@@ -446,7 +446,8 @@ static int make_group(std::vector<prag_gpu_index*>& shards, prag_gpu_index** out
     return PRAG_GPU_OK;
 }
 
-// Splits a host index by LPT into n shards uploaded to devices[r], grouped.
+// Splits a host index into n shards (plan_shard_ranges: whole lists by LPT,
+// the largest striped) uploaded to devices[r], grouped.
 static int group_from_host(const HostIndex& h, const int* devices, int n, prag_gpu_index** out) {
     if (n > kMaxParts) {
         set_error("sharded index: at most " + std::to_string(kMaxParts) + " shards");
@@ -456,8 +457,7 @@ static int group_from_host(const HostIndex& h, const int* devices, int n, prag_g
     const uint32_t nl = h.nlist;
     std::vector<uint64_t> sizes(nl);
     for (uint32_t l = 0; l < nl; ++l) sizes[l] = h.list_off[l + 1] - h.list_off[l];
-    std::vector<uint32_t> owner(nl);
-    plan_shards_lpt(sizes.data(), nl, uint32_t(n), owner.data());
+    std::vector<uint64_t> rb(nl), re(nl);
     std::vector<prag_gpu_index*> shards;
     struct Free {
         std::vector<prag_gpu_index*>& v;
@@ -466,6 +466,7 @@ static int group_from_host(const HostIndex& h, const int* devices, int n, prag_g
         }
     } guard{shards};
     for (int r = 0; r < n; ++r) {
+        plan_shard_ranges(sizes.data(), nl, uint32_t(n), uint32_t(r), rb.data(), re.data());
         HostIndex hr;
         hr.nlist = h.nlist;
         hr.d = h.d;
@@ -476,11 +477,10 @@ static int group_from_host(const HostIndex& h, const int* devices, int n, prag_g
         hr.ntotal_global = h.ntotal_global ? h.ntotal_global : h.ids.size();
         hr.list_off.assign(size_t(nl) + 1, 0);
         for (uint32_t l = 0; l < nl; ++l) {
-            const uint64_t len = owner[l] == uint32_t(r) ? sizes[l] : 0;
+            const uint64_t b = h.list_off[l] + rb[l], len = re[l] - rb[l];  // whole list or a stripe
             if (len) {
-                hr.ids.insert(hr.ids.end(), h.ids.begin() + h.list_off[l], h.ids.begin() + h.list_off[l] + len);
-                hr.codes.insert(hr.codes.end(), h.codes.begin() + h.list_off[l] * h.nsq,
-                                h.codes.begin() + (h.list_off[l] + len) * h.nsq);
+                hr.ids.insert(hr.ids.end(), h.ids.begin() + b, h.ids.begin() + b + len);
+                hr.codes.insert(hr.codes.end(), h.codes.begin() + b * h.nsq, h.codes.begin() + (b + len) * h.nsq);
             }
             hr.list_off[l + 1] = hr.list_off[l] + len;
         }

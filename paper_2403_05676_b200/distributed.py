@@ -5,8 +5,9 @@ Inverted lists are independent and a candidate's distance depends only on
 top-k of the union of per-shard top-k lists, ordered by (distance, chunk_id)
 (annindex.hpp:54-60, :313). One process per GPU:
 
-  1. every rank holds the lists `prag_gpu_plan_shards` (greedy LPT on list
-     bytes) assigns it, plus replicated centroids and codebooks, so every rank
+  1. every rank holds the entry ranges `prag_gpu_plan_shard_ranges` assigns
+     it (whole lists by greedy LPT on list bytes; lists >= 4x the mean size
+     striped over all ranks), plus replicated centroids and codebooks, so every rank
      computes the identical probe set (annindex.hpp:277-281);
   2. each rank searches its shard (K1-K4) -> per-shard top-k;
   3. one ncclAllGather of each rank's top-k block, issued by libprag_gpu on
@@ -27,7 +28,7 @@ from typing import Callable, Optional
 
 import numpy as np
 
-from .ivfpq import BatchResult, GpuIndex, merge_topk, plan_shards
+from .ivfpq import BatchResult, GpuIndex, merge_topk, plan_shard_ranges, plan_shards
 
 try:
     import torch
@@ -171,18 +172,21 @@ def _read_pragix(path: str):
 
 
 def write_shard_pragix(src: str, dst: str, rank: int, world: int) -> np.ndarray:
-    """Writes the PRAGIX01 file of one shard: the lists plan_shards assigns to
-    `rank` (others empty), centroids and codebooks replicated. Returns the
-    owner array. Host-only (no GPU)."""
+    """Writes the PRAGIX01 file of one shard: the entry ranges
+    plan_shard_ranges gives `rank` (whole lists, or a stripe of a large one;
+    others empty), centroids and codebooks replicated. Returns the owner
+    array (`world` = striped). Host-only (no GPU)."""
     (ver, nlist, d, nsq), cent, words, lists = _read_pragix(src)
-    owner = plan_shards([len(l) for l in lists], world)
+    sizes = [len(l) for l in lists]
+    owner = plan_shards(sizes, world)
+    beg, end = plan_shard_ranges(sizes, world, rank)
     with open(dst, "wb") as f:
         f.write(b"PRAGIX01")
         f.write(struct.pack("<IIII", ver, nlist, d, nsq))
         f.write(cent.tobytes())
         f.write(words.tobytes())
-        for l, o in zip(lists, owner):
-            keep = l if int(o) == rank else l[:0]
+        for l, b, e in zip(lists, beg, end):
+            keep = l[int(b):int(e)]
             f.write(struct.pack("<Q", len(keep)))
             f.write(keep.tobytes())
     return owner

@@ -505,10 +505,20 @@ def recall_at_k(approx: SearchResult, exact: SearchResult) -> float:
 
 # ------------------------------------------------------------ multi-GPU
 def plan_shards(list_sizes: Sequence[int], world: int) -> np.ndarray:
+    """Owner rank of every list; `world` marks a list striped over all ranks."""
     s = np.ascontiguousarray(list_sizes, dtype=np.uint64)
     owner = np.zeros(len(s), dtype=np.uint32)
     check(lib().prag_gpu_plan_shards(_ptr(s), len(s), world, _ptr(owner)))
     return owner
+
+
+def plan_shard_ranges(list_sizes: Sequence[int], world: int, rank: int):
+    """(begin, end) entry range of every list on shard `rank` (whole lists or stripes)."""
+    s = np.ascontiguousarray(list_sizes, dtype=np.uint64)
+    b = np.zeros(len(s), dtype=np.uint64)
+    e = np.zeros(len(s), dtype=np.uint64)
+    check(lib().prag_gpu_plan_shard_ranges(_ptr(s), len(s), world, rank, _ptr(b), _ptr(e)))
+    return b, e
 
 
 def merge_topk(ids, dist, count, scanned, k: int, device: int = 0, stream=None, out=None):

@@ -41,26 +41,62 @@ def test_no_cpu_fallback_without_device(tmp_path):
                       np.zeros((1, 1), np.uint32), None, 1)
 
 
+def _plan_restated(sizes, world):
+    """Stripe rule + LPT, restated (index_io.cpp plan_shards_lpt)."""
+    sizes = [int(x) for x in sizes]
+    total, nl = sum(sizes), len(sizes)
+    owner = np.zeros(nl, np.uint32)
+    load = [0] * world
+    rest = []
+    for l, n in enumerate(sizes):
+        if world > 1 and n >= world * 1024 and n * nl >= 4 * total:
+            owner[l] = world
+            for r in range(world):
+                load[r] += n * (r + 1) // world - n * r // world
+        else:
+            rest.append(l)
+    for l in sorted(rest, key=lambda l: (-sizes[l], l)):
+        r = min(range(world), key=lambda i: (load[i], i))
+        owner[l] = r
+        load[r] += sizes[l]
+    return owner, load
+
+
 def test_plan_shards_lpt():
     rng = np.random.default_rng(0)
-    sizes = rng.integers(0, 5000, size=1000).astype(np.uint64)
-    for world in (1, 2, 4, 8):
-        owner = pg.plan_shards(sizes, world)
-        assert owner.max() < world
-        loads = np.bincount(owner, weights=sizes.astype(np.float64), minlength=world)
-        # LPT bound: max load <= mean + largest item
-        assert loads.max() <= sizes.sum() / world + sizes.max()
-        # restatement: descending size (stable), least-loaded shard (lowest rank on ties)
-        order = sorted(range(len(sizes)), key=lambda l: (-int(sizes[l]), l))
-        load = [0] * world
-        ref = np.zeros(len(sizes), np.uint32)
-        for l in order:
-            r = min(range(world), key=lambda i: (load[i], i))
-            ref[l] = r
-            load[r] += int(sizes[l])
-        np.testing.assert_array_equal(owner, ref)
+    flat = rng.integers(0, 5000, size=1000).astype(np.uint64)  # nothing to stripe
+    skew = np.minimum(rng.lognormal(7.0, 1.5, size=1000), 2e6).astype(np.uint64)
+    for sizes in (flat, skew):
+        for world in (1, 2, 4, 8):
+            owner = pg.plan_shards(sizes, world)
+            ref, load = _plan_restated(sizes, world)
+            np.testing.assert_array_equal(owner, ref)
+            whole = owner < world
+            if sizes is flat:
+                assert whole.all()
+            elif world > 1:
+                assert (~whole).any()  # the skewed sizes have lists to stripe
+            # balance bound: max load <= mean + largest whole list
+            biggest = int(sizes[whole].max()) if whole.any() else 0
+            assert max(load) <= sizes.sum() / world + biggest
+            # ranges: every entry of every list on exactly one rank
+            cover = np.zeros(len(sizes), np.uint64)
+            prev_end = np.zeros(len(sizes), np.uint64)
+            for r in range(world):
+                b, e = pg.plan_shard_ranges(sizes, world, r)
+                assert (b <= e).all() and (e <= sizes).all()
+                held = e > b
+                assert (held[whole] == (owner[whole] == r)).all()
+                st = ~whole
+                assert (b[st] == prev_end[st]).all()  # stripes are consecutive, in rank order
+                prev_end[st] = e[st]
+                cover += e - b
+                assert int((e - b).sum()) == load[r]
+            np.testing.assert_array_equal(cover, sizes)
     with pytest.raises(pg.ConfigError):
-        pg.plan_shards(sizes, 0)
+        pg.plan_shards(flat, 0)
+    with pytest.raises(pg.ConfigError):
+        pg.plan_shard_ranges(flat, 2, 2)
 
 
 def test_select_nprobe_kats():

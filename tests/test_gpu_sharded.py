@@ -222,3 +222,53 @@ def test_sharded_index_over_torch_distributed(fx):
         si.close()
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name", ["d384_m32", "d384_m64"])
+def test_striped_lists_equal_unsharded(tmp_path, name):
+    """Large lists striped over the shards (plan_shard_ranges): list 0 holds 4
+    copies of every entry (new ids, same codes), so it is striped at every
+    world here and its stripes hold exact distance ties with each other. The
+    group (load_sharded), shard handles (load_shard, read by entry range) and
+    the oracle on the unsharded file agree bit for bit."""
+    from test_multiproc_cpu import _skewed_pragix
+    src = os.path.join(HERE, "golden", name + ".pragix")
+    path = str(tmp_path / "skew.pragix")
+    sizes = _skewed_pragix(src, path)
+    q = np.load(os.path.join(HERE, "golden", name + ".npz"))["queries"]
+    full = pg.GpuIndex.load(path, 0)
+    oi = O.OracleIndex(path)
+    for world in (2, 3, 8):
+        assert pg.plan_shards(sizes, world)[0] == world
+        g = pg.GpuIndex.load_sharded(path, [0] * world)
+        assert (g.list_sizes() == full.list_sizes()).all()
+        h = pg.GpuIndex.group([pg.GpuIndex.load_shard(path, r, world, 0) for r in range(world)])
+        for nprobe, k in ((32, 10), (4, 32), (1, 10), (32, 100)):
+            ref = full.search_batch(q, k, nprobe)
+            _same(f"{name}/stripe{world}/p{nprobe}k{k}", g.search_batch(q, k, nprobe), ref)
+            _same(f"{name}/stripe{world}/shards/p{nprobe}k{k}", h.search_batch(q, k, nprobe), ref)
+        r = g.search_batch(q, 10, 32)
+        assert_same(f"{name}/stripe{world}/oracle", r.ids, r.dist, r.count, r.scanned, *oi.search(q, 32, 10))
+
+
+def test_synthetic_striped_shards_equal_full_synthetic():
+    """Synthetic shards with a heavy list-size skew: the largest lists are
+    striped (each stripe keeps its entries' global chunk ids and codes)."""
+    cents, words = _model(256, 384, 64, 11)
+    n, seed, sigma = 600_000, 21, 1.6
+    full = pg.GpuIndex.synthetic(cents, words, n, seed=seed, sigma=sigma)
+    sizes = full.list_sizes()
+    for world in (2, 4):
+        owner = pg.plan_shards(sizes, world)
+        assert (owner == world).sum() >= 3
+        shards = [pg.GpuIndex.synthetic_shard(cents, words, n, r, world, seed=seed, sigma=sigma) for r in range(world)]
+        for r, s in enumerate(shards):
+            b, e = pg.plan_shard_ranges(sizes, world, r)
+            assert (s.list_sizes() == e - b).all()
+        g = pg.GpuIndex.group(shards)
+        big = np.argsort(-sizes.astype(np.int64))[:8]  # queries at the largest lists' centroids
+        rng = np.random.default_rng(4)
+        q = (cents[np.concatenate([big, rng.integers(0, 256, 8)])] +
+             rng.standard_normal((16, 384)).astype(np.float32) * 0.3).astype(np.float32)
+        for nprobe, k in ((1, 10), (8, 32), (64, 10)):
+            _same(f"synth-stripe{world}/p{nprobe}k{k}", g.search_batch(q, k, nprobe), full.search_batch(q, k, nprobe))

@@ -69,14 +69,46 @@ def _worker(rank, world, port, path, shard_dir, q, nprobe, k, out_dir):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_gloo_sharded_search_equals_unsharded(golden, tmp_path, world):
+def _skewed_pragix(src, dst):
+    """d384_m32 with list 0 replaced by 4 copies of every entry (new chunk
+    ids, same codes): one list far above 4x the mean, so the shard plan
+    stripes it, and exact distance ties between entries of different stripes."""
+    import struct
+
+    from paper_2403_05676_b200 import distributed as D
+    (ver, nlist, d, nsq), cent, words, lists = D._read_pragix(src)
+    allent = np.concatenate(lists)
+    big = []
+    for c in range(4):
+        e = allent.copy()
+        e["id"] = e["id"] + np.uint64(10**6 * (c + 1))
+        big.append(e)
+    lists = [np.concatenate(big)] + list(lists[1:])
+    with open(dst, "wb") as f:
+        f.write(b"PRAGIX01")
+        f.write(struct.pack("<IIII", ver, nlist, d, nsq))
+        f.write(cent.tobytes())
+        f.write(words.tobytes())
+        for l in lists:
+            f.write(struct.pack("<Q", len(l)))
+            f.write(l.tobytes())
+    return [len(l) for l in lists]
+
+
+@pytest.mark.parametrize("world,skew", [(2, False), (3, False), (2, True), (3, True)])
+def test_gloo_sharded_search_equals_unsharded(golden, tmp_path, world, skew):
     import torch.multiprocessing as mp
 
     import _oracle as O
+    from paper_2403_05676_b200 import plan_shards
     path, z, grid = golden("d384_m32")
     q = z["queries"]
     nprobe, k = 8, 10
+    if skew:
+        path = str(tmp_path / "skew.pragix")
+        sizes = _skewed_pragix(golden("d384_m32")[0], path)
+        assert plan_shards(sizes, world)[0] == world  # list 0 is striped
+        nprobe = 32  # every list probed, list 0 included
     port = _free_port()
     mp.start_processes(_worker, args=(world, port, path, str(tmp_path), q, nprobe, k, str(tmp_path)),
                        nprocs=world, join=True, start_method="spawn")
@@ -91,29 +123,31 @@ def test_gloo_sharded_search_equals_unsharded(golden, tmp_path, world):
 
 
 def test_shard_files_partition_the_index(golden, tmp_path):
-    """Every list lands on exactly one shard; shard sizes follow the LPT plan."""
+    """Every entry lands on exactly one shard (whole lists by LPT, large lists
+    striped in rank order); shard sizes follow the plan."""
     from paper_2403_05676_b200 import distributed as D
     path, _, _ = golden("d384_m32")
     _, _, _, lists = D._read_pragix(path)
     sizes = np.array([len(l) for l in lists])
-    world = 3
-    seen = np.zeros(len(lists), dtype=int)
-    loads = []
-    for r in range(world):
-        sp = str(tmp_path / f"s{r}.pragix")
-        owner = D.write_shard_pragix(path, sp, r, world)
-        _, _, _, sl = D._read_pragix(sp)
-        got = np.array([len(l) for l in sl])
-        assert ((got > 0) <= (owner == r)).all()
-        seen += (owner == r)
-        loads.append(int(got.sum()))
-        for l, l2 in zip(lists, sl):
-            if len(l2):
-                assert (l2["id"] == l["id"]).all() and (l2["code"] == l["code"]).all()
-    assert (seen == 1).all()
-    assert sum(loads) == int(sizes.sum())
-    # LPT bound: max load <= mean + largest list
-    assert max(loads) <= sizes.sum() / world + sizes.max()
+    for world in (2, 3):
+        got_lists = [[] for _ in lists]
+        loads = []
+        for r in range(world):
+            sp = str(tmp_path / f"s{world}_{r}.pragix")
+            owner = D.write_shard_pragix(path, sp, r, world)
+            _, _, _, sl = D._read_pragix(sp)
+            got = np.array([len(l) for l in sl])
+            assert ((got > 0) <= ((owner == r) | (owner == world))).all()
+            loads.append(int(got.sum()))
+            for i, l2 in enumerate(sl):
+                got_lists[i].append(l2)
+        for l, parts in zip(lists, got_lists):  # the stripes concatenate to the list
+            cat = np.concatenate(parts)
+            assert len(cat) == len(l)
+            assert (cat["id"] == l["id"]).all() and (cat["code"] == l["code"]).all()
+        assert sum(loads) == int(sizes.sum())
+        whole = owner < world
+        assert max(loads) <= sizes.sum() / world + (sizes[whole].max() if whole.any() else 0)
 
 
 def test_pack_unpack_roundtrip():
