@@ -23,11 +23,14 @@ ap.add_argument("--n", type=int, default=10_000_000)
 ap.add_argument("--nlist", type=int, default=4096)
 ap.add_argument("--m", type=int, default=32)
 ap.add_argument("--reps", type=int, default=20)
+ap.add_argument("--seed", type=int, default=1)
+ap.add_argument("--coarse", type=int, default=0, help="prag_gpu_set_coarse_path: 0 auto (tensor cores), 1 exact SIMT")
 a = ap.parse_args()
 if a.small:
     a.n, a.nlist = 1_000_000, 1024
-path, q, meta = F.ensure_fixture(a.n, 384, a.nlist, a.m, 1, nq=64, log=lambda *x: print(*x, file=sys.stderr))
+path, q, meta = F.ensure_fixture(a.n, 384, a.nlist, a.m, a.seed, nq=64, log=lambda *x: print(*x, file=sys.stderr))
 ix = pg.GpuIndex.load(path, 0)
+ix.set_coarse_path(a.coarse)
 s = torch.cuda.Stream()
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 rows = []
@@ -68,7 +71,7 @@ for nq in (1, 16, 64):
                ("coarse_ms", "select_ms", "plan_ms", "scan_ms", "final_ms", "total_ms")}
         sb = statistics.median([p["scanned_bytes"] for p in ph])
         win = statistics.median([p["coarse_window"] for p in ph]) / nq
-        r = {"nq": nq, "nprobe": nprobe, "host_issue_ms": round(statistics.median(host), 4),
+        r = {"nq": nq, "nprobe": nprobe, "coarse_path": a.coarse, "host_issue_ms": round(statistics.median(host), 4),
              "event_ms": round(statistics.median(ev), 4), "phases": med, "scanned_MB": round(sb / 1e6, 2), "coarse_window_per_q": win,
              "scan_GBps": round(sb / (med["scan_ms"] / 1e3) / 1e9, 1) if med["scan_ms"] else None}
         rows.append(r)
