@@ -31,6 +31,7 @@
 // uses (8d + 256) * 2^-24 (~1.7x margin at d = 384), and the GPU parity suite
 // checks the observed |A - R| against it.
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 
 #include "internal.h"
@@ -270,7 +271,8 @@ __global__ void __launch_bounds__(128, 1) coarse_tc_kernel(const float* __restri
 }
 
 // ------------------------------------------------------------------ K1b
-constexpr uint32_t kWinThreads = 512;
+constexpr uint32_t kWinThreads = 512;      // K1b block size when nq is large
+constexpr uint32_t kWinThreadsMax = 1024;  // and its largest (SMEM reduction scratch is sized for it)
 constexpr uint32_t kWinCap = 1024;   // window slots (ids + exact distances in SMEM)
 constexpr uint32_t kStageRowsMax = 64;  // centroid rows staged per rescoring batch (fewer for large d)
 
@@ -281,7 +283,7 @@ __device__ __forceinline__ uint32_t fkey(float f) {
 
 // nprobe-th smallest of the CTA's keys (rank is 1-based; keys in registers,
 // VPT per thread, invalid slots hold 0xffffffff and are masked by `n`).
-template <uint32_t VPT, class K>
+template <uint32_t VPT, uint32_t NT, class K>
 __device__ K block_select_kth(const K (&key)[VPT], uint32_t n, uint32_t rank, uint32_t* hist, uint32_t* misc) {
     const uint32_t tid = threadIdx.x;
     K* sel = reinterpret_cast<K*>(misc + 2);  // selected prefix (misc[2..3])
@@ -292,12 +294,12 @@ __device__ K block_select_kth(const K (&key)[VPT], uint32_t n, uint32_t rank, ui
     }
     K mask = 0;
     for (int shift = int(sizeof(K)) * 8 - 8; shift >= 0; shift -= 8) {
-        for (uint32_t i = tid; i < 256; i += kWinThreads) hist[i] = 0;
+        for (uint32_t i = tid; i < 256; i += NT) hist[i] = 0;
         __syncthreads();
         const K prefix = *sel;
 #pragma unroll
         for (uint32_t i = 0; i < VPT; ++i) {
-            const bool act = (key[i] & mask) == prefix && i * kWinThreads + tid < n;
+            const bool act = (key[i] & mask) == prefix && i * NT + tid < n;
             const uint32_t bucket = uint32_t(key[i] >> shift) & 255u;
             const unsigned am = __ballot_sync(0xffffffffu, act);
             if (act) {
@@ -344,14 +346,14 @@ __device__ K block_select_kth(const K (&key)[VPT], uint32_t n, uint32_t rank, ui
 
 // Appends every list c < n with pred(c) to win[] (order arbitrary); returns
 // the count (may exceed kWinCap: only the first kWinCap are stored).
-template <class Pred>
+template <uint32_t NT, class Pred>
 __device__ uint32_t block_collect(uint32_t n, Pred pred, uint32_t* win, uint32_t* counter) {
     const uint32_t tid = threadIdx.x;
     __syncthreads();
     if (tid == 0) *counter = 0;
     __syncthreads();
-    const uint32_t span = (n + kWinThreads - 1) / kWinThreads * kWinThreads;
-    for (uint32_t c = tid; c < span; c += kWinThreads) {
+    const uint32_t span = (n + NT - 1) / NT * NT;
+    for (uint32_t c = tid; c < span; c += NT) {
         const bool in = c < n && pred(c);
         const unsigned bal = __ballot_sync(0xffffffffu, in);
         uint32_t base = 0;
@@ -370,7 +372,7 @@ __device__ uint32_t block_collect(uint32_t n, Pred pred, uint32_t* win, uint32_t
 // every list into the query's scratch row, then selection on the unique
 // (distance, list id) keys. Kept out of line: it never runs on well-posed
 // inputs and would otherwise bloat the hot kernel's instruction footprint.
-template <uint32_t VPT>
+template <uint32_t VPT, uint32_t NT>
 __device__ __noinline__ uint32_t exact_fallback(float* upq, const float* __restrict__ centroids, const float* sq,
                                                 uint32_t nlist, uint32_t d, uint32_t nprobe, uint32_t* hist,
                                                 uint32_t* misc, uint32_t* win, float* wd) {
@@ -378,7 +380,7 @@ __device__ __noinline__ uint32_t exact_fallback(float* upq, const float* __restr
     uint32_t W;
         // fallback: exact distance of every list into this query's scratch row
     __syncthreads();
-    for (uint32_t c = tid; c < nlist; c += kWinThreads) {
+    for (uint32_t c = tid; c < nlist; c += NT) {
         const float* row = centroids + size_t(c) * d;
         float acc = 0.0f;
 #pragma unroll 8
@@ -394,13 +396,13 @@ __device__ __noinline__ uint32_t exact_fallback(float* upq, const float* __restr
     uint64_t key64[VPT];
 #pragma unroll
     for (uint32_t i = 0; i < VPT; ++i) {
-        const uint32_t c = i * kWinThreads + tid;
+        const uint32_t c = i * NT + tid;
         key64[i] = c < nlist ? (uint64_t(fkey(upq[c])) << 32 | c) : ~0ull;
     }
-    const uint64_t tkey = block_select_kth<VPT>(key64, nlist, nprobe, hist, misc);
-    W = block_collect(nlist, [&](uint32_t c) { return (uint64_t(fkey(upq[c])) << 32 | c) <= tkey; }, win,
+    const uint64_t tkey = block_select_kth<VPT, NT>(key64, nlist, nprobe, hist, misc);
+    W = block_collect<NT>(nlist, [&](uint32_t c) { return (uint64_t(fkey(upq[c])) << 32 | c) <= tkey; }, win,
                       misc + 4);
-    for (uint32_t i = tid; i < W; i += kWinThreads) wd[i] = upq[win[i]];
+    for (uint32_t i = tid; i < W; i += NT) wd[i] = upq[win[i]];
         return W;
 }
 
@@ -409,8 +411,8 @@ __device__ __noinline__ uint32_t exact_fallback(float* upq, const float* __restr
 // exactly and ranked. If the window exceeds kWinCap (not seen in practice:
 // windows are nprobe + a few) the CTA falls back to the
 // exact distance of every list and selects on the unique (distance, id) keys.
-template <uint32_t VPT>  // lists per thread: nlist <= VPT * 512
-__global__ void __launch_bounds__(kWinThreads) select_window_kernel(
+template <uint32_t VPT, uint32_t NT>  // lists per thread, threads: nlist <= VPT * NT
+__global__ void __launch_bounds__(NT) select_window_kernel(
     float* __restrict__ partial, uint32_t nslices, const float* __restrict__ cent_norm, float bound_c,
     const float* __restrict__ centroids, const float* __restrict__ queries, uint32_t nq, uint32_t nlist, uint32_t d,
     uint32_t nprobe, uint32_t* __restrict__ probe, float* __restrict__ probe_dist,
@@ -427,21 +429,21 @@ __global__ void __launch_bounds__(kWinThreads) select_window_kernel(
     float* wd = reinterpret_cast<float*>(win + kWinCap);       // [kWinCap] exact distances
     float* sq = wd + kWinCap;                                  // [d] the query
     float* rows = sq + ((d + 3) & ~3u);                        // [2][kStageRows][d + 1] (kStageRows: launch arg)
-    float* red = rows + 2 * kStageRows * (d + 1);              // [kWinThreads / 32] reduction scratch
+    float* red = rows + 2 * kStageRows * (d + 1);              // [NT / 32] reduction scratch
 
     const uint32_t q = blockIdx.x, tid = threadIdx.x;
     // ||c||^2 is index data: load it before waiting on the previous kernel
     float cnv[VPT];
 #pragma unroll
     for (uint32_t i = 0; i < VPT; ++i) {
-        const uint32_t c = i * kWinThreads + tid;
+        const uint32_t c = i * NT + tid;
         cnv[i] = c < nlist ? __ldg(cent_norm + c) : 0.0f;
     }
     // ||q||^2 (any order: it only enters the approximate A and the bound E).
     // The queries were written before K1 started, so they are read before
     // waiting on K1.
     float part = 0.0f;
-    for (uint32_t j = tid; j < d; j += kWinThreads) {
+    for (uint32_t j = tid; j < d; j += NT) {
         const float x = queries[size_t(q) * d + j];
         sq[j] = x;
         part = __fadd_rn(part, __fmul_rn(x, x));  // no FFMA anywhere in this kernel (SASS guard)
@@ -464,7 +466,7 @@ __global__ void __launch_bounds__(kWinThreads) select_window_kernel(
             const float* pz = partial + (size_t(z0 + zz) * nq + q) * nlist;
 #pragma unroll
             for (uint32_t i = 0; i < VPT; ++i) {
-                const uint32_t c = i * kWinThreads + tid;
+                const uint32_t c = i * NT + tid;
                 pv[zz][i] = (z0 + zz < nslices && c < nlist) ? pz[c] : 0.0f;
             }
         }
@@ -477,13 +479,13 @@ __global__ void __launch_bounds__(kWinThreads) select_window_kernel(
     }
     __syncthreads();
     float qn = 0.0f;
-    for (uint32_t w = 0; w < kWinThreads / 32; ++w) qn += red[w];
+    for (uint32_t w = 0; w < NT / 32; ++w) qn += red[w];
     // A = ||q||^2 + ||c||^2 - 2 q.c; keys of A + E, and A - E
     uint32_t key[VPT];
     float lov[VPT];
 #pragma unroll
     for (uint32_t i = 0; i < VPT; ++i) {
-        const uint32_t c = i * kWinThreads + tid;
+        const uint32_t c = i * NT + tid;
         key[i] = 0xffffffffu;
         lov[i] = 0.0f;
         if (c < nlist) {
@@ -513,9 +515,9 @@ __global__ void __launch_bounds__(kWinThreads) select_window_kernel(
             // nprobe-th smallest group minimum is itself >= U (an order
             // statistic of a subset), found by one warp ranking <= 32 values
             uint32_t sz = 32;
-            while (sz > 1 && kWinThreads / (sz / 2) <= 32 && kWinThreads / sz < nprobe) sz >>= 1;
-            // (kWinThreads / sz groups; sz = 32 gives 16 groups)
-            const uint32_t G = kWinThreads / sz;
+            while (sz > 1 && NT / (sz / 2) <= 32 && NT / sz < nprobe) sz >>= 1;
+            // (NT / sz groups; sz = 32 gives 16 groups)
+            const uint32_t G = NT / sz;
             uint32_t gm = kmin[0];
             for (uint32_t o = 1; o < sz; o <<= 1) gm = min(gm, __shfl_xor_sync(0xffffffffu, gm, o));
             if ((tid & (sz - 1)) == 0) hist[tid / sz] = gm;  // hist[] is free until the radix fallback
@@ -534,7 +536,7 @@ __global__ void __launch_bounds__(kWinThreads) select_window_kernel(
             __syncthreads();
             ub = misc[7];
         } else {
-            ub = block_select_kth<1>(kmin, kWinThreads, nprobe, hist, misc);
+            ub = block_select_kth<1, NT>(kmin, NT, nprobe, hist, misc);
         }
         uint32_t* cand = reinterpret_cast<uint32_t*>(wd);  // scratch until the window is rescored
         if (tid == 0) misc[5] = 0;
@@ -554,7 +556,7 @@ __global__ void __launch_bounds__(kWinThreads) select_window_kernel(
         __syncthreads();
         const uint32_t nc = misc[5];
         if (nc <= kWinCap) {
-            for (uint32_t i = tid; i < nc; i += kWinThreads) {
+            for (uint32_t i = tid; i < nc; i += NT) {
                 const uint32_t ki = cand[i];
                 uint32_t less = 0, eq = 0;
                 for (uint32_t j = 0; j < nc; ++j) {
@@ -567,10 +569,10 @@ __global__ void __launch_bounds__(kWinThreads) select_window_kernel(
             __syncthreads();
             ukey = misc[6];
         } else {
-            ukey = block_select_kth<VPT>(key, nlist, nprobe, hist, misc);
+            ukey = block_select_kth<VPT, NT>(key, nlist, nprobe, hist, misc);
         }
     } else {
-        ukey = block_select_kth<VPT>(key, nlist, nprobe, hist, misc);
+        ukey = block_select_kth<VPT, NT>(key, nlist, nprobe, hist, misc);
     }
     CT_MARK(9);
     // window: lists whose lower bound A - E does not exceed U
@@ -582,7 +584,7 @@ __global__ void __launch_bounds__(kWinThreads) select_window_kernel(
         __syncthreads();
 #pragma unroll
         for (uint32_t i = 0; i < VPT; ++i) {
-            const uint32_t c = i * kWinThreads + tid;
+            const uint32_t c = i * NT + tid;
             const bool in = c < nlist && fkey(lov[i]) <= ukey;
             const unsigned bal = __ballot_sync(0xffffffffu, in);
             uint32_t base = 0;
@@ -608,7 +610,7 @@ __global__ void __launch_bounds__(kWinThreads) select_window_kernel(
             const uint32_t nb = min(kStageRows, W - b0);
             float* dst = rows + buf * kStageRows * rs;
             // warp w stages rows w, w + 16, ...; lanes stride the row (no division)
-            for (uint32_t r = tid >> 5; r < nb; r += kWinThreads / 32) {
+            for (uint32_t r = tid >> 5; r < nb; r += NT / 32) {
                 const float* src = centroids + size_t(win[b0 + r]) * d;
                 const uint32_t drow = smem_addr(dst + r * rs);
                 for (uint32_t j = tid & 31u; j < d; j += 32)
@@ -640,12 +642,12 @@ __global__ void __launch_bounds__(kWinThreads) select_window_kernel(
             __syncthreads();  // batch buffer free for the prefetch two batches on
         }
     } else {
-        W = exact_fallback<VPT>(upq, centroids, sq, nlist, d, nprobe, hist, misc, win, wd);
+        W = exact_fallback<VPT, NT>(upq, centroids, sq, nlist, d, nprobe, hist, misc, win, wd);
     }
     __syncthreads();
     CT_MARK(11);
     // rank by (distance, list id) (annindex.hpp:281 std::sort of pairs)
-    for (uint32_t i = tid; i < W; i += kWinThreads) {
+    for (uint32_t i = tid; i < W; i += NT) {
         const float di = wd[i];
         const uint32_t ci = win[i];
         uint32_t r = 0;
@@ -670,7 +672,7 @@ CT_BIND_FN(ct_bind_coarse)
 // rows per rescoring batch: up to kStageRowsMax while the double-buffered
 // staging fits the 227 KiB opt-in (more rows fold in parallel for large nprobe)
 static uint32_t window_stage_rows(uint32_t d) {
-    const size_t fixed = (256 + 8 + 2 * kWinCap) * 4 + ((d + 3) & ~3u) * 4 + (kWinThreads / 32) * 4;
+    const size_t fixed = (256 + 8 + 2 * kWinCap) * 4 + ((d + 3) & ~3u) * 4 + (kWinThreadsMax / 32) * 4;
     const size_t per_row = 2 * size_t(d + 1) * 4;
     const size_t fit = fixed < 227 * 1024 ? (227 * 1024 - fixed) / per_row : 0;
     return uint32_t(std::min<size_t>(kStageRowsMax, fit));
@@ -679,7 +681,7 @@ static uint32_t window_stage_rows(uint32_t d) {
 size_t tc_window_smem(uint32_t d) {
     const uint32_t rows = std::max<uint32_t>(window_stage_rows(d), 8);
     return (256 + 8 + 2 * kWinCap) * 4 + ((d + 3) & ~3u) * 4 + 2 * size_t(rows) * (d + 1) * 4 +
-           (kWinThreads / 32) * 4;
+           (kWinThreadsMax / 32) * 4;
 }
 
 bool tc_coarse_supported(uint32_t nlist, uint32_t d) {
@@ -739,29 +741,47 @@ int launch_coarse_tc(const DeviceIndex& ix, const float* queries, uint32_t nq, f
     return PRAG_GPU_OK;
 }
 
+// K1b block size for this shape (see launch_select_window).
+static uint32_t k1b_threads(uint32_t nlist, uint32_t nq) {
+    (void)nq;
+    return nlist > 2 * kWinThreads ? kWinThreadsMax : kWinThreads;
+}
+
 int launch_select_window(const DeviceIndex& ix, float* partial, const float* queries, uint32_t nq, uint32_t nprobe,
                          uint32_t* probe, float* probe_dist, unsigned long long* win_stat, cudaStream_t s) {
     const size_t smem = tc_window_smem(ix.d);
-#define PG_WIN(V)                                                                                              \
+#define PG_WIN(V, T)                                                                                           \
     do {                                                                                                       \
-        PG_CUDA(ensure_smem(reinterpret_cast<const void*>(select_window_kernel<V>), \
-                                     int(smem)));                                                              \
-        PG_CUDA(launch_pdl(select_window_kernel<V>, dim3(nq), dim3(kWinThreads), smem, s, partial,           \
-                           tc_slices(ix.d), ix.cent_norm, tc_bound_c(ix.d), ix.centroids, queries, nq, ix.nlist, \
-                           ix.d, nprobe, probe, probe_dist, win_stat,                                           \
-                           std::max<uint32_t>(window_stage_rows(ix.d), 8)));                                    \
+        PG_CUDA(ensure_smem(reinterpret_cast<const void*>(select_window_kernel<V, T>), int(smem)));             \
+        PG_CUDA(launch_pdl(select_window_kernel<V, T>, dim3(nq), dim3(T), smem, s, partial, tc_slices(ix.d),     \
+                           ix.cent_norm, tc_bound_c(ix.d), ix.centroids, queries, nq, ix.nlist, ix.d, nprobe, probe, \
+                           probe_dist, win_stat, std::max<uint32_t>(window_stage_rows(ix.d), 8)));              \
     } while (0)
-    const uint32_t vpt = (ix.nlist + kWinThreads - 1) / kWinThreads;
-    if (vpt <= 2)
-        PG_WIN(2);
+    // Block size: the per-query CTA's phases (slice sums, U, window, ranking)
+    // are latency chains over VPT keys per thread, so fewer keys per thread
+    // shortens them. PRAG_GPU_K1B_THREADS (512 / 1024) overrides (A/B knob).
+    const char* te = getenv("PRAG_GPU_K1B_THREADS");
+    const uint32_t nt = te ? (atoi(te) >= 1024 ? 1024u : 512u) : k1b_threads(ix.nlist, nq);
+    const uint32_t vpt = (ix.nlist + nt - 1) / nt;
+    if (nt == 1024) {
+        if (vpt <= 2)
+            PG_WIN(2, 1024);
+        else if (vpt <= 4)
+            PG_WIN(4, 1024);
+        else if (vpt <= 8)
+            PG_WIN(8, 1024);
+        else
+            PG_WIN(16, 1024);
+    } else if (vpt <= 2)
+        PG_WIN(2, 512);
     else if (vpt <= 4)
-        PG_WIN(4);
+        PG_WIN(4, 512);
     else if (vpt <= 8)
-        PG_WIN(8);
+        PG_WIN(8, 512);
     else if (vpt <= 16)
-        PG_WIN(16);
+        PG_WIN(16, 512);
     else
-        PG_WIN(32);
+        PG_WIN(32, 512);
 #undef PG_WIN
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {

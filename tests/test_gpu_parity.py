@@ -234,10 +234,13 @@ def _probe_both(ix, q, nprobe):
     return a, b
 
 
+@pytest.mark.parametrize("threads", ["512", "1024"])
 @pytest.mark.parametrize("nsq", [32, 64])
-def test_tc_coarse_probe_lists_exact(synth, nsq):
+def test_tc_coarse_probe_lists_exact(synth, nsq, threads, monkeypatch):
     """K1 tcgen05 pre-filter + exact window rescoring == exact SIMT coarse ==
-    the oracle's sequential squared_l2 order (annindex.hpp:277-281)."""
+    the oracle's sequential squared_l2 order (annindex.hpp:277-281), with
+    K1b at both block sizes."""
+    monkeypatch.setenv("PRAG_GPU_K1B_THREADS", threads)
     p, q = synth[nsq]
     ix = pg.GpuIndex.load(p, 0)
     oi = O.OracleIndex(p)
@@ -273,8 +276,14 @@ def _adversarial_index(tmp_path, nlist=256, d=64, nsq=16, dup=8, seed=3):
     return p, q
 
 
-def test_tc_coarse_adversarial_ties(gpu, tmp_path):
-    p, q = _adversarial_index(tmp_path)
+@pytest.mark.parametrize("nlist,threads", [(256, None), (256, "1024"), (4096, "512"), (4096, "1024"),
+                                           (16384, "512"), (16384, "1024")])
+def test_tc_coarse_adversarial_ties(gpu, tmp_path, nlist, threads, monkeypatch):
+    """Also at the benchmarked list counts, where K1b holds 4-32 keys per
+    thread (every select_window_kernel<VPT, threads> instantiation in use)."""
+    if threads:
+        monkeypatch.setenv("PRAG_GPU_K1B_THREADS", threads)
+    p, q = _adversarial_index(tmp_path, nlist=nlist)
     ix = pg.GpuIndex.load(p, gpu)
     oi = O.OracleIndex(p)
     for nprobe in (1, 3, 4, 5, 17, 128, 256):

@@ -28,10 +28,11 @@ ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--n", type=int, default=10_000_000)
 ap.add_argument("--nlist", type=int, default=4096)
 ap.add_argument("--m", type=int, default=32)
+ap.add_argument("--seed", type=int, default=1)
 ap.add_argument("--flush", default="write", choices=["write", "read", "none"],
                 help="L2 flush before each search: memset (bench.py's), a read sweep (clean lines), or none")
 a = ap.parse_args()
-path, q, _ = F.ensure_fixture(a.n, 384, a.nlist, a.m, 1, nq=64, log=lambda *x: None)
+path, q, _ = F.ensure_fixture(a.n, 384, a.nlist, a.m, a.seed, nq=64, log=lambda *x: None)
 ix = pg.GpuIndex.load(path, 0)
 qd = torch.from_numpy(q[:a.nq].copy()).cuda()
 f = lib().prag_gpu_debug_chain_trace
