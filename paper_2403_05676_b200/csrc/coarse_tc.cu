@@ -131,9 +131,9 @@ __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__flo
 
 // K1. Grid (nlist / 128, ceil(nq / N), ceil(d / 96)); 128 threads. A CTA
 // owns 128 centroids x N queries x one 96-wide K slice (3 blocks of 32), so
-// nlist = 4096, d = 384 runs 128 CTAs. The pre-split centroid blocks
-// (cent_tc, 32 KiB each) are bulk-copied on one mbarrier before waiting on
-// the previous kernel; the query rows of the slice are read by all threads
+// nlist = 4096, d = 384 runs 128 CTAs. The centroid blocks (cent_tc, 16 KiB
+// of fp32 each, split into hi | lo in SMEM after they land) are bulk-copied
+// on one mbarrier before waiting on the previous kernel; the query rows of the slice are read by all threads
 // (one float4 per lane, four rows in flight per warp) and split hi/lo straight
 // into the core-matrix layout; 36 MMAs are issued by one thread, and the
 // partial dot products go out as partial[slice][q][c] (summed, with the norms
@@ -168,10 +168,13 @@ __global__ void __launch_bounds__(128, 1) coarse_tc_kernel(const float* __restri
         bar_init(bars, 1);
         bar_init(bars + 1, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        bar_expect_tx(bars, nkb * kA);
-        // index data: it does not depend on the previous kernel
+        bar_expect_tx(bars, nkb * (kA / 2));
+        // index data: it does not depend on the previous kernel. Only the fp32
+        // centroids travel (half the bytes of a pre-split hi | lo copy); they
+        // land in the hi slot and are split in SMEM below.
         for (uint32_t i = 0; i < nkb; ++i)
-            bulk_load(sA + i * kA, cent_tc + (size_t(tile) * nkb_all + kb0 + i) * (2 * kTcRows * kTcKBlock), kA, bars);
+            bulk_load(sA + i * kA, cent_tc + (size_t(tile) * nkb_all + kb0 + i) * (kTcRows * kTcKBlock), kA / 2,
+                      bars);
     }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(tmem_slot)),
@@ -212,6 +215,21 @@ __global__ void __launch_bounds__(128, 1) coarse_tc_kernel(const float* __restri
                 *reinterpret_cast<float4*>(b + off) = hi;
                 *reinterpret_cast<float4*>(b + kBp + off) = lo;
             }
+        }
+    }
+    __syncthreads();  // the barriers' init is visible to every thread
+    // A: split the staged centroids x into hi = x with the low 13 mantissa
+    // bits cleared and lo = x - hi (exact), element-wise in place: the same
+    // operands the round-1 host-side pre-split produced
+    bar_wait(bars, 0);
+    for (uint32_t i = 0; i < nkb; ++i) {
+        float4* hp = reinterpret_cast<float4*>(sA + i * kA);
+        float4* lp = reinterpret_cast<float4*>(sA + i * kA + kA / 2);
+        for (uint32_t e = tid; e < kTcRows * kTcKBlock / 4; e += 128) {
+            const float4 x = hp[e];
+            const float4 hi = make_float4(tf32_hi(x.x), tf32_hi(x.y), tf32_hi(x.z), tf32_hi(x.w));
+            hp[e] = hi;
+            lp[e] = make_float4(__fsub_rn(x.x, hi.x), __fsub_rn(x.y, hi.y), __fsub_rn(x.z, hi.z), __fsub_rn(x.w, hi.w));
         }
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic STS -> tensor-core reads
@@ -692,13 +710,14 @@ bool tc_coarse_supported(uint32_t nlist, uint32_t d) {
 
 float tc_bound_c(uint32_t d) { return float((8.0 * d + 256.0) * 0x1p-24); }
 
-// Host-side pre-split of the centroids for K1's A operand: per 128-row tile
-// and 32-element K block, [hi | lo] parts, each [k chunk 8][row group 16][8
-// rows][4] (the no-swizzle K-major core-matrix layout).
+// K1's A operand, host-side: the fp32 centroids per 128-row tile and
+// 32-element K block in [k chunk 8][row group 16][8 rows][4] order (the
+// no-swizzle K-major core-matrix layout); K1 splits each staged block into
+// its hi and lo parts in SMEM.
 void build_tc_centroids(const float* cent, uint32_t nlist, uint32_t d, std::vector<float>& out,
                         std::vector<float>& norms) {
     const uint32_t tiles = nlist / kTcRows, nkb = d / kTcKBlock;
-    out.assign(size_t(nlist) * d * 2, 0.0f);
+    out.assign(size_t(nlist) * d, 0.0f);
     norms.resize(nlist);
     for (uint32_t c = 0; c < nlist; ++c) {
         double s = 0.0;
@@ -707,18 +726,11 @@ void build_tc_centroids(const float* cent, uint32_t nlist, uint32_t d, std::vect
     }
     for (uint32_t t = 0; t < tiles; ++t)
         for (uint32_t kb = 0; kb < nkb; ++kb) {
-            float* blk = out.data() + (size_t(t) * nkb + kb) * (2 * kTcRows * kTcKBlock);
+            float* blk = out.data() + (size_t(t) * nkb + kb) * (kTcRows * kTcKBlock);
             for (uint32_t r = 0; r < kTcRows; ++r)
                 for (uint32_t k = 0; k < kTcKBlock; ++k) {
-                    const float x = cent[size_t(t * kTcRows + r) * d + kb * kTcKBlock + k];
-                    uint32_t u;
-                    std::memcpy(&u, &x, 4);
-                    u &= 0xffffe000u;
-                    float hi;
-                    std::memcpy(&hi, &u, 4);
                     const size_t off = size_t(k >> 2) * (kTcRows * 4) + (r >> 3) * 32 + (r & 7) * 4 + (k & 3);
-                    blk[off] = hi;
-                    blk[kTcRows * kTcKBlock + off] = x - hi;
+                    blk[off] = cent[size_t(t * kTcRows + r) * d + kb * kTcKBlock + k];
                 }
         }
 }

@@ -193,7 +193,7 @@ struct DeviceIndex {
     float* codewords = nullptr;   // [nsq][256][sub_dim] (LUT-image kernel)
     uint64_t* skew_off = nullptr; // [nlist+1] tile offsets into skew_codes
     uint8_t* skew_codes = nullptr;
-    float* cent_tc = nullptr;     // K1 A operand: centroids pre-split hi/lo in UMMA core-matrix order
+    float* cent_tc = nullptr;     // K1 A operand: fp32 centroids in UMMA core-matrix order (split hi/lo in SMEM)
     float* cent_norm = nullptr;   // [nlist] ||c||^2
     bool tc_ok = false;           // tensor-core coarse quantizer usable for this shape
     bool plain_codes = true;      // codes[] present (generic path); false for device-built synthetic indexes
