@@ -621,13 +621,16 @@ __global__ void __launch_bounds__(NT) select_window_kernel(
     const uint32_t rs = d + 1;
     if (W <= kWinCap) {
         // exact rescoring (common.hpp:73-80 via annindex.hpp:279): rows staged
-        // in SMEM (stride d + 1: conflict-free) by cp.async, two batches of
-        // kStageRows in flight (batch b+1 loads while batch b is folded); one
-        // thread folds one list
+        // in SMEM (stride d + 1: conflict-free) by cp.async; one thread folds
+        // one list. A window that fits both staging buffers is staged and
+        // folded as ONE batch (one fold chain instead of two in sequence);
+        // larger ones go in batches of kStageRows, batch b+1 loading while
+        // batch b is folded
+        const uint32_t SB = W <= 2 * kStageRows ? 2 * kStageRows : kStageRows;
         auto stage_batch = [&](uint32_t b0, uint32_t buf) {
-            const uint32_t nb = min(kStageRows, W - b0);
+            const uint32_t nb = min(SB, W - b0);
             float* dst = rows + buf * kStageRows * rs;
-            // warp w stages rows w, w + 16, ...; lanes stride the row (no division)
+            // warp w stages rows w, w + NT / 32, ...; lanes stride the row (no division)
             for (uint32_t r = tid >> 5; r < nb; r += NT / 32) {
                 const float* src = centroids + size_t(win[b0 + r]) * d;
                 const uint32_t drow = smem_addr(dst + r * rs);
@@ -638,10 +641,10 @@ __global__ void __launch_bounds__(NT) select_window_kernel(
             asm volatile("cp.async.commit_group;" ::: "memory");
         };
         if (W) stage_batch(0, 0);
-        for (uint32_t b0 = 0, buf = 0; b0 < W; b0 += kStageRows, buf ^= 1u) {
-            const uint32_t nb = min(kStageRows, W - b0);
-            if (b0 + kStageRows < W) {
-                stage_batch(b0 + kStageRows, buf ^ 1u);
+        for (uint32_t b0 = 0, buf = 0; b0 < W; b0 += SB, buf ^= 1u) {
+            const uint32_t nb = min(SB, W - b0);
+            if (b0 + SB < W) {  // (SB = kStageRows here: two buffers in turn)
+                stage_batch(b0 + SB, buf ^ 1u);
                 asm volatile("cp.async.wait_group 1;" ::: "memory");
             } else {
                 asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -664,18 +667,23 @@ __global__ void __launch_bounds__(NT) select_window_kernel(
     }
     __syncthreads();
     CT_MARK(11);
-    // rank by (distance, list id) (annindex.hpp:281 std::sort of pairs)
-    for (uint32_t i = tid; i < W; i += NT) {
-        const float di = wd[i];
-        const uint32_t ci = win[i];
-        uint32_t r = 0;
-        for (uint32_t j = 0; j < W; ++j) {
-            const float dj = wd[j];
-            r += (dj < di) || (dj == di && win[j] < ci);
-        }
-        if (r < nprobe) {
-            probe[size_t(q) * nprobe + r] = ci;
-            probe_dist[size_t(q) * nprobe + r] = di;
+    // rank by (distance, list id) (annindex.hpp:281 std::sort of pairs): one
+    // warp per window list, its lanes counting the lists ordered before it
+    {
+        const uint32_t lane = tid & 31u;
+        for (uint32_t i = tid >> 5; i < W; i += NT / 32) {
+            const float di = wd[i];
+            const uint32_t ci = win[i];
+            uint32_t r = 0;
+            for (uint32_t j = lane; j < W; j += 32) {
+                const float dj = wd[j];
+                r += (dj < di) || (dj == di && win[j] < ci);
+            }
+            r = __reduce_add_sync(0xffffffffu, r);
+            if (lane == 0 && r < nprobe) {
+                probe[size_t(q) * nprobe + r] = ci;
+                probe_dist[size_t(q) * nprobe + r] = di;
+            }
         }
     }
     CT_END(1);
