@@ -553,30 +553,6 @@ __global__ void __launch_bounds__(NT) select_window_kernel(
             }
             __syncthreads();
             ub = misc[7];
-        } else if (nprobe <= 128) {
-            // the same bound with 32 < G <= 128 groups (G >= nprobe), the
-            // group minima ranked by G threads against each other in SMEM
-            // (a 4-pass radix select over all per-thread minima took ~4.4 us
-            // at nprobe 64, r4h_chain_trace.jsonl)
-            uint32_t sz = 32;
-            while (sz > 1 && NT / sz < nprobe) sz >>= 1;
-            const uint32_t G = NT / sz;
-            uint32_t gm = kmin[0];
-            for (uint32_t o = 1; o < sz; o <<= 1) gm = min(gm, __shfl_xor_sync(0xffffffffu, gm, o));
-            if ((tid & (sz - 1)) == 0) hist[tid / sz] = gm;  // G <= 128 <= 256 slots
-            __syncthreads();
-            if (tid < G) {
-                const uint32_t v = hist[tid];
-                uint32_t less = 0, eq = 0;
-                for (uint32_t j = 0; j < G; ++j) {
-                    const uint32_t x = hist[j];
-                    less += x < v;
-                    eq += x == v;
-                }
-                if (less < nprobe && nprobe <= less + eq) misc[7] = v;
-            }
-            __syncthreads();
-            ub = misc[7];
         } else {
             ub = block_select_kth<1, NT>(kmin, NT, nprobe, hist, misc);
         }
