@@ -244,7 +244,9 @@ def test_tc_coarse_probe_lists_exact(synth, nsq, threads, monkeypatch):
     p, q = synth[nsq]
     ix = pg.GpuIndex.load(p, 0)
     oi = O.OracleIndex(p)
-    for nprobe in (1, 2, 16, 64, 200, 256):
+    # 120-129: K1b windows on both sides of the one-batch rescoring limit
+    # (2 x 64 staged rows at d = 384)
+    for nprobe in (1, 2, 16, 64, 120, 124, 126, 127, 128, 129, 200, 256):
         (tl, td), (el, ed) = _probe_both(ix, q, nprobe)
         assert (tl == el).all(), f"nprobe={nprobe}: TC probe lists differ from exact"
         assert (td.view(np.uint32) == ed.view(np.uint32)).all()
